@@ -1,0 +1,418 @@
+#!/usr/bin/env python3
+"""Benchmark of the FSDP2 Shard(0) hot path (BASELINE.json metric: "FSDP unshard+reshard
+GB/s per layer (fraction of NVLink/HBM peak) at 1/2/4/8 B200").
+
+One step = one pass of the whole hot path over the Llama 3.1 8B parameter layout
+(BASELINE.json configs[1]): for every FSDP unit (32 TransformerBlocks + root)
+unshard (copy-in -> NCCL all-gather -> copy-out, bf16) -> reshard -> reduce_scatter_grads
+(chunk-cat + fp32 cast + /W -> NCCL reduce-scatter fp32 -> sharded grad), with the next
+unit's unshard prefetched.  Bytes per unit: the all-gather
+output W*S*2 plus the reduce-scatter input W*S*4 per rank; `value` = those bytes summed
+over all ranks / max-over-ranks step time (whole job, weak scaling: every rank unshards
+the full model).
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; for N > 1 under torchrun.
+`--impl reference` times the CPU oracle (the reference arm of this tier) instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+WORKLOADS = {
+    "llama3.1-8b": dict(model="llama3.1-8b", fp8=False, cycle=None),
+    "llama3.1-8b-fp8": dict(model="llama3.1-8b", fp8=True, cycle=None),
+    "llama3.1-70b": dict(model="llama3.1-70b", fp8=False, cycle=4),
+    "toy": dict(model="toy", fp8=False, cycle=None),
+}
+METRIC = "FSDP unshard+reshard GB/s per layer (fraction of NVLink/HBM peak)"
+NVLINK_GBS = 900.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="llama3.1-8b", choices=list(WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--serial", action="store_true", help="no prefetch: each unit isolated")
+    ap.add_argument("--out", default=None, help="also append the JSON line to this file")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def unit_lists(model: str, include_root=True):
+    import synth
+    units = synth.model_units(model, include_root=include_root)
+    return [([s for _, s, _ in u], [e for _, _, e in u]) for u in units]
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", ",".join(str(g) for g in self.gpus)],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait(timeout=10)
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2410_06511_b200 as F
+
+    N = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if N != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={N}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if N > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        mesh = F.Mesh.from_process_group(device=local)
+    else:
+        mesh = F.Mesh(1, 0, local, unique_id=F.get_unique_id())
+    wl = WORKLOADS[args.workload]
+    units = unit_lists(wl["model"])
+    if wl["cycle"]:   # 70B: cycle `cycle` distinct block instances (memory), SURVEY.md §8(d) row 4
+        units = units[:wl["cycle"]]
+    pdtype = torch.float8_e4m3fn if wl["fp8"] else torch.bfloat16
+
+    # ---- setup: shard (synthetic seeded params written straight into the shards)
+    layers, grads = [], []
+    gen = torch.Generator(device=dev).manual_seed(241006511 + rank)
+    for ui, (shapes, elig) in enumerate(units):
+        l = F.fsdp_shard(mesh, None, elig, shapes=shapes)
+        flat = l.sharded_flat()
+        for p in range(l.P):
+            m = l.metas[p]
+            n = m["row_count"] * m["rest"]
+            if n:
+                flat[m["elem_offset"]:m["elem_offset"] + n].normal_(0.0, 0.02, generator=gen)
+        layers.append(l)
+        grads.append([(torch.randn(s, generator=gen, device=dev) * 1e-3).to(torch.bfloat16) for s in shapes])
+    torch.cuda.synchronize()
+    comp = torch.cuda.Stream(device=dev)
+    W = N
+
+    def step():
+        if wl["fp8"]:
+            F.precompute_fp8_scales(mesh, layers, stream=comp)
+        n = len(layers)
+        if not args.serial:
+            F.fsdp_unshard(layers[0], pdtype, stream=comp)
+        for i in range(n):
+            if args.serial:
+                F.fsdp_unshard(layers[i], pdtype, stream=comp)
+            F.fsdp_wait_unshard(layers[i], stream=comp)
+            if not args.serial and i + 1 < n:
+                F.fsdp_unshard(layers[i + 1], pdtype, stream=comp)   # prefetch
+            F.fsdp_reshard(layers[i], stream=comp)
+            F.reduce_scatter_grads(layers[i], grads[i], stream=comp)
+            if args.serial:
+                F.fsdp_wait_reduce_scatter(layers[i], stream=comp)
+        for l in layers:
+            F.fsdp_wait_reduce_scatter(l, stream=comp)
+
+    # algorithmic bytes per step per rank
+    slot_b = [(l.S_bytes_fp8 if wl["fp8"] else 2 * l.S) for l in layers]
+    bytes_rank = sum(W * sb + 4 * W * l.S for sb, l in zip(slot_b, layers))
+
+    def barrier():
+        if N > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        step()
+    comp.synchronize()
+    mesh.synchronize(600000)
+    barrier()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(list(range(N))) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    mesh.profile_enable(True)
+    mesh.profile_read(reset=True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(comp)
+    for _ in range(args.steps):
+        step()
+    e1.record(comp)
+    comp.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    prof = mesh.profile_read(reset=True)
+    mesh.profile_enable(False)
+    clk = clocks.stop() if clocks else None
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if N > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = N * bytes_rank / (ms_max * 1e-3) / 1e9
+    algbw_rank = bytes_rank / (ms_max * 1e-3) / 1e9
+    busbw_rank = algbw_rank * (W - 1) / W
+
+    # ---- roofline of the dominant kernel (largest total device time among ours)
+    peak, peak_src = measured_peaks()
+    ours = ["copy_in", "copy_out", "rs_copy_in", "rs_copy_out", "amax", "scale"]
+    dom = max(ours, key=lambda k: prof[k]["ms"])
+    d = prof[dom]
+    per_launch_bytes = d["bytes"] / max(d["launches"], 1)
+    avg_ms = d["ms"] / max(d["launches"], 1)
+    achieved = per_launch_bytes / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
+    kernels = {}
+    for k in ours + ["all_gather", "reduce_scatter", "all_reduce"]:
+        if prof[k]["launches"]:
+            kernels[k] = {"launches": prof[k]["launches"], "avg_us": round(prof[k]["ms"] / prof[k]["launches"] * 1e3, 2),
+                          "GBps": round(prof[k]["bytes"] / (prof[k]["ms"] * 1e-3) / 1e9, 1) if prof[k]["ms"] else None,
+                          "share_of_step": round(prof[k]["ms"] / args.steps / ms_max, 4)}
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(f"{args.workload}/w{N}", {}).get(dom)
+        except Exception:
+            traffic = None
+    gpu_launches = sum(prof[k]["launches"] for k in ours)
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the timing
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, F, torch, dist, mesh, layers, grads, comp, dev, N, W, pdtype, wl, bytes_rank,
+                      barrier)
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and N == 1:
+            cpu = cpu_baseline(args, W)
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp8_e4m3+bf16/f32" if wl["fp8"] else "bf16/f32",
+            "data": "synthetic (seeded normal params and bf16 grads, Llama 3.1 parameter shapes)",
+            "config": {"workload": f"{args.workload} layout: {len(layers)} FSDP units "
+                                   f"({'32 blocks + root' if args.workload.startswith('llama3.1-8b') else 'see DESIGN.md'}), "
+                                   f"{'fp8 e4m3' if wl['fp8'] else 'bf16'} all-gather / fp32 reduce-scatter, "
+                                   f"{'serial' if args.serial else 'prefetch next unit'}",
+                       "world_size": W, "units": len(layers),
+                       "l2": "inputs larger than L2 (every unit's shard/grads/buffers are 100s of MB; 126 MB L2)",
+                       "bytes_per_step_per_rank": bytes_rank},
+            "per_rank": {"algbw_GBps": round(algbw_rank, 2), "busbw_GBps": round(busbw_rank, 2),
+                         "busbw_frac_nvlink_900": round(busbw_rank / NVLINK_GBS, 4)},
+            "kernels": kernels,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
+                         "bytes_per_launch": int(per_launch_bytes), "traffic": traffic},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,
+        }
+    for l in layers:
+        l.destroy()
+    mesh.destroy()
+    if N > 1:
+        dist.destroy_process_group()
+    return line
+
+
+def run_e2e(args, F, torch, dist, mesh, layers, grads, comp, dev, N, W, pdtype, wl, bytes_rank, barrier):
+    """Same step through the public API, inputs (this step's full grads) copied H2D from
+    pinned host memory and the result (every unit's sharded fp32 grad) read back D2H,
+    all inside the timed region."""
+    max_g = max(sum(g.numel() for g in gs) for gs in grads)
+    max_s = max(l.S for l in layers)
+    h_in = torch.empty(max_g, dtype=torch.bfloat16).pin_memory()
+    big = max(range(len(grads)), key=lambda i: sum(g.numel() for g in grads[i]))
+    h_in.copy_(torch.cat([g.view(-1) for g in grads[big]]).cpu())
+    h_out = torch.empty(max_s, dtype=torch.float32).pin_memory()
+    h2d = sum(sum(g.numel() for g in gs) * 2 for gs in grads)
+    d2h = sum(4 * l.S for l in layers)
+
+    def step():
+        if wl["fp8"]:
+            F.precompute_fp8_scales(mesh, layers, stream=comp)
+        n = len(layers)
+        with torch.cuda.stream(comp):
+            F.fsdp_unshard(layers[0], pdtype, stream=comp)
+            for i in range(n):
+                off = 0
+                for g in grads[i]:       # this step's input: the unit's full grads, H2D
+                    g.view(-1).copy_(h_in[off:off + g.numel()], non_blocking=True)
+                    off += g.numel()
+                F.fsdp_wait_unshard(layers[i], stream=comp)
+                if i + 1 < n:
+                    F.fsdp_unshard(layers[i + 1], pdtype, stream=comp)
+                F.fsdp_reshard(layers[i], stream=comp)
+                F.reduce_scatter_grads(layers[i], grads[i], stream=comp)
+            for l in layers:             # the step's result: every sharded grad, D2H
+                F.fsdp_wait_reduce_scatter(l, stream=comp)
+                h_out[:l.S].copy_(l.sharded_grad_flat(), non_blocking=True)
+
+    step()
+    comp.synchronize()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(comp)
+    for _ in range(args.e2e_steps):
+        step()
+    e1.record(comp)
+    comp.synchronize()
+    ms = e0.elapsed_time(e1) / args.e2e_steps
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if N > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": round(N * bytes_rank / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 3),
+            "steps": args.e2e_steps, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU)
+def _oracle_sample(model: str, W: int):
+    """Bounded sample of the workload for the CPU oracle: the attention weights + norms of
+    one Llama block (41.9M of 218.1M params for 8B), all W ranks simulated."""
+    import synth
+    u = synth.model_units(model, include_root=False)[0]
+    keep = [i for i, (n, _, _) in enumerate(u) if n.startswith("attention")]
+    shapes = [u[i][1] for i in keep]
+    elig = [u[i][2] for i in keep]
+    params = [synth.param_values(0, p, s) for p, s in enumerate(shapes)]
+    grads = [[synth.grad_bf16_bits(0, p, q, s) for p, s in enumerate(shapes)] for q in range(W)]
+    return shapes, elig, params, grads
+
+
+def _oracle_step(World, BF16, FP8, shapes, elig, params, grads, W, fp8):
+    w = World(shapes, W, elig)
+    shards = w.shard(params)
+    if fp8:
+        _, scale = w.precompute_fp8_scales(shards)
+        w.unshard(shards, FP8, scale)
+    else:
+        w.unshard(shards, BF16)
+    w.reduce_scatter_grads(grads, BF16, True)
+    slot = w.S_bytes_fp8 if fp8 else 2 * w.S
+    return W * (W * slot + 4 * W * w.S)     # same algorithmic bytes, all simulated ranks
+
+
+def cpu_baseline(args, W):
+    from oracle import World
+    from oracle.world import BF16, FP8
+    wl = WORKLOADS[args.workload]
+    shapes, elig, params, grads = _oracle_sample(wl["model"], W)
+    t0 = time.perf_counter()
+    nbytes = _oracle_step(World, BF16, FP8, shapes, elig, params, grads, W, wl["fp8"])
+    dt = time.perf_counter() - t0
+    return {"value": round(nbytes / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "seconds": round(dt, 2),
+            "sample": f"one {wl['model']} block's attention weights + norms ({sum(int(np.prod(s)) for s in shapes)} params), "
+                      f"W={W} simulated ranks, unshard + reduce-scatter, single-threaded NumPy"}
+
+
+def run_reference(args):
+    N = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    from oracle import World
+    from oracle.world import BF16, FP8
+    wl = WORKLOADS[args.workload]
+    W = args.gpus
+    shapes, elig, params, grads = _oracle_sample(wl["model"], W)
+    for _ in range(args.warmup):
+        _oracle_step(World, BF16, FP8, shapes, elig, params, grads, W, wl["fp8"])
+    t0 = time.perf_counter()
+    nbytes = 0
+    for _ in range(args.steps):
+        nbytes += _oracle_step(World, BF16, FP8, shapes, elig, params, grads, W, wl["fp8"])
+    dt = time.perf_counter() - t0
+    value = nbytes / dt / 1e9
+    sample = (f"one {wl['model']} block's attention weights + norms per step, W={W} simulated ranks, "
+              f"unshard + reduce-scatter, single-threaded NumPy oracle")
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": N,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (numpy)",
+            "data": "synthetic", "config": {"workload": f"{args.workload} (bounded oracle sample)", "world_size": W},
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None:
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.out:
+            with open(args.out, "a") as f:
+                f.write(s + "\n")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,271 @@
+/*
+ * fsdp_b200.h — C ABI of the B200-native FSDP2 per-parameter Shard(0) hot path.
+ *
+ * The paper (arXiv 2410.06511, /root/reference/PAPER.md, cited "P:<line>") states the
+ * problem as
+ *   fully_shard(block, mesh=dp_mesh, mp_policy=MixedPrecisionPolicy(param_dtype,
+ *               reduce_dtype), reshard_after_forward=...)
+ * with parameters "represented as DTensors sharded on the tensor dimension 0"
+ * (P:460), a bf16 parameter all-gather and an fp32 gradient reduce-scatter (P:154,
+ * P:417), "only a single division kernel ... pre-dividing the local FP32
+ * reduce-scatter gradient by world size", multi-tensor all-gather /
+ * reduce-scatter kernels, "Float8 all-gather" with per-tensor scaling
+ * (P:157), deterministic memory release without record_stream and the data-
+ * parallel degree defaulting to all GPUs.  The calls below follow that
+ * statement: fsdp_shard(params, mesh), fsdp_unshard / fsdp_all_gather_params(layer,
+ * dtype, fp8_scale), fsdp_precompute_fp8_scales(params), fsdp_reduce_scatter_grads(
+ * layer, reduce_dtype, mean).
+ *
+ * Conventions (all functions):
+ *  - Every function returns fsdp_status_t; no C++ exception crosses the ABI.  On a
+ *    non-OK status fsdp_last_error() returns a thread-local message.  Argument, shape,
+ *    dtype and state errors are detected before any side effect.
+ *  - Pointers named *_dev are CUDA device pointers (or, where stated, any pointer
+ *    cudaMemcpyDefault accepts).  Streams are cudaStream_t passed as void*; NULL is the
+ *    legacy default stream.
+ *  - "Stream-ordered" calls return immediately; their device work is ordered after all
+ *    work previously enqueued on `compute`, and later work on `compute` may consume
+ *    the results after the matching fsdp_wait_* call.
+ *  - A mesh and its layers are used from one host thread.
+ *  - Layout: param order is the caller's order; rank r owns rows
+ *    [min(r*c, d0), min((r+1)*c, d0)) with c = ceil(d0/W) (trailing ranks may be
+ *    empty); the padded shard of param p has n_p = c*rest elements (rest = product of
+ *    the non-leading dims) and sits at elem_offset off_p = sum_{q<p} round_up(n_q, 16)
+ *    of a flat per-rank buffer of S = sum_p round_up(n_p, 16) elements.  The mixed
+ *    float8 all-gather slot uses byte offsets boff_p = sum_{q<p} round_up(n_q*e_q, 16)
+ *    with e = 1 (e4m3fn, fp8-eligible params) or 2 (bf16).
+ */
+#ifndef FSDP_B200_H
+#define FSDP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSDP_B200_ABI_VERSION 1
+#define FSDP_MAX_NDIM 8
+#define FSDP_UNIQUE_ID_BYTES 128
+
+typedef enum {
+  FSDP_OK = 0,
+  FSDP_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, bad enum, out-of-range index          */
+  FSDP_ERR_SHAPE = 2,            /* 0-dim param, ranks disagree on the layout   */
+  FSDP_ERR_DTYPE = 3,            /* dtype combination not supported                      */
+  FSDP_ERR_STATE = 4,            /* call out of order (e.g. unsharded_param before wait) */
+  FSDP_ERR_OUT_OF_MEMORY = 5,
+  FSDP_ERR_CUDA = 6,
+  FSDP_ERR_NCCL = 7,
+  FSDP_ERR_TIMEOUT = 8,
+  FSDP_ERR_NONFINITE = 9,        /* non-finite fp8 amax                     */
+  FSDP_ERR_UNAVAILABLE = 10      /* feature not available in this build / mesh           */
+} fsdp_status_t;
+
+typedef enum {
+  FSDP_FLOAT32 = 0,
+  FSDP_BFLOAT16 = 1,
+  FSDP_FLOAT8_E4M3FN = 2
+} fsdp_dtype_t;
+
+typedef struct fsdp_mesh fsdp_mesh_t;   /* 1-D data-parallel group: NCCL comms, streams */
+typedef struct fsdp_layer fsdp_layer_t; /* one FSDP unit (TransformerBlock or root)     */
+
+/* One parameter of an FSDP unit: its full (unsharded) shape and whether it takes part
+ * in the Float8 all-gather ("applied selectively to linear layers"). */
+typedef struct {
+  int32_t ndim;                  /* 1..FSDP_MAX_NDIM; 0-dim -> FSDP_ERR_SHAPE */
+  int32_t fp8_eligible;          /* 0/1 */
+  int64_t shape[FSDP_MAX_NDIM];  /* shape[0] may be 0 or < world_size */
+} fsdp_param_desc_t;
+
+/* Shard(0) metadata of one parameter on one rank (all in elements unless noted). */
+typedef struct {
+  int64_t dim0;            /* shape[0]                                    */
+  int64_t rest;            /* product of shape[1:]                        */
+  int64_t chunk_rows;      /* c = ceil(dim0 / W)                          */
+  int64_t row_begin;       /* min(r*c, dim0)                              */
+  int64_t row_count;       /* rows owned by this rank (may be 0)          */
+  int64_t padded_numel;    /* n = c * rest                                */
+  int64_t elem_offset;     /* off_p in the flat fp32/bf16 layouts         */
+  int64_t fp8_byte_offset; /* boff_p in the mixed float8 all-gather slot  */
+} fsdp_param_meta_t;
+
+/* Per-kernel device time accumulated while profiling is on (CUDA events recorded on
+ * the stream each kernel is launched on). */
+typedef enum {
+  FSDP_PROF_COPY_IN = 0,     /* K2/K3 unshard copy-in (bf16 or float8 cast)   */
+  FSDP_PROF_ALL_GATHER = 1,  /* NCCL all-gather                               */
+  FSDP_PROF_COPY_OUT = 2,    /* K4 unshard copy-out                           */
+  FSDP_PROF_RS_COPY_IN = 3,  /* K5 grad chunk-cat + fp32 cast + divide by W   */
+  FSDP_PROF_REDUCE_SCATTER = 4,
+  FSDP_PROF_RS_COPY_OUT = 5, /* K6 accumulate / widen                          */
+  FSDP_PROF_AMAX = 6,        /* K1                                            */
+  FSDP_PROF_SCALE = 7,       /* K1b                                           */
+  FSDP_PROF_ALL_REDUCE = 8,  /* NCCL all-reduce(max) of the amaxes            */
+  FSDP_PROF_NUM = 9
+} fsdp_prof_kind_t;
+
+typedef struct {
+  int64_t launches[FSDP_PROF_NUM];
+  double total_ms[FSDP_PROF_NUM];
+  int64_t bytes[FSDP_PROF_NUM];  /* algorithmic HBM bytes of those launches */
+} fsdp_profile_t;
+
+/* ---------------------------------------------------------------- generic */
+int32_t fsdp_abi_version(void);
+const char* fsdp_last_error(void);           /* thread-local; "" if none */
+const char* fsdp_status_string(fsdp_status_t s);
+
+/* Host-only Shard(0) layout of one unit for (world_size, rank); needs no GPU.
+ * out_metas: caller array of n_params entries.  out_hash: 64-bit FNV-1a hash of
+ * (W, every desc) — identical on all ranks iff they agree on the unit (the check
+ * fsdp_shard performs, "shape mismatch across members").  Any out_* may be NULL. */
+fsdp_status_t fsdp_layout_compute(int32_t n_params, const fsdp_param_desc_t* descs,
+                                  int32_t world_size, int32_t rank,
+                                  fsdp_param_meta_t* out_metas, int64_t* out_S,
+                                  int64_t* out_S_bytes_fp8, uint64_t* out_hash);
+
+/* ---------------------------------------------------------------- mesh */
+/* Rank 0 calls this and broadcasts the bytes (the Python binding uses the
+ * torch.distributed process group for that, its only torch.distributed use). */
+fsdp_status_t fsdp_get_unique_id(uint8_t id[FSDP_UNIQUE_ID_BYTES]);
+
+/* Collective over the W ranks: creates two NCCL communicators (all-gather, and
+ * reduce-scatter/all-reduce, so unshard of layer i-1 overlaps the reduce-scatter of
+ * layer i) plus internal high-priority streams on `cuda_device`.  world_size = the
+ * data-parallel shard degree (all ranks by default). */
+fsdp_status_t fsdp_mesh_init(const uint8_t id[FSDP_UNIQUE_ID_BYTES], int32_t world_size,
+                             int32_t rank, int32_t cuda_device, fsdp_mesh_t** out);
+
+/* A mesh without communicators: the layout is that of rank `rank` of `world_size`,
+ * the fsdp_stage_* entry points work, the collective calls work only when
+ * world_size == 1 (identity collectives) and return FSDP_ERR_UNAVAILABLE otherwise.
+ * Used to test every kernel at any W on one GPU. */
+fsdp_status_t fsdp_mesh_init_local(int32_t world_size, int32_t rank, int32_t cuda_device,
+                                   fsdp_mesh_t** out);
+
+/* Destroys the mesh (synchronizes its streams, frees its pools, destroys the comms).
+ * All layers of the mesh must have been destroyed. */
+fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* mesh);
+fsdp_status_t fsdp_mesh_info(const fsdp_mesh_t* mesh, int32_t* world_size, int32_t* rank,
+                             int32_t* cuda_device);
+
+/* Waits (host) until every internal stream of the mesh is idle, polling NCCL for
+ * asynchronous errors.  Returns FSDP_ERR_NONFINITE if a precompute saw a non-finite
+ * amax since the last call (flag is then cleared), FSDP_ERR_NCCL on a NCCL async
+ * error, FSDP_ERR_TIMEOUT after timeout_ms (<= 0: no timeout); after NCCL/TIMEOUT the
+ * communicators are aborted and the mesh is unusable. */
+fsdp_status_t fsdp_mesh_synchronize(fsdp_mesh_t* mesh, int64_t timeout_ms);
+
+/* Profiling: when on, every kernel / collective launch is bracketed by CUDA events on
+ * its own stream; fsdp_profile_read synchronizes and returns the totals since the last
+ * reset. */
+fsdp_status_t fsdp_profile_enable(fsdp_mesh_t* mesh, int32_t on);
+fsdp_status_t fsdp_profile_read(fsdp_mesh_t* mesh, fsdp_profile_t* out, int32_t reset);
+
+/* ---------------------------------------------------------------- shard (a1) */
+/* fsdp_shard(params, mesh): synchronous, collective over the mesh (all ranks call it
+ * with the same descs, checked by an all-gather of the layout hash -> FSDP_ERR_SHAPE).
+ * Copies descs.  full_params[p] (fp32, contiguous, host or device — anything
+ * cudaMemcpyDefault accepts — or NULL to leave the shard zero, or full_params == NULL
+ * for all) is read once: this rank's rows go to its flat fp32 shard, padding is +0.0.
+ * The layer owns: the fp32 shard [S], the fp32 sharded-grad buffer [S], tile tables. */
+fsdp_status_t fsdp_shard(fsdp_mesh_t* mesh, int32_t n_params, const fsdp_param_desc_t* descs,
+                         const float* const* full_params, fsdp_layer_t** out);
+/* Synchronizes the layer's pending work and frees it.  State must not be UNSHARDED. */
+fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* layer);
+fsdp_status_t fsdp_layer_info(const fsdp_layer_t* layer, int32_t* n_params, int64_t* S,
+                              int64_t* S_bytes_fp8);
+fsdp_status_t fsdp_param_meta(const fsdp_layer_t* layer, int32_t p, fsdp_param_meta_t* out);
+/* Views into the layer-owned fp32 shard (the optimizer's state; valid until destroy):
+ * param p's padded shard is (*dev)[0 .. padded_numel), rows [0,row_count) are real. */
+fsdp_status_t fsdp_sharded_param(const fsdp_layer_t* layer, int32_t p, float** dev);
+fsdp_status_t fsdp_sharded_flat(const fsdp_layer_t* layer, float** dev);
+
+/* ---------------------------------------------------------------- fp8 scales (a2) */
+/* precompute_fp8_scales(params): for every fp8-eligible param of the given layers,
+ * amax_p = max over ranks and elements of |shard_p| (one K1 launch over all layers,
+ * one NCCL all-reduce(max), one K1b launch), s_p = fp32(448 / fp64(max(amax_p,1e-12))).
+ * Stream-ordered on `stream`; results readable via fsdp_fp8_scales after work on
+ * `stream`.  A non-finite amax sets the mesh's error flag (see fsdp_mesh_synchronize)
+ * and leaves s_p = 0 for that param. */
+fsdp_status_t fsdp_precompute_fp8_scales(fsdp_mesh_t* mesh, fsdp_layer_t* const* layers,
+                                         int32_t n_layers, void* stream);
+/* Device arrays of P floats (entries of non-eligible params are 0). */
+fsdp_status_t fsdp_fp8_scales(const fsdp_layer_t* layer, const float** scales_dev,
+                              const float** amax_dev);
+
+/* ---------------------------------------------------------------- unshard (a3-a6) */
+/* fsdp_unshard / all_gather_params(layer, dtype, fp8_scale): stream-ordered after
+ * `compute`.  Acquires an all-gather buffer from the mesh pool (event-guarded, never
+ * record_stream), runs copy-in (K2 bf16 / K3 float8, in place into this
+ * rank's slot), the all-gather, and copy-out (K4) into per-parameter full tensors.
+ * param_dtype: FSDP_BFLOAT16 or FSDP_FLOAT8_E4M3FN (eligible params in
+ * e4m3fn with per-tensor scale, others bf16).  fp8_scales_dev: P device floats, or NULL
+ * to use the layer's precomputed scales.  State: SHARDED -> UNSHARDING. */
+fsdp_status_t fsdp_unshard(fsdp_layer_t* layer, fsdp_dtype_t param_dtype,
+                           const float* fp8_scales_dev, void* compute);
+/* Makes `compute` wait for the unshard.  State: UNSHARDING -> UNSHARDED. */
+fsdp_status_t fsdp_wait_unshard(fsdp_layer_t* layer, void* compute);
+/* fsdp_unshard + fsdp_wait_unshard (the name used by BASELINE.json). */
+fsdp_status_t fsdp_all_gather_params(fsdp_layer_t* layer, fsdp_dtype_t param_dtype,
+                                     const float* fp8_scales_dev, void* compute);
+/* Full tensor of param p (shape = desc shape, row-major, contiguous, 256B-aligned);
+ * dtype is BF16 or FLOAT8_E4M3FN.  Valid from wait_unshard until reshard.
+ * State must be UNSHARDED, else FSDP_ERR_STATE. */
+fsdp_status_t fsdp_unsharded_param(const fsdp_layer_t* layer, int32_t p, void** dev,
+                                   fsdp_dtype_t* dtype);
+/* Releases the unsharded storage: the buffer returns to the pool once the work
+ * enqueued on `compute` so far completes (event-guarded).  UNSHARDED -> SHARDED. */
+fsdp_status_t fsdp_reshard(fsdp_layer_t* layer, void* compute);
+
+/* ---------------------------------------------------------------- post-backward (a7-a9) */
+/* reduce_scatter_grads(layer, reduce_dtype, mean): full_grads_dev[p] = this rank's
+ * full gradient of param p (contiguous, desc shape, grad_dtype BF16 or FLOAT32).
+ * K5 chunks every grad on dim 0, widens to fp32, divides once by W when mean != 0
+ * (P:466), zero-pads, packs rank-major [W][S]; then a reduce-scatter (sum) in
+ * reduce_dtype (FLOAT32 default; BFLOAT16: inputs rounded to bf16 after the
+ * division) lands this rank's chunk in the layer's fp32 sharded-grad buffer
+ * (accumulate != 0: added to it, in fp32).  The caller keeps full_grads alive and
+ * unmodified until fsdp_wait_reduce_scatter (deterministic release). */
+fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* layer, const void* const* full_grads_dev,
+                                        fsdp_dtype_t grad_dtype, fsdp_dtype_t reduce_dtype,
+                                        int32_t mean, int32_t accumulate, void* compute);
+fsdp_status_t fsdp_wait_reduce_scatter(fsdp_layer_t* layer, void* compute);
+/* fp32 sharded grad of param p: (*dev)[0 .. row_count*rest) (views into the layer's
+ * grad buffer, same flat layout as the shard). */
+fsdp_status_t fsdp_sharded_grad(const fsdp_layer_t* layer, int32_t p, float** dev);
+fsdp_status_t fsdp_sharded_grad_flat(const fsdp_layer_t* layer, float** dev);
+fsdp_status_t fsdp_zero_grad(fsdp_layer_t* layer, void* stream);
+
+/* ---------------------------------------------------------------- stage entry points */
+/* One kernel each, no communication, stream-ordered on `stream`; they expose the
+ * individual steps (for tests at any W on one GPU and for custom collectives). */
+/* K2/K3: this rank's all-gather slot (S*2 bytes for BF16, S_bytes_fp8 for FLOAT8). */
+fsdp_status_t fsdp_stage_copy_in(const fsdp_layer_t* layer, fsdp_dtype_t param_dtype,
+                                 const float* fp8_scales_dev, void* ag_slot_dev, void* stream);
+/* K4: from a full rank-major all-gather buffer [W][slot] into per-param full tensors
+ * full_out_dev[p] (contiguous, numel = prod(shape) elements of the param's dtype). */
+fsdp_status_t fsdp_stage_copy_out(const fsdp_layer_t* layer, fsdp_dtype_t param_dtype,
+                                  const void* ag_buffer_dev, void* const* full_out_dev,
+                                  void* stream);
+/* K1 on one layer: amax_out_dev[p] = max |shard_p| on this rank (0 if not eligible). */
+fsdp_status_t fsdp_stage_local_amax(const fsdp_layer_t* layer, float* amax_out_dev, void* stream);
+/* K1b: scale_out[p] = eligible ? fp32(448/fp64(max(amax[p],1e-12))) : 0 (non-finite
+ * amax -> 0 and the mesh error flag is set). */
+fsdp_status_t fsdp_stage_fp8_scale(const fsdp_layer_t* layer, const float* amax_dev,
+                                   float* scale_out_dev, void* stream);
+/* K5: rs_in_dev = [W][S] (FLOAT32 or BFLOAT16 per reduce_dtype). */
+fsdp_status_t fsdp_stage_rs_copy_in(const fsdp_layer_t* layer, const void* const* full_grads_dev,
+                                    fsdp_dtype_t grad_dtype, fsdp_dtype_t reduce_dtype,
+                                    int32_t mean, void* rs_in_dev, void* stream);
+/* K6: the layer's fp32 grad buffer [S] = (accumulate ? grad + : ) widen(rs_out_dev[S]). */
+fsdp_status_t fsdp_stage_rs_copy_out(fsdp_layer_t* layer, const void* rs_out_dev,
+                                     fsdp_dtype_t reduce_dtype, int32_t accumulate, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSDP_B200_H */

@@ -1,0 +1,1052 @@
+// C-ABI implementation (include/fsdp_b200.h): mesh (NCCL communicators + streams +
+// buffer pools), layers (fp32 shard, sharded grad, tile tables), and the stream-ordered
+// unshard / reshard / reduce-scatter / fp8-precompute calls.
+//
+// Stream topology per mesh (all high priority, non-blocking):
+//   s_cin  : K2/K3 copy-in                       (unshard of layer i+1 runs here while
+//   s_ag   : NCCL all-gather on comm_ag           the all-gather of layer i is on s_ag
+//   s_cout : K4 copy-out                          and its copy-out on s_cout)
+//   s_rsc  : K5 RS copy-in
+//   s_rs   : NCCL reduce-scatter / all-reduce(max) on comm_rs, then K6, K1, K1b
+// Two communicators let the all-gather of layer i-1 overlap the reduce-scatter of layer
+// i in backward.  Buffer reuse is guarded by CUDA events recorded on the consuming
+// stream (never cudaStreamAddCallback/record_stream), so memory is released
+// deterministically.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "fsdp_b200.h"
+#include "kernels.h"
+#include "layout.h"
+
+using fsdpk::Tile;
+using fsdpl::Layout;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Error {
+  fsdp_status_t st;
+  std::string msg;
+};
+
+[[noreturn]] void fail(fsdp_status_t st, const std::string& msg) { throw Error{st, msg}; }
+
+#define CUDA_CHECK(x)                                                                        \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      fail(e_ == cudaErrorMemoryAllocation ? FSDP_ERR_OUT_OF_MEMORY : FSDP_ERR_CUDA,         \
+           std::string(#x) + ": " + cudaGetErrorString(e_));                                 \
+  } while (0)
+
+#define NCCL_CHECK(x)                                                                        \
+  do {                                                                                       \
+    ncclResult_t r_ = (x);                                                                   \
+    if (r_ != ncclSuccess) fail(FSDP_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+template <class F>
+fsdp_status_t guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return FSDP_OK;
+  } catch (const Error& e) {
+    g_last_error = e.msg;
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host out of memory";
+    return FSDP_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return FSDP_ERR_CUDA;
+  }
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) CUDA_CHECK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) CUDA_CHECK(cudaFree(p));
+    p = nullptr;
+    cap = 0;
+    // +64 B slack: the misaligned 16-byte loads of K4/K5 may touch the aligned block
+    // holding the last byte
+    CUDA_CHECK(cudaMalloc(&p, bytes + 64));
+    cap = bytes;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct DevTiles {
+  Tile* d = nullptr;
+  int n = 0;
+  std::vector<int> first;   // per-param first tile (param-major tables)
+  void upload(const std::vector<Tile>& h) {
+    release();
+    n = (int)h.size();
+    if (n) {
+      CUDA_CHECK(cudaMalloc(&d, sizeof(Tile) * h.size()));
+      CUDA_CHECK(cudaMemcpy(d, h.data(), sizeof(Tile) * h.size(), cudaMemcpyHostToDevice));
+    }
+  }
+  void release() {
+    if (d) cudaFree(d);
+    d = nullptr;
+    n = 0;
+  }
+};
+
+struct Slot {             // one pooled buffer set
+  DevBuf a, b;            // AG: a = [W][slot] buffer, b = unsharded arena
+                          // RS: a = [W][S] reduce-scatter input, b = staging output [S]
+  cudaEvent_t free_ev = nullptr;
+  bool in_use = false;
+  bool ever_used = false;
+  uint64_t last_use = 0;
+};
+
+struct ProfRec {
+  int kind;
+  cudaEvent_t a, b;
+  int64_t bytes;
+};
+
+enum LayerState { SHARDED = 0, UNSHARDING = 1, UNSHARDED = 2 };
+
+}  // namespace
+
+struct fsdp_layer;
+
+struct fsdp_mesh {
+  int W = 1, rank = 0, device = 0;
+  bool local = true;
+  ncclComm_t comm_ag = nullptr, comm_rs = nullptr;
+  cudaStream_t s_cin = nullptr, s_ag = nullptr, s_cout = nullptr, s_rsc = nullptr, s_rs = nullptr;
+  fsdpk::LaunchCfg cfg{};
+  std::vector<Slot*> ag_slots, rs_slots;
+  uint64_t use_seq = 0;
+  // fp8 scale registry: one entry per param of every layer (contiguous per layer)
+  int reg_size = 0, reg_cap = 0;
+  uint32_t* reg_acc = nullptr;
+  float* reg_amax = nullptr;
+  float* reg_scale = nullptr;
+  uint8_t* reg_elig = nullptr;
+  int* d_err = nullptr;
+  cudaEvent_t ev_pre_call = nullptr, ev_pre_done = nullptr;
+  std::vector<fsdp_layer*> layers;
+  // precompute cache: layer list -> (amax tiles, finalize index list)
+  struct PreSet {
+    std::vector<fsdp_layer*> layers;
+    DevTiles tiles;
+    int32_t* idx = nullptr;
+    int nidx = 0;
+    int64_t bytes = 0;
+  };
+  std::vector<PreSet*> presets;
+  // profiling
+  bool prof = false;
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  fsdp_profile_t prof_acc{};
+  bool aborted = false;
+};
+
+struct fsdp_layer {
+  fsdp_mesh* mesh = nullptr;
+  int P = 0;
+  std::vector<fsdp_param_desc_t> descs;
+  Layout L;
+  float* shard = nullptr;
+  float* grad = nullptr;
+  int reg_base = 0;
+  int32_t* d_idx_local = nullptr;   // 0..P-1 (stage fp8 scale)
+  DevTiles t_cin_fp8, t_cout_bf16, t_cout_fp8, t_rsin;
+  int64_t bytes_cin_fp8 = 0, bytes_cout_bf16 = 0, bytes_cout_fp8 = 0;
+  int64_t grad_numel_total = 0;
+  // unshard state
+  int state = SHARDED;
+  Slot* slot = nullptr;
+  fsdp_dtype_t ushard_dtype = FSDP_BFLOAT16;
+  cudaEvent_t ev_call = nullptr, ev_cin = nullptr, ev_ag = nullptr, ev_done = nullptr;
+  // reduce-scatter state
+  bool rs_pending = false;
+  cudaEvent_t ev_rcall = nullptr, ev_k5 = nullptr, ev_rs_done = nullptr;
+};
+
+namespace {
+
+cudaEvent_t new_event(bool timing = false) {
+  cudaEvent_t e;
+  CUDA_CHECK(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+  return e;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- profiling helpers
+struct ProfScope {
+  fsdp_mesh* m;
+  int kind;
+  cudaStream_t st;
+  int64_t bytes;
+  cudaEvent_t a = nullptr;
+  ProfScope(fsdp_mesh* m_, int k, cudaStream_t s, int64_t b) : m(m_), kind(k), st(s), bytes(b) {
+    if (!m->prof) return;
+    a = take();
+    CUDA_CHECK(cudaEventRecord(a, st));
+  }
+  cudaEvent_t take() {
+    if (!m->ev_pool.empty()) {
+      cudaEvent_t e = m->ev_pool.back();
+      m->ev_pool.pop_back();
+      return e;
+    }
+    return new_event(true);
+  }
+  void done() {
+    if (!m->prof || !a) return;
+    cudaEvent_t b = take();
+    CUDA_CHECK(cudaEventRecord(b, st));
+    m->prof_recs.push_back(ProfRec{kind, a, b, bytes});
+    a = nullptr;
+  }
+};
+
+void prof_collect(fsdp_mesh* m) {
+  for (auto& r : m->prof_recs) {
+    CUDA_CHECK(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+    m->prof_acc.launches[r.kind] += 1;
+    m->prof_acc.total_ms[r.kind] += ms;
+    m->prof_acc.bytes[r.kind] += r.bytes;
+    m->ev_pool.push_back(r.a);
+    m->ev_pool.push_back(r.b);
+  }
+  m->prof_recs.clear();
+}
+
+// ---- pools
+Slot* acquire_slot(fsdp_mesh* m, std::vector<Slot*>& pool, size_t a_bytes, size_t b_bytes, int min_slots) {
+  Slot* best = nullptr;
+  int n_free = 0;
+  for (Slot* s : pool) {
+    if (s->in_use) continue;
+    ++n_free;
+    if (!best) { best = s; continue; }
+    const bool s_done = !s->ever_used || cudaEventQuery(s->free_ev) == cudaSuccess;
+    const bool b_done = !best->ever_used || cudaEventQuery(best->free_ev) == cudaSuccess;
+    if (s_done != b_done) { if (s_done) best = s; continue; }
+    if (s->last_use < best->last_use) best = s;
+  }
+  cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not sticky; clear it anyway
+  const bool best_busy = best && best->ever_used && cudaEventQuery(best->free_ev) != cudaSuccess;
+  cudaGetLastError();
+  if (!best || ((int)pool.size() < min_slots && best_busy)) {
+    Slot* s = new Slot();
+    s->free_ev = new_event();
+    pool.push_back(s);
+    best = s;
+  }
+  if (best->a.cap < a_bytes || best->b.cap < b_bytes) {
+    if (best->ever_used) CUDA_CHECK(cudaEventSynchronize(best->free_ev));   // growth: setup-time only
+    best->a.ensure(a_bytes);
+    best->b.ensure(b_bytes);
+  }
+  best->in_use = true;
+  best->last_use = ++m->use_seq;
+  return best;
+}
+
+void release_slot(Slot* s, cudaStream_t last_user) {
+  CUDA_CHECK(cudaEventRecord(s->free_ev, last_user));
+  s->ever_used = true;
+  s->in_use = false;
+}
+
+void check_mesh(const fsdp_mesh* m) {
+  if (!m) fail(FSDP_ERR_INVALID_ARGUMENT, "mesh is NULL");
+  if (m->aborted) fail(FSDP_ERR_STATE, "mesh was aborted after a NCCL error/timeout");
+}
+void check_layer(const fsdp_layer* l) {
+  if (!l) fail(FSDP_ERR_INVALID_ARGUMENT, "layer is NULL");
+  check_mesh(l->mesh);
+}
+void check_param(const fsdp_layer* l, int p) {
+  if (p < 0 || p >= l->P) fail(FSDP_ERR_INVALID_ARGUMENT, "param index out of range");
+}
+
+bool comm_ready(const fsdp_mesh* m) { return !m->local && m->W > 1; }
+
+void ensure_registry(fsdp_mesh* m, int need) {
+  if (need <= m->reg_cap) return;
+  int cap = std::max(need, std::max(64, 2 * m->reg_cap));
+  uint32_t* acc;
+  float *amax, *scale;
+  uint8_t* elig;
+  CUDA_CHECK(cudaMalloc(&acc, sizeof(uint32_t) * cap));
+  CUDA_CHECK(cudaMalloc(&amax, sizeof(float) * cap));
+  CUDA_CHECK(cudaMalloc(&scale, sizeof(float) * cap));
+  CUDA_CHECK(cudaMalloc(&elig, cap));
+  CUDA_CHECK(cudaMemset(acc, 0, sizeof(uint32_t) * cap));
+  CUDA_CHECK(cudaMemset(amax, 0, sizeof(float) * cap));
+  CUDA_CHECK(cudaMemset(scale, 0, sizeof(float) * cap));
+  CUDA_CHECK(cudaMemset(elig, 0, cap));
+  if (m->reg_size) {
+    CUDA_CHECK(cudaDeviceSynchronize());
+    CUDA_CHECK(cudaMemcpy(acc, m->reg_acc, sizeof(uint32_t) * m->reg_size, cudaMemcpyDeviceToDevice));
+    CUDA_CHECK(cudaMemcpy(amax, m->reg_amax, sizeof(float) * m->reg_size, cudaMemcpyDeviceToDevice));
+    CUDA_CHECK(cudaMemcpy(scale, m->reg_scale, sizeof(float) * m->reg_size, cudaMemcpyDeviceToDevice));
+    CUDA_CHECK(cudaMemcpy(elig, m->reg_elig, m->reg_size, cudaMemcpyDeviceToDevice));
+  }
+  cudaFree(m->reg_acc); cudaFree(m->reg_amax); cudaFree(m->reg_scale); cudaFree(m->reg_elig);
+  m->reg_acc = acc; m->reg_amax = amax; m->reg_scale = scale; m->reg_elig = elig;
+  m->reg_cap = cap;
+  for (auto* ps : m->presets) { ps->tiles.release(); cudaFree(ps->idx); delete ps; }
+  m->presets.clear();
+}
+
+void clear_presets(fsdp_mesh* m) {
+  for (auto* ps : m->presets) { ps->tiles.release(); cudaFree(ps->idx); delete ps; }
+  m->presets.clear();
+}
+
+int64_t dtype_size(fsdp_dtype_t d) { return d == FSDP_FLOAT32 ? 4 : (d == FSDP_BFLOAT16 ? 2 : 1); }
+
+// ---- K4 / K5 launches (fsdp_shard enforces P <= kMaxPtrs, one pointer array per launch)
+void launch_copy_out_all(fsdp_layer* l, bool fp8, const void* ag, void* const* outs, cudaStream_t st) {
+  const DevTiles& T = fp8 ? l->t_cout_fp8 : l->t_cout_bf16;
+  fsdpk::PtrArray pa{};
+  for (int p = 0; p < l->P; ++p) pa.p[p] = outs[p];
+  CUDA_CHECK(fsdpk::launch_copy_out(T.d, T.n, ag, pa, l->mesh->cfg, st));
+}
+
+void launch_rs_copy_in_all(fsdp_layer* l, const void* const* grads, bool grad_bf16, void* rs_in, bool out_bf16,
+                           bool mean, cudaStream_t st) {
+  fsdpk::PtrArray pa{};
+  for (int p = 0; p < l->P; ++p) pa.p[p] = grads[p];
+  CUDA_CHECK(fsdpk::launch_rs_copy_in(l->t_rsin.d, l->t_rsin.n, pa, grad_bf16, rs_in, out_bf16, mean, l->mesh->W,
+                                      l->mesh->cfg, st));
+}
+
+int64_t cin_bytes(const fsdp_layer* l, bool fp8) { return fp8 ? l->bytes_cin_fp8 : 6 * l->L.S; }
+int64_t slot_bytes(const fsdp_layer* l, bool fp8) { return fp8 ? l->L.S_bytes_fp8 : 2 * l->L.S; }
+
+void do_copy_in(fsdp_layer* l, bool fp8, const float* scales, void* dst, cudaStream_t st) {
+  fsdp_mesh* m = l->mesh;
+  ProfScope ps(m, FSDP_PROF_COPY_IN, st, cin_bytes(l, fp8));
+  if (fp8) CUDA_CHECK(fsdpk::launch_copy_in_fp8(l->t_cin_fp8.d, l->t_cin_fp8.n, l->shard, dst, scales, m->cfg, st));
+  else CUDA_CHECK(fsdpk::launch_copy_in_bf16(l->shard, dst, l->L.S, m->cfg, st));
+  ps.done();
+}
+
+void validate_grads(const fsdp_layer* l, const void* const* grads, fsdp_dtype_t gd, fsdp_dtype_t rd) {
+  if (!grads) fail(FSDP_ERR_INVALID_ARGUMENT, "full_grads is NULL");
+  for (int p = 0; p < l->P; ++p)
+    if (!grads[p] && l->L.numel[p] > 0) fail(FSDP_ERR_INVALID_ARGUMENT, "full_grads[p] is NULL");
+  if (gd != FSDP_BFLOAT16 && gd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "grad_dtype must be BFLOAT16 or FLOAT32");
+  if (rd != FSDP_BFLOAT16 && rd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "reduce_dtype must be FLOAT32 or BFLOAT16");
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t fsdp_abi_version(void) { return FSDP_B200_ABI_VERSION; }
+const char* fsdp_last_error(void) { return g_last_error.c_str(); }
+
+const char* fsdp_status_string(fsdp_status_t s) {
+  switch (s) {
+    case FSDP_OK: return "FSDP_OK";
+    case FSDP_ERR_INVALID_ARGUMENT: return "FSDP_ERR_INVALID_ARGUMENT";
+    case FSDP_ERR_SHAPE: return "FSDP_ERR_SHAPE";
+    case FSDP_ERR_DTYPE: return "FSDP_ERR_DTYPE";
+    case FSDP_ERR_STATE: return "FSDP_ERR_STATE";
+    case FSDP_ERR_OUT_OF_MEMORY: return "FSDP_ERR_OUT_OF_MEMORY";
+    case FSDP_ERR_CUDA: return "FSDP_ERR_CUDA";
+    case FSDP_ERR_NCCL: return "FSDP_ERR_NCCL";
+    case FSDP_ERR_TIMEOUT: return "FSDP_ERR_TIMEOUT";
+    case FSDP_ERR_NONFINITE: return "FSDP_ERR_NONFINITE";
+    case FSDP_ERR_UNAVAILABLE: return "FSDP_ERR_UNAVAILABLE";
+  }
+  return "FSDP_ERR_UNKNOWN";
+}
+
+fsdp_status_t fsdp_layout_compute(int32_t n_params, const fsdp_param_desc_t* descs, int32_t world_size,
+                                  int32_t rank, fsdp_param_meta_t* out_metas, int64_t* out_S,
+                                  int64_t* out_S_bytes_fp8, uint64_t* out_hash) {
+  return guarded([&] {
+    Layout L;
+    const char* msg = "";
+    fsdp_status_t st = fsdpl::compute_layout(n_params, descs, world_size, rank, &L, &msg);
+    if (st != FSDP_OK) fail(st, msg);
+    if (out_metas) std::copy(L.metas.begin(), L.metas.end(), out_metas);
+    if (out_S) *out_S = L.S;
+    if (out_S_bytes_fp8) *out_S_bytes_fp8 = L.S_bytes_fp8;
+    if (out_hash) *out_hash = L.hash;
+  });
+}
+
+fsdp_status_t fsdp_get_unique_id(uint8_t id[FSDP_UNIQUE_ID_BYTES]) {
+  return guarded([&] {
+    if (!id) fail(FSDP_ERR_INVALID_ARGUMENT, "id is NULL");
+    static_assert(sizeof(ncclUniqueId) == FSDP_UNIQUE_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId u;
+    NCCL_CHECK(ncclGetUniqueId(&u));
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+static void mesh_common_init(fsdp_mesh* m) {
+  int prio_lo = 0, prio_hi = 0;
+  CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  for (cudaStream_t* s : {&m->s_cin, &m->s_ag, &m->s_cout, &m->s_rsc, &m->s_rs})
+    CUDA_CHECK(cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, prio_hi));
+  int sms = 0;
+  CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device));
+  m->cfg.grid_cap = sms * 4;
+  CUDA_CHECK(cudaMalloc(&m->d_err, sizeof(int)));
+  CUDA_CHECK(cudaMemset(m->d_err, 0, sizeof(int)));
+  m->ev_pre_call = new_event();
+  m->ev_pre_done = new_event();
+}
+
+static fsdp_status_t mesh_init_impl(const uint8_t* id, int32_t W, int32_t rank, int32_t dev, bool local,
+                                    fsdp_mesh_t** out) {
+  return guarded([&] {
+    if (!out) fail(FSDP_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (W < 1 || rank < 0 || rank >= W) fail(FSDP_ERR_INVALID_ARGUMENT, "invalid world_size/rank");
+    if (!local && !id) fail(FSDP_ERR_INVALID_ARGUMENT, "unique id is NULL");
+    int ndev = 0;
+    CUDA_CHECK(cudaGetDeviceCount(&ndev));
+    if (dev < 0 || dev >= ndev) fail(FSDP_ERR_INVALID_ARGUMENT, "cuda_device out of range");
+    DeviceGuard g(dev);
+    auto* m = new fsdp_mesh();
+    m->W = W;
+    m->rank = rank;
+    m->device = dev;
+    m->local = local;
+    try {
+      mesh_common_init(m);
+      if (!local) {
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof(u));
+        NCCL_CHECK(ncclCommInitRank(&m->comm_ag, W, u, rank));
+        NCCL_CHECK(ncclCommSplit(m->comm_ag, 0, rank, &m->comm_rs, nullptr));
+      }
+    } catch (...) {
+      fsdp_mesh_destroy(m);
+      throw;
+    }
+    *out = m;
+  });
+}
+
+fsdp_status_t fsdp_mesh_init(const uint8_t id[FSDP_UNIQUE_ID_BYTES], int32_t world_size, int32_t rank,
+                             int32_t cuda_device, fsdp_mesh_t** out) {
+  return mesh_init_impl(id, world_size, rank, cuda_device, false, out);
+}
+
+fsdp_status_t fsdp_mesh_init_local(int32_t world_size, int32_t rank, int32_t cuda_device, fsdp_mesh_t** out) {
+  return mesh_init_impl(nullptr, world_size, rank, cuda_device, true, out);
+}
+
+fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
+  return guarded([&] {
+    if (!m) return;
+    if (!m->layers.empty()) fail(FSDP_ERR_STATE, "destroy all layers of the mesh first");
+    DeviceGuard g(m->device);
+    for (cudaStream_t s : {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs})
+      if (s) cudaStreamSynchronize(s);
+    for (auto* pool : {&m->ag_slots, &m->rs_slots})
+      for (Slot* s : *pool) { s->a.release(); s->b.release(); if (s->free_ev) cudaEventDestroy(s->free_ev); delete s; }
+    clear_presets(m);
+    for (auto& r : m->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : m->ev_pool) cudaEventDestroy(e);
+    cudaFree(m->reg_acc); cudaFree(m->reg_amax); cudaFree(m->reg_scale); cudaFree(m->reg_elig);
+    cudaFree(m->d_err);
+    if (m->ev_pre_call) cudaEventDestroy(m->ev_pre_call);
+    if (m->ev_pre_done) cudaEventDestroy(m->ev_pre_done);
+    if (m->comm_rs) { if (m->aborted) ncclCommAbort(m->comm_rs); else ncclCommDestroy(m->comm_rs); }
+    if (m->comm_ag) { if (m->aborted) ncclCommAbort(m->comm_ag); else ncclCommDestroy(m->comm_ag); }
+    for (cudaStream_t s : {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs})
+      if (s) cudaStreamDestroy(s);
+    delete m;
+  });
+}
+
+fsdp_status_t fsdp_mesh_info(const fsdp_mesh_t* m, int32_t* W, int32_t* rank, int32_t* dev) {
+  return guarded([&] {
+    if (!m) fail(FSDP_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if (W) *W = m->W;
+    if (rank) *rank = m->rank;
+    if (dev) *dev = m->device;
+  });
+}
+
+fsdp_status_t fsdp_mesh_synchronize(fsdp_mesh_t* m, int64_t timeout_ms) {
+  return guarded([&] {
+    check_mesh(m);
+    DeviceGuard g(m->device);
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t ss[] = {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs};
+    for (;;) {
+      bool idle = true;
+      for (cudaStream_t s : ss) {
+        cudaError_t e = cudaStreamQuery(s);
+        if (e == cudaErrorNotReady) { idle = false; continue; }
+        if (e != cudaSuccess) fail(FSDP_ERR_CUDA, std::string("stream error: ") + cudaGetErrorString(e));
+      }
+      if (comm_ready(m)) {
+        for (ncclComm_t c : {m->comm_ag, m->comm_rs}) {
+          ncclResult_t ar = ncclSuccess;
+          NCCL_CHECK(ncclCommGetAsyncError(c, &ar));
+          if (ar != ncclSuccess) {
+            m->aborted = true;
+            fail(FSDP_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(ar));
+          }
+        }
+      }
+      if (idle) break;
+      if (timeout_ms > 0 && std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(timeout_ms)) {
+        m->aborted = true;
+        if (m->comm_ag) ncclCommAbort(m->comm_ag);
+        if (m->comm_rs) ncclCommAbort(m->comm_rs);
+        m->comm_ag = m->comm_rs = nullptr;
+        fail(FSDP_ERR_TIMEOUT, "mesh streams did not drain before the timeout; communicators aborted");
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    int err = 0;
+    CUDA_CHECK(cudaMemcpy(&err, m->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) {
+      CUDA_CHECK(cudaMemset(m->d_err, 0, sizeof(int)));
+      fail(FSDP_ERR_NONFINITE, "non-finite fp8 amax seen by fsdp_precompute_fp8_scales (SPEC.md:38)");
+    }
+  });
+}
+
+fsdp_status_t fsdp_profile_enable(fsdp_mesh_t* m, int32_t on) {
+  return guarded([&] {
+    check_mesh(m);
+    m->prof = on != 0;
+  });
+}
+
+fsdp_status_t fsdp_profile_read(fsdp_mesh_t* m, fsdp_profile_t* out, int32_t reset) {
+  return guarded([&] {
+    check_mesh(m);
+    DeviceGuard g(m->device);
+    prof_collect(m);
+    if (out) *out = m->prof_acc;
+    if (reset) m->prof_acc = fsdp_profile_t{};
+  });
+}
+
+// ------------------------------------------------------------------------- shard
+fsdp_status_t fsdp_shard(fsdp_mesh_t* m, int32_t n, const fsdp_param_desc_t* descs,
+                         const float* const* full_params, fsdp_layer_t** out) {
+  return guarded([&] {
+    check_mesh(m);
+    if (!out) fail(FSDP_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (n < 1) fail(FSDP_ERR_INVALID_ARGUMENT, "a unit needs at least one parameter");
+    Layout L;
+    const char* msg = "";
+    fsdp_status_t st = fsdpl::compute_layout(n, descs, m->W, m->rank, &L, &msg);
+    if (st != FSDP_OK) fail(st, msg);
+    if (n > fsdpk::kMaxPtrs) fail(FSDP_ERR_UNAVAILABLE, "units with more than 512 parameters are not supported in this build");
+    DeviceGuard g(m->device);
+    if (comm_ready(m)) {  // all ranks must agree on the unit ("shape mismatch across members")
+      uint64_t* d = nullptr;
+      CUDA_CHECK(cudaMalloc(&d, sizeof(uint64_t) * m->W));
+      CUDA_CHECK(cudaMemcpy(d + m->rank, &L.hash, sizeof(uint64_t), cudaMemcpyHostToDevice));
+      NCCL_CHECK(ncclAllGather(d + m->rank, d, 8, ncclUint8, m->comm_ag, m->s_ag));
+      std::vector<uint64_t> h(m->W);
+      CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
+      CUDA_CHECK(cudaMemcpy(h.data(), d, sizeof(uint64_t) * m->W, cudaMemcpyDeviceToHost));
+      cudaFree(d);
+      for (uint64_t x : h)
+        if (x != L.hash) fail(FSDP_ERR_SHAPE, "ranks disagree on the unit's parameter shapes (layout hash mismatch)");
+    }
+    auto* l = new fsdp_layer();
+    l->mesh = m;
+    l->P = n;
+    l->descs.assign(descs, descs + n);
+    l->L = std::move(L);
+    try {
+      const Layout& Ly = l->L;
+      const size_t sbytes = sizeof(float) * (size_t)std::max<int64_t>(Ly.S, 16);
+      CUDA_CHECK(cudaMalloc(&l->shard, sbytes));
+      CUDA_CHECK(cudaMalloc(&l->grad, sbytes));
+      CUDA_CHECK(cudaMemset(l->shard, 0, sbytes));
+      CUDA_CHECK(cudaMemset(l->grad, 0, sbytes));
+      if (full_params) {
+        for (int p = 0; p < n; ++p) {
+          const auto& mt = Ly.metas[p];
+          const int64_t cnt = mt.row_count * mt.rest;
+          if (!full_params[p] || cnt == 0) continue;
+          CUDA_CHECK(cudaMemcpy(l->shard + mt.elem_offset, full_params[p] + mt.row_begin * mt.rest,
+                                sizeof(float) * cnt, cudaMemcpyDefault));
+        }
+      }
+      l->t_cin_fp8.upload(fsdpl::tiles_copy_in_fp8(Ly));
+      l->t_cout_bf16.upload(fsdpl::tiles_copy_out(Ly, false, &l->t_cout_bf16.first));
+      l->t_cout_fp8.upload(fsdpl::tiles_copy_out(Ly, true, &l->t_cout_fp8.first));
+      l->t_rsin.upload(fsdpl::tiles_rs_copy_in(Ly, &l->t_rsin.first));
+      for (int p = 0; p < n; ++p) {
+        const int64_t es = Ly.fp8[p] ? 1 : 2;
+        l->bytes_cin_fp8 += Ly.metas[p].padded_numel * (4 + es);
+        l->bytes_cout_bf16 += 2 * 2 * Ly.numel[p];
+        l->bytes_cout_fp8 += 2 * es * Ly.numel[p];
+        l->grad_numel_total += Ly.numel[p];
+      }
+      // fp8 registry entries [reg_base, reg_base + P)
+      ensure_registry(m, m->reg_size + n);
+      l->reg_base = m->reg_size;
+      m->reg_size += n;
+      CUDA_CHECK(cudaMemcpy(m->reg_elig + l->reg_base, Ly.fp8.data(), n, cudaMemcpyHostToDevice));
+      std::vector<int32_t> idx(n);
+      for (int p = 0; p < n; ++p) idx[p] = p;
+      CUDA_CHECK(cudaMalloc(&l->d_idx_local, sizeof(int32_t) * n));
+      CUDA_CHECK(cudaMemcpy(l->d_idx_local, idx.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+      for (cudaEvent_t* e : {&l->ev_call, &l->ev_cin, &l->ev_ag, &l->ev_done, &l->ev_rcall, &l->ev_k5, &l->ev_rs_done})
+        *e = new_event();
+      CUDA_CHECK(cudaDeviceSynchronize());
+    } catch (...) {
+      m->layers.push_back(l);
+      fsdp_layer_destroy(l);
+      throw;
+    }
+    m->layers.push_back(l);
+    *out = l;
+  });
+}
+
+fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* l) {
+  return guarded([&] {
+    if (!l) return;
+    fsdp_mesh* m = l->mesh;
+    if (l->state != SHARDED) fail(FSDP_ERR_STATE, "reshard the layer before destroying it");
+    DeviceGuard g(m->device);
+    for (cudaStream_t s : {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs}) cudaStreamSynchronize(s);
+    cudaFree(l->shard);
+    cudaFree(l->grad);
+    cudaFree(l->d_idx_local);
+    l->t_cin_fp8.release(); l->t_cout_bf16.release(); l->t_cout_fp8.release(); l->t_rsin.release();
+    for (cudaEvent_t e : {l->ev_call, l->ev_cin, l->ev_ag, l->ev_done, l->ev_rcall, l->ev_k5, l->ev_rs_done})
+      if (e) cudaEventDestroy(e);
+    m->layers.erase(std::remove(m->layers.begin(), m->layers.end(), l), m->layers.end());
+    clear_presets(m);
+    delete l;
+  });
+}
+
+fsdp_status_t fsdp_layer_info(const fsdp_layer_t* l, int32_t* n, int64_t* S, int64_t* Sb) {
+  return guarded([&] {
+    if (!l) fail(FSDP_ERR_INVALID_ARGUMENT, "layer is NULL");
+    if (n) *n = l->P;
+    if (S) *S = l->L.S;
+    if (Sb) *Sb = l->L.S_bytes_fp8;
+  });
+}
+
+fsdp_status_t fsdp_param_meta(const fsdp_layer_t* l, int32_t p, fsdp_param_meta_t* out) {
+  return guarded([&] {
+    if (!l) fail(FSDP_ERR_INVALID_ARGUMENT, "layer is NULL");
+    check_param(l, p);
+    if (!out) fail(FSDP_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = l->L.metas[p];
+  });
+}
+
+fsdp_status_t fsdp_sharded_param(const fsdp_layer_t* l, int32_t p, float** dev) {
+  return guarded([&] {
+    if (!l || !dev) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL argument");
+    check_param(l, p);
+    *dev = l->shard + l->L.metas[p].elem_offset;
+  });
+}
+
+fsdp_status_t fsdp_sharded_flat(const fsdp_layer_t* l, float** dev) {
+  return guarded([&] {
+    if (!l || !dev) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL argument");
+    *dev = l->shard;
+  });
+}
+
+// ------------------------------------------------------------------------- fp8 scales
+fsdp_status_t fsdp_precompute_fp8_scales(fsdp_mesh_t* m, fsdp_layer_t* const* layers, int32_t n, void* stream) {
+  return guarded([&] {
+    check_mesh(m);
+    if (n < 0 || (n > 0 && !layers)) fail(FSDP_ERR_INVALID_ARGUMENT, "layers is NULL");
+    for (int i = 0; i < n; ++i) {
+      if (!layers[i] || layers[i]->mesh != m) fail(FSDP_ERR_INVALID_ARGUMENT, "layer does not belong to this mesh");
+    }
+    if (m->local && m->W > 1) fail(FSDP_ERR_UNAVAILABLE, "local mesh with world_size > 1 has no communicator");
+    DeviceGuard g(m->device);
+    std::vector<fsdp_layer*> key(layers, layers + n);
+    fsdp_mesh::PreSet* ps = nullptr;
+    for (auto* c : m->presets) if (c->layers == key) { ps = c; break; }
+    if (!ps) {
+      ps = new fsdp_mesh::PreSet();
+      ps->layers = key;
+      std::vector<Tile> tiles;
+      std::vector<int32_t> idx;
+      for (fsdp_layer* l : key) {
+        fsdpl::append_tiles_amax(l->L, l->shard, l->reg_base, &tiles);
+        for (int p = 0; p < l->P; ++p) {
+          idx.push_back(l->reg_base + p);
+          if (l->L.fp8[p]) ps->bytes += 4 * l->L.metas[p].padded_numel;
+        }
+      }
+      ps->tiles.upload(tiles);
+      ps->nidx = (int)idx.size();
+      if (ps->nidx) {
+        CUDA_CHECK(cudaMalloc(&ps->idx, sizeof(int32_t) * idx.size()));
+        CUDA_CHECK(cudaMemcpy(ps->idx, idx.data(), sizeof(int32_t) * idx.size(), cudaMemcpyHostToDevice));
+      }
+      m->presets.push_back(ps);
+    }
+    // precompute runs on s_rs (the stream owning comm_rs), ordered after `stream`, and
+    // `stream` waits for it: K1 over all layers -> all-reduce(max) -> K1b
+    cudaStream_t st = as_stream(stream);
+    CUDA_CHECK(cudaEventRecord(m->ev_pre_call, st));
+    CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, m->ev_pre_call, 0));
+    {
+      ProfScope pa(m, FSDP_PROF_AMAX, m->s_rs, ps->bytes);
+      CUDA_CHECK(fsdpk::launch_amax(ps->tiles.d, ps->tiles.n, m->reg_acc, m->cfg, m->s_rs));
+      pa.done();
+    }
+    if (comm_ready(m) && m->reg_size > 0) {
+      // max of non-negative fp32 bit patterns == uint32 max (NaN patterns propagate)
+      ProfScope pr(m, FSDP_PROF_ALL_REDUCE, m->s_rs, (int64_t)4 * m->reg_size);
+      NCCL_CHECK(ncclAllReduce(m->reg_acc, m->reg_acc, (size_t)m->reg_size, ncclUint32, ncclMax, m->comm_rs, m->s_rs));
+      pr.done();
+    }
+    {
+      ProfScope pk(m, FSDP_PROF_SCALE, m->s_rs, (int64_t)ps->nidx * 12);
+      CUDA_CHECK(fsdpk::launch_fp8_scale(ps->idx, ps->nidx, m->reg_acc, m->reg_amax, m->reg_scale, m->reg_elig,
+                                         m->d_err, true, m->s_rs));
+      pk.done();
+    }
+    CUDA_CHECK(cudaEventRecord(m->ev_pre_done, m->s_rs));
+    CUDA_CHECK(cudaStreamWaitEvent(st, m->ev_pre_done, 0));
+  });
+}
+
+fsdp_status_t fsdp_fp8_scales(const fsdp_layer_t* l, const float** scales_dev, const float** amax_dev) {
+  return guarded([&] {
+    check_layer(l);
+    if (scales_dev) *scales_dev = l->mesh->reg_scale + l->reg_base;
+    if (amax_dev) *amax_dev = l->mesh->reg_amax + l->reg_base;
+  });
+}
+
+// ------------------------------------------------------------------------- unshard
+fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales, void* compute) {
+  return guarded([&] {
+    check_layer(l);
+    fsdp_mesh* m = l->mesh;
+    if (l->state != SHARDED) fail(FSDP_ERR_STATE, "layer is already unsharded (reshard it first)");
+    if (dt != FSDP_BFLOAT16 && dt != FSDP_FLOAT8_E4M3FN) fail(FSDP_ERR_DTYPE, "param_dtype must be BFLOAT16 or FLOAT8_E4M3FN");
+    if (m->local && m->W > 1) fail(FSDP_ERR_UNAVAILABLE, "local mesh with world_size > 1 has no communicator");
+    const bool fp8 = dt == FSDP_FLOAT8_E4M3FN;
+    if (fp8 && !scales) scales = m->reg_scale + l->reg_base;
+    DeviceGuard g(m->device);
+    const int64_t sb = slot_bytes(l, fp8);
+    const int64_t arena = fp8 ? l->L.arena_fp8 : l->L.arena_bf16;
+    Slot* slot = acquire_slot(m, m->ag_slots, (size_t)(m->W * sb), (size_t)arena, 1);
+    cudaStream_t cs = as_stream(compute);
+    // copy-in after the caller's prior work (optimizer step on the shard) and after the
+    // previous user of this buffer released it
+    CUDA_CHECK(cudaEventRecord(l->ev_call, cs));
+    CUDA_CHECK(cudaStreamWaitEvent(m->s_cin, l->ev_call, 0));
+    if (slot->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_cin, slot->free_ev, 0));
+    uint8_t* ag = (uint8_t*)slot->a.p;
+    do_copy_in(l, fp8, scales, ag + (size_t)m->rank * sb, m->s_cin);
+    CUDA_CHECK(cudaEventRecord(l->ev_cin, m->s_cin));
+    cudaEvent_t ready = l->ev_cin;
+    if (comm_ready(m)) {
+      CUDA_CHECK(cudaStreamWaitEvent(m->s_ag, l->ev_cin, 0));
+      ProfScope pg(m, FSDP_PROF_ALL_GATHER, m->s_ag, (int64_t)(m->W - 1) * sb);
+      NCCL_CHECK(ncclAllGather(ag + (size_t)m->rank * sb, ag, (size_t)sb, ncclUint8, m->comm_ag, m->s_ag));
+      pg.done();
+      CUDA_CHECK(cudaEventRecord(l->ev_ag, m->s_ag));
+      ready = l->ev_ag;
+    }
+    CUDA_CHECK(cudaStreamWaitEvent(m->s_cout, ready, 0));
+    std::vector<void*> outs(l->P);
+    const auto& uoff = fp8 ? l->L.uoff_fp8 : l->L.uoff_bf16;
+    for (int p = 0; p < l->P; ++p) outs[p] = (uint8_t*)slot->b.p + uoff[p];
+    {
+      ProfScope po(m, FSDP_PROF_COPY_OUT, m->s_cout, fp8 ? l->bytes_cout_fp8 : l->bytes_cout_bf16);
+      launch_copy_out_all(l, fp8, ag, outs.data(), m->s_cout);
+      po.done();
+    }
+    CUDA_CHECK(cudaEventRecord(l->ev_done, m->s_cout));
+    l->slot = slot;
+    l->ushard_dtype = dt;
+    l->state = UNSHARDING;
+  });
+}
+
+fsdp_status_t fsdp_wait_unshard(fsdp_layer_t* l, void* compute) {
+  return guarded([&] {
+    check_layer(l);
+    if (l->state == UNSHARDED) return;
+    if (l->state != UNSHARDING) fail(FSDP_ERR_STATE, "fsdp_wait_unshard without fsdp_unshard");
+    DeviceGuard g(l->mesh->device);
+    CUDA_CHECK(cudaStreamWaitEvent(as_stream(compute), l->ev_done, 0));
+    l->state = UNSHARDED;
+  });
+}
+
+fsdp_status_t fsdp_all_gather_params(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales, void* compute) {
+  fsdp_status_t st = fsdp_unshard(l, dt, scales, compute);
+  if (st != FSDP_OK) return st;
+  return fsdp_wait_unshard(l, compute);
+}
+
+fsdp_status_t fsdp_unsharded_param(const fsdp_layer_t* l, int32_t p, void** dev, fsdp_dtype_t* dt) {
+  return guarded([&] {
+    check_layer(l);
+    check_param(l, p);
+    if (!dev) fail(FSDP_ERR_INVALID_ARGUMENT, "dev is NULL");
+    if (l->state != UNSHARDED) fail(FSDP_ERR_STATE, "unsharded params are valid only between wait_unshard and reshard");
+    const bool fp8 = l->ushard_dtype == FSDP_FLOAT8_E4M3FN;
+    const auto& uoff = fp8 ? l->L.uoff_fp8 : l->L.uoff_bf16;
+    *dev = (uint8_t*)l->slot->b.p + uoff[p];
+    if (dt) *dt = (fp8 && l->L.fp8[p]) ? FSDP_FLOAT8_E4M3FN : FSDP_BFLOAT16;
+  });
+}
+
+fsdp_status_t fsdp_reshard(fsdp_layer_t* l, void* compute) {
+  return guarded([&] {
+    check_layer(l);
+    if (l->state == SHARDED) return;
+    DeviceGuard g(l->mesh->device);
+    cudaStream_t cs = as_stream(compute);
+    if (l->state == UNSHARDING) CUDA_CHECK(cudaStreamWaitEvent(cs, l->ev_done, 0));
+    // the buffer is free once everything enqueued on `compute` so far (the consumers of
+    // the unsharded params) has run; the next user's copy-in waits on this event
+    release_slot(l->slot, cs);
+    l->slot = nullptr;
+    l->state = SHARDED;
+  });
+}
+
+// ------------------------------------------------------------------------- reduce-scatter
+fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grads, fsdp_dtype_t gd,
+                                        fsdp_dtype_t rd, int32_t mean, int32_t accumulate, void* compute) {
+  return guarded([&] {
+    check_layer(l);
+    fsdp_mesh* m = l->mesh;
+    validate_grads(l, grads, gd, rd);
+    if (l->rs_pending) fail(FSDP_ERR_STATE, "previous reduce_scatter_grads of this layer was not waited");
+    if (m->local && m->W > 1) fail(FSDP_ERR_UNAVAILABLE, "local mesh with world_size > 1 has no communicator");
+    DeviceGuard g(m->device);
+    const bool obf = rd == FSDP_BFLOAT16;
+    const int64_t osz = obf ? 2 : 4;
+    const int64_t S = l->L.S;
+    // fp32, no accumulation: the reduce-scatter (or, at W=1, K5 itself) writes straight
+    // into the layer's grad buffer — the zero-copy "view" copy-out
+    const bool direct = !obf && !accumulate;
+    const bool need_in = comm_ready(m) || !direct;
+    Slot* slot = acquire_slot(m, m->rs_slots, need_in ? (size_t)(m->W * S * osz) : 0,
+                              (comm_ready(m) && !direct) ? (size_t)(S * osz) : 0, 2);
+    cudaStream_t cs = as_stream(compute);
+    CUDA_CHECK(cudaEventRecord(l->ev_rcall, cs));
+    CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, l->ev_rcall, 0));
+    if (slot->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, slot->free_ev, 0));
+    void* rs_in = need_in ? slot->a.p : (void*)l->grad;
+    {
+      ProfScope pk(m, FSDP_PROF_RS_COPY_IN, m->s_rsc,
+                   l->grad_numel_total * dtype_size(gd) + (int64_t)m->W * S * osz);
+      launch_rs_copy_in_all(l, grads, gd == FSDP_BFLOAT16, rs_in, obf, mean != 0, m->s_rsc);
+      pk.done();
+    }
+    CUDA_CHECK(cudaEventRecord(l->ev_k5, m->s_rsc));
+    CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, l->ev_k5, 0));
+    const void* rs_out = rs_in;   // W == 1: the reduce-scatter is the identity
+    if (comm_ready(m)) {
+      void* out = direct ? (void*)l->grad : slot->b.p;
+      ProfScope pr(m, FSDP_PROF_REDUCE_SCATTER, m->s_rs, (int64_t)(m->W - 1) * S * osz);
+      NCCL_CHECK(ncclReduceScatter(rs_in, out, (size_t)S, obf ? ncclBfloat16 : ncclFloat32, ncclSum, m->comm_rs,
+                                   m->s_rs));
+      pr.done();
+      rs_out = out;
+    }
+    if (!direct) {
+      ProfScope po(m, FSDP_PROF_RS_COPY_OUT, m->s_rs, S * (osz + 4 + (accumulate ? 4 : 0)));
+      CUDA_CHECK(fsdpk::launch_rs_copy_out(rs_out, obf, l->grad, accumulate != 0, S, m->cfg, m->s_rs));
+      po.done();
+    }
+    CUDA_CHECK(cudaEventRecord(l->ev_rs_done, m->s_rs));
+    release_slot(slot, m->s_rs);
+    l->rs_pending = true;
+  });
+}
+
+fsdp_status_t fsdp_wait_reduce_scatter(fsdp_layer_t* l, void* compute) {
+  return guarded([&] {
+    check_layer(l);
+    if (!l->rs_pending) return;
+    DeviceGuard g(l->mesh->device);
+    CUDA_CHECK(cudaStreamWaitEvent(as_stream(compute), l->ev_rs_done, 0));
+    l->rs_pending = false;
+  });
+}
+
+fsdp_status_t fsdp_sharded_grad(const fsdp_layer_t* l, int32_t p, float** dev) {
+  return guarded([&] {
+    if (!l || !dev) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL argument");
+    check_param(l, p);
+    *dev = l->grad + l->L.metas[p].elem_offset;
+  });
+}
+
+fsdp_status_t fsdp_sharded_grad_flat(const fsdp_layer_t* l, float** dev) {
+  return guarded([&] {
+    if (!l || !dev) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL argument");
+    *dev = l->grad;
+  });
+}
+
+fsdp_status_t fsdp_zero_grad(fsdp_layer_t* l, void* stream) {
+  return guarded([&] {
+    check_layer(l);
+    DeviceGuard g(l->mesh->device);
+    CUDA_CHECK(cudaMemsetAsync(l->grad, 0, sizeof(float) * (size_t)l->L.S, as_stream(stream)));
+  });
+}
+
+// ------------------------------------------------------------------------- stage entry points
+fsdp_status_t fsdp_stage_copy_in(const fsdp_layer_t* lc, fsdp_dtype_t dt, const float* scales, void* slot,
+                                 void* stream) {
+  return guarded([&] {
+    fsdp_layer* l = const_cast<fsdp_layer*>(lc);
+    check_layer(l);
+    if (!slot) fail(FSDP_ERR_INVALID_ARGUMENT, "ag_slot is NULL");
+    if (dt != FSDP_BFLOAT16 && dt != FSDP_FLOAT8_E4M3FN) fail(FSDP_ERR_DTYPE, "param_dtype must be BFLOAT16 or FLOAT8_E4M3FN");
+    const bool fp8 = dt == FSDP_FLOAT8_E4M3FN;
+    if (fp8 && !scales) scales = l->mesh->reg_scale + l->reg_base;
+    DeviceGuard g(l->mesh->device);
+    do_copy_in(l, fp8, scales, slot, as_stream(stream));
+  });
+}
+
+fsdp_status_t fsdp_stage_copy_out(const fsdp_layer_t* lc, fsdp_dtype_t dt, const void* ag, void* const* outs,
+                                  void* stream) {
+  return guarded([&] {
+    fsdp_layer* l = const_cast<fsdp_layer*>(lc);
+    check_layer(l);
+    if (!ag || !outs) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL buffer");
+    for (int p = 0; p < l->P; ++p)
+      if (!outs[p] && l->L.numel[p] > 0) fail(FSDP_ERR_INVALID_ARGUMENT, "full_out[p] is NULL");
+    if (dt != FSDP_BFLOAT16 && dt != FSDP_FLOAT8_E4M3FN) fail(FSDP_ERR_DTYPE, "param_dtype must be BFLOAT16 or FLOAT8_E4M3FN");
+    const bool fp8 = dt == FSDP_FLOAT8_E4M3FN;
+    DeviceGuard g(l->mesh->device);
+    ProfScope po(l->mesh, FSDP_PROF_COPY_OUT, as_stream(stream), fp8 ? l->bytes_cout_fp8 : l->bytes_cout_bf16);
+    launch_copy_out_all(l, fp8, ag, outs, as_stream(stream));
+    po.done();
+  });
+}
+
+fsdp_status_t fsdp_stage_local_amax(const fsdp_layer_t* lc, float* amax_out, void* stream) {
+  return guarded([&] {
+    fsdp_layer* l = const_cast<fsdp_layer*>(lc);
+    check_layer(l);
+    if (!amax_out) fail(FSDP_ERR_INVALID_ARGUMENT, "amax_out is NULL");
+    DeviceGuard g(l->mesh->device);
+    cudaStream_t st = as_stream(stream);
+    std::vector<Tile> tiles;
+    fsdpl::append_tiles_amax(l->L, l->shard, 0, &tiles);
+    DevTiles T;
+    T.upload(tiles);   // synchronous upload (test entry point, not on the hot path)
+    CUDA_CHECK(cudaMemsetAsync(amax_out, 0, sizeof(float) * l->P, st));
+    cudaError_t e = fsdpk::launch_amax(T.d, T.n, reinterpret_cast<uint32_t*>(amax_out), l->mesh->cfg, st);
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    T.release();
+    CUDA_CHECK(e);
+  });
+}
+
+fsdp_status_t fsdp_stage_fp8_scale(const fsdp_layer_t* lc, const float* amax, float* scale_out, void* stream) {
+  return guarded([&] {
+    fsdp_layer* l = const_cast<fsdp_layer*>(lc);
+    check_layer(l);
+    if (!amax || !scale_out) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL buffer");
+    DeviceGuard g(l->mesh->device);
+    // amax is read as non-negative fp32 bit patterns; amax_out == amax (rewritten as is)
+    CUDA_CHECK(fsdpk::launch_fp8_scale(l->d_idx_local, l->P, (uint32_t*)const_cast<float*>(amax),
+                                       const_cast<float*>(amax), scale_out, l->mesh->reg_elig + l->reg_base,
+                                       l->mesh->d_err, false, as_stream(stream)));
+  });
+}
+
+fsdp_status_t fsdp_stage_rs_copy_in(const fsdp_layer_t* lc, const void* const* grads, fsdp_dtype_t gd,
+                                    fsdp_dtype_t rd, int32_t mean, void* rs_in, void* stream) {
+  return guarded([&] {
+    fsdp_layer* l = const_cast<fsdp_layer*>(lc);
+    check_layer(l);
+    validate_grads(l, grads, gd, rd);
+    if (!rs_in) fail(FSDP_ERR_INVALID_ARGUMENT, "rs_in is NULL");
+    DeviceGuard g(l->mesh->device);
+    const int64_t osz = rd == FSDP_BFLOAT16 ? 2 : 4;
+    ProfScope pk(l->mesh, FSDP_PROF_RS_COPY_IN, as_stream(stream),
+                 l->grad_numel_total * dtype_size(gd) + (int64_t)l->mesh->W * l->L.S * osz);
+    launch_rs_copy_in_all(l, grads, gd == FSDP_BFLOAT16, rs_in, rd == FSDP_BFLOAT16, mean != 0, as_stream(stream));
+    pk.done();
+  });
+}
+
+fsdp_status_t fsdp_stage_rs_copy_out(fsdp_layer_t* l, const void* rs_out, fsdp_dtype_t rd, int32_t accumulate,
+                                     void* stream) {
+  return guarded([&] {
+    check_layer(l);
+    if (!rs_out) fail(FSDP_ERR_INVALID_ARGUMENT, "rs_out is NULL");
+    if (rd != FSDP_BFLOAT16 && rd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "reduce_dtype must be FLOAT32 or BFLOAT16");
+    DeviceGuard g(l->mesh->device);
+    const int64_t osz = rd == FSDP_BFLOAT16 ? 2 : 4;
+    ProfScope po(l->mesh, FSDP_PROF_RS_COPY_OUT, as_stream(stream), l->L.S * (osz + 4 + (accumulate ? 4 : 0)));
+    CUDA_CHECK(fsdpk::launch_rs_copy_out(rs_out, rd == FSDP_BFLOAT16, l->grad, accumulate != 0, l->L.S,
+                                         l->mesh->cfg, as_stream(stream)));
+    po.done();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,472 @@
+// Hand-written sm_100a kernels of the FSDP2 per-parameter Shard(0) step.
+//
+//   K2 copy-in bf16   (P:417 bf16 all-gather; P:464 multi-tensor all-gather copy-in)
+//   K3 copy-in fp8    (P:157 Float8 all-gather with per-tensor scales)
+//   K4 copy-out       (rank-major all-gather output -> per-parameter tensors)
+//   K5 RS copy-in     (P:466 single pre-division by W; P:544 fp32 reduce-scatter)
+//   K6 RS copy-out    (accumulate / widen into the fp32 sharded gradient)
+//   K1 amax, K1b scale (P:157 dynamic tensorwise scaling)
+//
+// All of it is HBM-bound streaming work, so no tensor cores: the design rules are
+// 128-bit coalesced accesses, several independent 16-byte loads in flight per thread,
+// persistent grids sized to the SM count, and per-layer tile tables so the ragged
+// per-parameter segments become uniform ~64 KB work items.  Compiled without fast
+// math: IEEE division, no flush-to-zero (bit-exactness vs the oracle depends on it).
+#include "kernels.h"
+
+#include <cuda_bf16.h>
+
+namespace fsdpk {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// fp32 pair -> packed bf16x2, round to nearest even (cvt.rn.bf16x2.f32; lo in low half).
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// fp32 pair -> packed e4m3x2 with saturation to +-448 (cvt.rn.satfinite; lo in low byte).
+__device__ __forceinline__ uint32_t pack_e4m3x2(float lo, float hi) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return (uint32_t)r;
+}
+
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// 16 bytes starting at byte phase k (1..15) of the 32 bytes a:b.
+__device__ __forceinline__ uint4 extract16(uint4 a, uint4 b, uint32_t k) {
+  const uint32_t sh = (k & 3u) * 8u;
+  uint4 r;
+  switch (k >> 2) {
+    case 0:
+      r.x = __funnelshift_r(a.x, a.y, sh); r.y = __funnelshift_r(a.y, a.z, sh);
+      r.z = __funnelshift_r(a.z, a.w, sh); r.w = __funnelshift_r(a.w, b.x, sh);
+      break;
+    case 1:
+      r.x = __funnelshift_r(a.y, a.z, sh); r.y = __funnelshift_r(a.z, a.w, sh);
+      r.z = __funnelshift_r(a.w, b.x, sh); r.w = __funnelshift_r(b.x, b.y, sh);
+      break;
+    case 2:
+      r.x = __funnelshift_r(a.z, a.w, sh); r.y = __funnelshift_r(a.w, b.x, sh);
+      r.z = __funnelshift_r(b.x, b.y, sh); r.w = __funnelshift_r(b.y, b.z, sh);
+      break;
+    default:
+      r.x = __funnelshift_r(a.w, b.x, sh); r.y = __funnelshift_r(b.x, b.y, sh);
+      r.z = __funnelshift_r(b.y, b.z, sh); r.w = __funnelshift_r(b.z, b.w, sh);
+      break;
+  }
+  return r;
+}
+
+// 16 bytes at an arbitrary address whose phase within 16 B is `k` (uniform per tile).
+// For k != 0 two aligned loads are made; the second aligned block always contains at
+// least one requested byte, so it lies inside the (>= 16 B granular) allocation.
+template <bool kAligned>
+__device__ __forceinline__ uint4 load16(const uint8_t* p, uint32_t k) {
+  if (kAligned) return ld_stream(p);
+  const uint8_t* a = p - k;
+  return extract16(ld_stream(a), ld_stream(a + 16), k);
+}
+
+// ------------------------------------------------------------------- K2 copy-in bf16
+__global__ void __launch_bounds__(kThreads) k_copy_in_bf16(const float4* __restrict__ src,
+                                                           uint4* __restrict__ dst, int64_t n8) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  for (; i + (kUnroll - 1) * stride < n8; i += kUnroll * stride) {
+    uint4 a[kUnroll], b[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      a[u] = ld_stream(src + 2 * (i + u * stride));
+      b[u] = ld_stream(src + 2 * (i + u * stride) + 1);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      uint4 o;
+      o.x = pack_bf16x2(__uint_as_float(a[u].x), __uint_as_float(a[u].y));
+      o.y = pack_bf16x2(__uint_as_float(a[u].z), __uint_as_float(a[u].w));
+      o.z = pack_bf16x2(__uint_as_float(b[u].x), __uint_as_float(b[u].y));
+      o.w = pack_bf16x2(__uint_as_float(b[u].z), __uint_as_float(b[u].w));
+      st_v4(dst + i + u * stride, o);
+    }
+  }
+  for (; i < n8; i += stride) {
+    uint4 a = ld_stream(src + 2 * i), b = ld_stream(src + 2 * i + 1);
+    uint4 o;
+    o.x = pack_bf16x2(__uint_as_float(a.x), __uint_as_float(a.y));
+    o.y = pack_bf16x2(__uint_as_float(a.z), __uint_as_float(a.w));
+    o.z = pack_bf16x2(__uint_as_float(b.x), __uint_as_float(b.y));
+    o.w = pack_bf16x2(__uint_as_float(b.z), __uint_as_float(b.w));
+    st_v4(dst + i, o);
+  }
+}
+
+// ------------------------------------------------------------------- K3 copy-in fp8
+__global__ void __launch_bounds__(kThreads) k_copy_in_fp8(const Tile* __restrict__ tiles, int ntiles,
+                                                          const float* __restrict__ shard,
+                                                          uint8_t* __restrict__ slot,
+                                                          const float* __restrict__ scales) {
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    const float* src = shard + tl.src;   // 16-element aligned
+    uint8_t* dst = slot + tl.dst;        // 16-byte aligned
+    const uint32_t n = tl.n;
+    if (tl.kind == TK_FP8) {
+      const float s = scales[tl.param];
+      const uint32_t nv = n / 16;
+      for (uint32_t v = threadIdx.x; v < nv; v += kThreads) {
+        uint4 q[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) q[j] = ld_stream(src + 16 * v + 4 * j);
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t lo = pack_e4m3x2(__fmul_rn(__uint_as_float(q[j].x), s),
+                                          __fmul_rn(__uint_as_float(q[j].y), s));
+          const uint32_t hi = pack_e4m3x2(__fmul_rn(__uint_as_float(q[j].z), s),
+                                          __fmul_rn(__uint_as_float(q[j].w), s));
+          w[j] = lo | (hi << 16);
+        }
+        st_v4(dst + 16 * v, make_uint4(w[0], w[1], w[2], w[3]));
+      }
+      for (uint32_t e = nv * 16 + threadIdx.x; e < n; e += kThreads) {
+        const float x = __fmul_rn(src[e], s);
+        dst[e] = (uint8_t)(pack_e4m3x2(x, 0.0f) & 0xFFu);
+      }
+    } else {  // bf16 param inside a float8 unit
+      const uint32_t nv = n / 8;
+      uint16_t* d16 = reinterpret_cast<uint16_t*>(dst);
+      for (uint32_t v = threadIdx.x; v < nv; v += kThreads) {
+        const uint4 a = ld_stream(src + 8 * v), b = ld_stream(src + 8 * v + 4);
+        uint4 o;
+        o.x = pack_bf16x2(__uint_as_float(a.x), __uint_as_float(a.y));
+        o.y = pack_bf16x2(__uint_as_float(a.z), __uint_as_float(a.w));
+        o.z = pack_bf16x2(__uint_as_float(b.x), __uint_as_float(b.y));
+        o.w = pack_bf16x2(__uint_as_float(b.z), __uint_as_float(b.w));
+        st_v4(d16 + 8 * v, o);
+      }
+      for (uint32_t e = nv * 8 + threadIdx.x; e < n; e += kThreads)
+        d16[e] = (uint16_t)(pack_bf16x2(src[e], 0.0f) & 0xFFFFu);
+    }
+  }
+}
+
+// ------------------------------------------------------------------- K4 copy-out
+template <bool kAligned>
+__device__ __forceinline__ void copy_body(const uint8_t* s, uint8_t* d, uint32_t nv, uint32_t k) {
+  uint32_t v = threadIdx.x;
+  for (; v + (kUnroll - 1) * kThreads < nv; v += kUnroll * kThreads) {
+    uint4 r[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) r[u] = load16<kAligned>(s + 16 * (v + u * kThreads), k);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) st_v4(d + 16 * (v + u * kThreads), r[u]);
+  }
+  for (; v < nv; v += kThreads) st_v4(d + 16 * v, load16<kAligned>(s + 16 * v, k));
+}
+
+__global__ void __launch_bounds__(kThreads) k_copy_out(const Tile* __restrict__ tiles, int ntiles,
+                                                       const uint8_t* __restrict__ ag, PtrArray outs) {
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    const uint8_t* s = ag + tl.src;
+    uint8_t* d = (uint8_t*)outs.p[tl.param] + tl.dst;
+    uint32_t n = tl.n;
+    uint32_t head = (uint32_t)((16u - ((uintptr_t)d & 15u)) & 15u);
+    if (head > n) head = n;
+    if (threadIdx.x < head) d[threadIdx.x] = s[threadIdx.x];
+    s += head; d += head; n -= head;
+    const uint32_t nv = n >> 4;
+    const uint32_t k = (uint32_t)((uintptr_t)s & 15u);
+    if (k == 0) copy_body<true>(s, d, nv, 0);
+    else copy_body<false>(s, d, nv, k);
+    for (uint32_t e = nv * 16 + threadIdx.x; e < n; e += kThreads) d[e] = s[e];
+  }
+}
+
+// ------------------------------------------------------------------- K5 RS copy-in
+struct DivW {
+  float w, inv;
+  bool pow2, mean;
+  __device__ __forceinline__ float operator()(float x) const {
+    if (!mean) return x;
+    return pow2 ? __fmul_rn(x, inv) : __fdiv_rn(x, w);   // both equal IEEE x / W
+  }
+};
+
+// 8 consecutive grad elements (as fp32) at byte address p with phase k.
+template <bool kGradBf16, bool kAligned>
+__device__ __forceinline__ void load8(const uint8_t* p, uint32_t k, float (&x)[8]) {
+  if (kGradBf16) {
+    const uint4 a = load16<kAligned>(p, k);
+    x[0] = bf16_lo(a.x); x[1] = bf16_hi(a.x); x[2] = bf16_lo(a.y); x[3] = bf16_hi(a.y);
+    x[4] = bf16_lo(a.z); x[5] = bf16_hi(a.z); x[6] = bf16_lo(a.w); x[7] = bf16_hi(a.w);
+  } else {
+    const uint4 a = load16<kAligned>(p, k), b = load16<kAligned>(p + 16, k);
+    x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y);
+    x[2] = __uint_as_float(a.z); x[3] = __uint_as_float(a.w);
+    x[4] = __uint_as_float(b.x); x[5] = __uint_as_float(b.y);
+    x[6] = __uint_as_float(b.z); x[7] = __uint_as_float(b.w);
+  }
+}
+
+template <bool kOutBf16>
+__device__ __forceinline__ void store8(uint8_t* d, const float (&y)[8]) {
+  if (kOutBf16) {
+    st_v4(d, make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]), pack_bf16x2(y[4], y[5]),
+                        pack_bf16x2(y[6], y[7])));
+  } else {
+    st_v4(d, make_uint4(__float_as_uint(y[0]), __float_as_uint(y[1]), __float_as_uint(y[2]),
+                        __float_as_uint(y[3])));
+    st_v4(d + 16, make_uint4(__float_as_uint(y[4]), __float_as_uint(y[5]), __float_as_uint(y[6]),
+                             __float_as_uint(y[7])));
+  }
+}
+
+template <bool kGradBf16, bool kOutBf16, bool kAligned>
+__device__ __forceinline__ void rs_body(const uint8_t* s, uint8_t* d, uint32_t nv, uint32_t k, DivW div) {
+  constexpr uint32_t gs = kGradBf16 ? 16 : 32;   // source bytes per 8 elements
+  constexpr uint32_t os = kOutBf16 ? 16 : 32;    // output bytes per 8 elements
+  uint32_t v = threadIdx.x;
+  for (; v + (kUnroll - 1) * kThreads < nv; v += kUnroll * kThreads) {
+    float x[kUnroll][8];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) load8<kGradBf16, kAligned>(s + gs * (v + u * kThreads), k, x[u]);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[u][j] = div(x[u][j]);
+      store8<kOutBf16>(d + os * (v + u * kThreads), x[u]);
+    }
+  }
+  for (; v < nv; v += kThreads) {
+    float x[8];
+    load8<kGradBf16, kAligned>(s + gs * v, k, x);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = div(x[j]);
+    store8<kOutBf16>(d + os * v, x);
+  }
+}
+
+template <bool kGradBf16, bool kOutBf16>
+__global__ void __launch_bounds__(kThreads) k_rs_copy_in(const Tile* __restrict__ tiles, int ntiles,
+                                                         PtrArray grads, uint8_t* __restrict__ rs_in,
+                                                         DivW div) {
+  constexpr uint32_t gsz = kGradBf16 ? 2 : 4;
+  constexpr uint32_t osz = kOutBf16 ? 2 : 4;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    uint8_t* d = rs_in + tl.dst * osz;   // 16-byte aligned (tiles start at 16-element offsets)
+    const uint32_t n = tl.n;             // multiple of 16
+    const uint32_t ns = tl.pad;          // valid source elements
+    const uint32_t nv = ns / 8;
+    const uint8_t* s = (const uint8_t*)grads.p[tl.param] + tl.src * gsz;
+    if (nv > 0) {
+      const uint32_t k = (uint32_t)((uintptr_t)s & 15u);
+      if (k == 0) rs_body<kGradBf16, kOutBf16, true>(s, d, nv, 0, div);
+      else rs_body<kGradBf16, kOutBf16, false>(s, d, nv, k, div);
+    }
+    const uint32_t zb = min((ns + 7u) & ~7u, n);
+    for (uint32_t e = nv * 8 + threadIdx.x; e < zb; e += kThreads) {
+      float x = 0.0f;
+      if (e < ns) {
+        if (kGradBf16) x = __uint_as_float(((uint32_t)((const uint16_t*)s)[e]) << 16);
+        else x = ((const float*)s)[e];
+        x = div(x);
+      }
+      if (kOutBf16) ((uint16_t*)d)[e] = (uint16_t)(pack_bf16x2(x, 0.0f) & 0xFFFFu);
+      else ((float*)d)[e] = x;
+    }
+    // zero fill [zb, n): padding rows and the alignment gap
+    for (uint32_t b = zb * osz + 16 * threadIdx.x; b < n * osz; b += 16 * kThreads)
+      st_v4(d + b, make_uint4(0, 0, 0, 0));
+  }
+}
+
+// ------------------------------------------------------------------- K6 RS copy-out
+template <bool kInBf16, bool kAcc>
+__global__ void __launch_bounds__(kThreads) k_rs_copy_out(const uint8_t* __restrict__ in,
+                                                          float* __restrict__ grad, int64_t n8) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n8; i += stride) {
+    float x[8];
+    if (kInBf16) {
+      const uint4 a = ld_stream(in + 16 * i);
+      x[0] = bf16_lo(a.x); x[1] = bf16_hi(a.x); x[2] = bf16_lo(a.y); x[3] = bf16_hi(a.y);
+      x[4] = bf16_lo(a.z); x[5] = bf16_hi(a.z); x[6] = bf16_lo(a.w); x[7] = bf16_hi(a.w);
+    } else {
+      const uint4 a = ld_stream(in + 32 * i), b = ld_stream(in + 32 * i + 16);
+      x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y); x[2] = __uint_as_float(a.z);
+      x[3] = __uint_as_float(a.w); x[4] = __uint_as_float(b.x); x[5] = __uint_as_float(b.y);
+      x[6] = __uint_as_float(b.z); x[7] = __uint_as_float(b.w);
+    }
+    float4* g = reinterpret_cast<float4*>(grad + 8 * i);
+    if (kAcc) {
+      const float4 g0 = g[0], g1 = g[1];
+      x[0] = __fadd_rn(g0.x, x[0]); x[1] = __fadd_rn(g0.y, x[1]); x[2] = __fadd_rn(g0.z, x[2]);
+      x[3] = __fadd_rn(g0.w, x[3]); x[4] = __fadd_rn(g1.x, x[4]); x[5] = __fadd_rn(g1.y, x[5]);
+      x[6] = __fadd_rn(g1.z, x[6]); x[7] = __fadd_rn(g1.w, x[7]);
+    }
+    g[0] = make_float4(x[0], x[1], x[2], x[3]);
+    g[1] = make_float4(x[4], x[5], x[6], x[7]);
+  }
+}
+
+// ------------------------------------------------------------------- K1 amax
+__global__ void __launch_bounds__(kThreads) k_amax(const Tile* __restrict__ tiles, int ntiles,
+                                                   uint32_t* __restrict__ acc) {
+  __shared__ uint32_t warp_max[kThreads / 32];
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    const float* src = reinterpret_cast<const float*>(tl.src);
+    const uint32_t n = tl.n;
+    const uint32_t nv = n / 4;
+    uint32_t m = 0;   // max of |x| bit patterns (non-negative floats order like uints; NaN > inf)
+    uint32_t v = threadIdx.x;
+    for (; v + (kUnroll - 1) * kThreads < nv; v += kUnroll * kThreads) {
+      uint4 q[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) q[u] = ld_stream(src + 4 * (v + u * kThreads));
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        m = max(m, max(max(q[u].x & 0x7FFFFFFFu, q[u].y & 0x7FFFFFFFu),
+                       max(q[u].z & 0x7FFFFFFFu, q[u].w & 0x7FFFFFFFu)));
+    }
+    for (; v < nv; v += kThreads) {
+      const uint4 q = ld_stream(src + 4 * v);
+      m = max(m, max(max(q.x & 0x7FFFFFFFu, q.y & 0x7FFFFFFFu), max(q.z & 0x7FFFFFFFu, q.w & 0x7FFFFFFFu)));
+    }
+    for (uint32_t e = nv * 4 + threadIdx.x; e < n; e += kThreads) m = max(m, __float_as_uint(src[e]) & 0x7FFFFFFFu);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    if ((threadIdx.x & 31) == 0) warp_max[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      m = threadIdx.x < kThreads / 32 ? warp_max[threadIdx.x] : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+      if (threadIdx.x == 0 && m != 0) atomicMax(acc + tl.param, m);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------- K1b scale
+__global__ void k_fp8_scale(const int32_t* __restrict__ idx, int n, uint32_t* __restrict__ acc,
+                            float* __restrict__ amax_out, float* __restrict__ scale_out,
+                            const uint8_t* __restrict__ eligible, int* __restrict__ err, bool reset) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int j = idx[i];
+  const float a = __uint_as_float(acc[j]);
+  amax_out[j] = a;
+  float s = 0.0f;
+  if (eligible[j]) {
+    if (!isfinite(a)) {
+      atomicExch(err, 1);
+    } else {
+      const float c = fmaxf(a, 1e-12f);
+      s = __double2float_rn(__ddiv_rn(448.0, (double)c));
+    }
+  }
+  scale_out[j] = s;
+  if (reset) acc[j] = 0u;
+}
+
+inline int grid_for(int64_t work_items, LaunchCfg cfg) {
+  int64_t g = work_items;
+  if (g > cfg.grid_cap) g = cfg.grid_cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace
+
+cudaError_t launch_copy_in_bf16(const float* shard, void* slot, int64_t S, LaunchCfg cfg, cudaStream_t st) {
+  const int64_t n8 = S / 8;
+  if (n8 == 0) return cudaSuccess;
+  k_copy_in_bf16<<<grid_for((n8 + kThreads - 1) / kThreads, cfg), kThreads, 0, st>>>(
+      reinterpret_cast<const float4*>(shard), reinterpret_cast<uint4*>(slot), n8);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_in_fp8(const Tile* tiles, int ntiles, const float* shard, void* slot,
+                               const float* scales, LaunchCfg cfg, cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  k_copy_in_fp8<<<grid_for(ntiles, cfg), kThreads, 0, st>>>(tiles, ntiles, shard, (uint8_t*)slot, scales);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_out(const Tile* tiles, int ntiles, const void* ag, const PtrArray& outs,
+                            LaunchCfg cfg, cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  k_copy_out<<<grid_for(ntiles, cfg), kThreads, 0, st>>>(tiles, ntiles, (const uint8_t*)ag, outs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rs_copy_in(const Tile* tiles, int ntiles, const PtrArray& grads, bool grad_bf16,
+                              void* rs_in, bool out_bf16, bool mean, int world_size, LaunchCfg cfg,
+                              cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  DivW div;
+  div.w = (float)world_size;
+  div.pow2 = (world_size & (world_size - 1)) == 0;
+  div.inv = 1.0f / (float)world_size;
+  div.mean = mean;
+  const int g = grid_for(ntiles, cfg);
+  uint8_t* d = (uint8_t*)rs_in;
+  if (grad_bf16 && !out_bf16) k_rs_copy_in<true, false><<<g, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
+  else if (grad_bf16 && out_bf16) k_rs_copy_in<true, true><<<g, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
+  else if (!grad_bf16 && !out_bf16) k_rs_copy_in<false, false><<<g, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
+  else k_rs_copy_in<false, true><<<g, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rs_copy_out(const void* rs_out, bool in_bf16, float* grad, bool accumulate, int64_t S,
+                               LaunchCfg cfg, cudaStream_t st) {
+  const int64_t n8 = S / 8;
+  if (n8 == 0) return cudaSuccess;
+  const int g = grid_for((n8 + kThreads - 1) / kThreads, cfg);
+  const uint8_t* in = (const uint8_t*)rs_out;
+  if (in_bf16 && accumulate) k_rs_copy_out<true, true><<<g, kThreads, 0, st>>>(in, grad, n8);
+  else if (in_bf16) k_rs_copy_out<true, false><<<g, kThreads, 0, st>>>(in, grad, n8);
+  else if (accumulate) k_rs_copy_out<false, true><<<g, kThreads, 0, st>>>(in, grad, n8);
+  else k_rs_copy_out<false, false><<<g, kThreads, 0, st>>>(in, grad, n8);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_amax(const Tile* tiles, int ntiles, uint32_t* acc_bits, LaunchCfg cfg, cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  k_amax<<<grid_for(ntiles, cfg), kThreads, 0, st>>>(tiles, ntiles, acc_bits);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fp8_scale(const int32_t* idx, int n, uint32_t* acc_bits, float* amax_out, float* scale_out,
+                             const uint8_t* eligible, int* err_flag, bool reset_acc, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_fp8_scale<<<(n + 127) / 128, 128, 0, st>>>(idx, n, acc_bits, amax_out, scale_out, eligible, err_flag,
+                                                 reset_acc);
+  return cudaGetLastError();
+}
+
+}  // namespace fsdpk

@@ -1,0 +1,47 @@
+// Host-side Shard(0) layout and tile-table construction (component N1).
+// Pure host code, deterministic, no CUDA calls.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "fsdp_b200.h"
+#include "kernels.h"
+
+namespace fsdpl {
+
+inline int64_t round_up(int64_t n, int64_t a) { return ((n + a - 1) / a) * a; }
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+constexpr int64_t kAlignElems = 16;   // flat-segment alignment in elements (R2)
+constexpr int64_t kAlignBytes = 16;   // mixed fp8/bf16 slot alignment in bytes (R2)
+constexpr int64_t kArenaAlign = 256;  // unsharded tensors are 256-byte aligned
+
+struct Layout {
+  int W = 1, rank = 0;
+  std::vector<fsdp_param_meta_t> metas;
+  std::vector<int64_t> numel;     // d0 * rest
+  std::vector<uint8_t> fp8;       // eligibility
+  int64_t S = 0;                  // elements per rank
+  int64_t S_bytes_fp8 = 0;        // bytes per rank of the mixed fp8 slot
+  uint64_t hash = 0;
+  // unsharded arena offsets (bytes) for the bf16 and the fp8 unshard
+  std::vector<int64_t> uoff_bf16, uoff_fp8;
+  int64_t arena_bf16 = 0, arena_fp8 = 0;
+};
+
+// Returns FSDP_OK or an error status with *msg set.
+fsdp_status_t compute_layout(int n, const fsdp_param_desc_t* descs, int W, int rank, Layout* out,
+                             const char** msg);
+
+// K3: per param, fp8 (e4m3) or bf16 segments of n_p elements.
+std::vector<fsdpk::Tile> tiles_copy_in_fp8(const Layout& L);
+// K4: per (param, rank) byte copies from the [W][slot] buffer to output tensor param.
+// fp8 == false: the bf16 unshard.  Tiles are param-major; first_tile[p] marks ranges.
+std::vector<fsdpk::Tile> tiles_copy_out(const Layout& L, bool fp8, std::vector<int>* first_tile);
+// K5: per (param, rank) grad chunk copies + zero fill of padding / alignment gaps.
+std::vector<fsdpk::Tile> tiles_rs_copy_in(const Layout& L, std::vector<int>* first_tile);
+// K1: amax tiles of the eligible params of a layer; src = absolute address.
+void append_tiles_amax(const Layout& L, const float* shard_dev, int reg_base,
+                       std::vector<fsdpk::Tile>* out);
+
+}  // namespace fsdpl

@@ -1,0 +1,344 @@
+"""Thin Python binding of the C ABI (include/fsdp_b200.h): same names, torch tensors in,
+pointers out.  Every step of the path runs in libfsdp_b200.so; this module only
+marshals arguments, wraps library-owned device memory as torch views, and (in
+``Mesh.from_process_group``) broadcasts the NCCL unique id over torch.distributed.
+
+Names follow BASELINE.json / the paper's statement of the problem:
+``fsdp_shard(params, mesh)``, ``fsdp_unshard`` / ``all_gather_params(layer, dtype,
+fp8_scale)``, ``precompute_fp8_scales(params)``, ``reduce_scatter_grads(layer,
+reduce_dtype, mean)``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import _capi as capi
+from ._capi import ParamDesc, ParamMeta, call
+
+_DT = {torch.float32: capi.FLOAT32, torch.bfloat16: capi.BFLOAT16, torch.float8_e4m3fn: capi.FLOAT8_E4M3FN}
+_DT_INV = {v: k for k, v in _DT.items()}
+
+
+def _dtype_code(dt) -> int:
+    if isinstance(dt, int):
+        return dt
+    if dt not in _DT:
+        raise ValueError(f"unsupported dtype {dt}")
+    return _DT[dt]
+
+
+def _stream(stream) -> C.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+class _CAI:
+    """__cuda_array_interface__ view of library-owned device memory (no copy)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(int(s) for s in shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None,
+                                         "stream": None}
+
+
+def _view(ptr: int, shape, dtype: torch.dtype, device: int) -> torch.Tensor:
+    shape = tuple(int(s) for s in shape)
+    n = 1
+    for s in shape:
+        n *= s
+    if n == 0 or not ptr:
+        return torch.empty(shape, dtype=dtype, device=f"cuda:{device}")
+    if dtype == torch.float32:
+        return torch.as_tensor(_CAI(ptr, shape, "<f4"), device=f"cuda:{device}")
+    if dtype == torch.bfloat16:
+        return torch.as_tensor(_CAI(ptr, shape, "<u2"), device=f"cuda:{device}").view(torch.bfloat16)
+    if dtype == torch.float8_e4m3fn:
+        return torch.as_tensor(_CAI(ptr, shape, "|u1"), device=f"cuda:{device}").view(torch.float8_e4m3fn)
+    if dtype == torch.uint8:
+        return torch.as_tensor(_CAI(ptr, shape, "|u1"), device=f"cuda:{device}")
+    raise ValueError(dtype)
+
+
+def _descs(shapes, fp8_eligible) -> C.Array:
+    n = len(shapes)
+    arr = (ParamDesc * max(n, 1))()
+    for p, shape in enumerate(shapes):
+        shape = tuple(int(s) for s in shape)
+        arr[p].ndim = len(shape)
+        arr[p].fp8_eligible = int(bool(fp8_eligible[p])) if fp8_eligible is not None else 0
+        for i, s in enumerate(shape[:capi.FSDP_MAX_NDIM]):
+            arr[p].shape[i] = s
+    return arr
+
+
+def _meta_dict(m: ParamMeta) -> dict:
+    return {k: int(getattr(m, k)) for k, _ in ParamMeta._fields_}
+
+
+# ----------------------------------------------------------------------- host-only
+def layout_compute(shapes: Sequence[Sequence[int]], world_size: int, rank: int,
+                   fp8_eligible: Optional[Sequence[bool]] = None):
+    """Shard(0) metadata on the host (no GPU): (list of meta dicts, S, S_bytes_fp8, hash)."""
+    n = len(shapes)
+    descs = _descs(shapes, fp8_eligible)
+    metas = (ParamMeta * max(n, 1))()
+    S = C.c_int64()
+    Sb = C.c_int64()
+    h = C.c_uint64()
+    call("fsdp_layout_compute", n, descs, world_size, rank, metas, C.byref(S), C.byref(Sb), C.byref(h))
+    return [_meta_dict(metas[p]) for p in range(n)], S.value, Sb.value, h.value
+
+
+def get_unique_id() -> bytes:
+    buf = (C.c_uint8 * capi.FSDP_UNIQUE_ID_BYTES)()
+    call("fsdp_get_unique_id", buf)
+    return bytes(buf)
+
+
+# ----------------------------------------------------------------------- mesh
+class Mesh:
+    """1-D data-parallel mesh (fsdp_mesh_t).  world_size defaults to all ranks."""
+
+    def __init__(self, world_size: int, rank: int, device: int, unique_id: Optional[bytes] = None,
+                 local: bool = False):
+        self.world_size, self.rank, self.device = int(world_size), int(rank), int(device)
+        self.local = local
+        h = C.c_void_p()
+        if local:
+            call("fsdp_mesh_init_local", self.world_size, self.rank, self.device, C.byref(h))
+        else:
+            if unique_id is None or len(unique_id) != capi.FSDP_UNIQUE_ID_BYTES:
+                raise ValueError("unique_id of 128 bytes required")
+            idb = (C.c_uint8 * capi.FSDP_UNIQUE_ID_BYTES).from_buffer_copy(unique_id)
+            call("fsdp_mesh_init", idb, self.world_size, self.rank, self.device, C.byref(h))
+        self.handle = h
+        self.layers: List["Layer"] = []
+
+    @classmethod
+    def from_process_group(cls, group=None, device: Optional[int] = None) -> "Mesh":
+        """Collective: rank 0 creates the NCCL unique id, torch.distributed broadcasts it
+        (the binding's only torch.distributed use), every rank initialises the mesh."""
+        import torch.distributed as dist
+        if device is None:
+            device = torch.cuda.current_device()
+        W = dist.get_world_size(group)
+        r = dist.get_rank(group)
+        obj = [get_unique_id() if r == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        return cls(W, r, device, unique_id=obj[0])
+
+    def synchronize(self, timeout_ms: int = 0):
+        call("fsdp_mesh_synchronize", self.handle, int(timeout_ms))
+
+    def profile_enable(self, on: bool = True):
+        call("fsdp_profile_enable", self.handle, int(bool(on)))
+
+    def profile_read(self, reset: bool = True) -> dict:
+        pr = capi.Profile()
+        call("fsdp_profile_read", self.handle, C.byref(pr), int(bool(reset)))
+        return {k: {"launches": int(pr.launches[i]), "ms": float(pr.total_ms[i]), "bytes": int(pr.bytes[i])}
+                for i, k in enumerate(capi.PROF_KINDS)}
+
+    def destroy(self):
+        for l in list(self.layers):
+            l.destroy()
+        if self.handle:
+            call("fsdp_mesh_destroy", self.handle)
+            self.handle = None
+
+
+# ----------------------------------------------------------------------- layer
+class Layer:
+    """One FSDP unit (fsdp_layer_t).  Tensor accessors return views of library memory."""
+
+    def __init__(self, mesh: Mesh, handle: C.c_void_p, shapes, fp8_eligible):
+        self.mesh = mesh
+        self.handle = handle
+        self.shapes = [tuple(int(s) for s in sh) for sh in shapes]
+        self.fp8_eligible = [bool(e) for e in fp8_eligible]
+        n = C.c_int32()
+        S = C.c_int64()
+        Sb = C.c_int64()
+        call("fsdp_layer_info", handle, C.byref(n), C.byref(S), C.byref(Sb))
+        self.P, self.S, self.S_bytes_fp8 = n.value, S.value, Sb.value
+        self.metas = [self.meta(p) for p in range(self.P)]
+        self._pending_grads = None
+        self._unshard_dtype = None
+
+    @property
+    def device(self) -> int:
+        return self.mesh.device
+
+    def meta(self, p: int) -> dict:
+        m = ParamMeta()
+        call("fsdp_param_meta", self.handle, p, C.byref(m))
+        return _meta_dict(m)
+
+    def sharded_flat(self) -> torch.Tensor:
+        ptr = C.c_void_p()
+        call("fsdp_sharded_flat", self.handle, C.byref(ptr))
+        return _view(ptr.value, (self.S,), torch.float32, self.device)
+
+    def sharded_param(self, p: int, padded: bool = False) -> torch.Tensor:
+        """fp32 local shard of param p: (row_count, *shape[1:]) (or the padded chunk)."""
+        ptr = C.c_void_p()
+        call("fsdp_sharded_param", self.handle, p, C.byref(ptr))
+        m = self.metas[p]
+        rows = m["chunk_rows"] if padded else m["row_count"]
+        return _view(ptr.value, (rows,) + self.shapes[p][1:], torch.float32, self.device)
+
+    def sharded_grad_flat(self) -> torch.Tensor:
+        ptr = C.c_void_p()
+        call("fsdp_sharded_grad_flat", self.handle, C.byref(ptr))
+        return _view(ptr.value, (self.S,), torch.float32, self.device)
+
+    def sharded_grad(self, p: int) -> torch.Tensor:
+        ptr = C.c_void_p()
+        call("fsdp_sharded_grad", self.handle, p, C.byref(ptr))
+        m = self.metas[p]
+        return _view(ptr.value, (m["row_count"],) + self.shapes[p][1:], torch.float32, self.device)
+
+    def unsharded_param(self, p: int) -> torch.Tensor:
+        ptr = C.c_void_p()
+        dt = C.c_int32()
+        call("fsdp_unsharded_param", self.handle, p, C.byref(ptr), C.byref(dt))
+        return _view(ptr.value, self.shapes[p], _DT_INV[dt.value], self.device)
+
+    def unsharded_params(self) -> List[torch.Tensor]:
+        return [self.unsharded_param(p) for p in range(self.P)]
+
+    def fp8_scales(self):
+        s = C.c_void_p()
+        a = C.c_void_p()
+        call("fsdp_fp8_scales", self.handle, C.byref(s), C.byref(a))
+        return _view(s.value, (self.P,), torch.float32, self.device), _view(a.value, (self.P,), torch.float32, self.device)
+
+    def destroy(self):
+        if self.handle:
+            call("fsdp_layer_destroy", self.handle)
+            self.handle = None
+            if self in self.mesh.layers:
+                self.mesh.layers.remove(self)
+
+
+def _ptr_array(tensors) -> C.Array:
+    arr = (C.c_void_p * max(len(tensors), 1))()
+    for i, t in enumerate(tensors):
+        if t is None:
+            arr[i] = None
+        elif isinstance(t, torch.Tensor):
+            if not t.is_contiguous():
+                raise ValueError("tensors must be contiguous")
+            arr[i] = t.data_ptr() if t.numel() else None
+        else:  # numpy array (host)
+            arr[i] = t.ctypes.data if t.size else None
+    return arr
+
+
+# ----------------------------------------------------------------------- API
+def fsdp_shard(mesh: Mesh, params, fp8_eligible: Optional[Sequence[bool]] = None, shapes=None) -> Layer:
+    """fsdp_shard(params, mesh): params = full fp32 tensors (host or device, contiguous) or
+    None (then `shapes` gives the shapes and the shard starts at zero)."""
+    if params is None:
+        if shapes is None:
+            raise ValueError("give params or shapes")
+        full = None
+    else:
+        shapes = [tuple(p.shape) for p in params]
+        for p in params:
+            if isinstance(p, torch.Tensor) and p.dtype != torch.float32:
+                raise ValueError("full params must be fp32 (the master copy)")
+        full = _ptr_array(params)
+    if fp8_eligible is None:
+        fp8_eligible = [False] * len(shapes)
+    descs = _descs(shapes, fp8_eligible)
+    h = C.c_void_p()
+    call("fsdp_shard", mesh.handle, len(shapes), descs, full, C.byref(h))
+    layer = Layer(mesh, h, shapes, fp8_eligible)
+    mesh.layers.append(layer)
+    return layer
+
+
+def precompute_fp8_scales(mesh: Mesh, layers: Sequence[Layer], stream=None):
+    arr = (C.c_void_p * max(len(layers), 1))(*[l.handle.value for l in layers])
+    call("fsdp_precompute_fp8_scales", mesh.handle, arr, len(layers), _stream(stream))
+
+
+def fsdp_unshard(layer: Layer, dtype=torch.bfloat16, fp8_scales: Optional[torch.Tensor] = None, stream=None):
+    sp = C.c_void_p(fp8_scales.data_ptr()) if fp8_scales is not None else C.c_void_p()
+    call("fsdp_unshard", layer.handle, _dtype_code(dtype), sp, _stream(stream))
+    layer._unshard_dtype = dtype
+
+
+def fsdp_wait_unshard(layer: Layer, stream=None):
+    call("fsdp_wait_unshard", layer.handle, _stream(stream))
+
+
+def all_gather_params(layer: Layer, dtype=torch.bfloat16, fp8_scales: Optional[torch.Tensor] = None,
+                      stream=None) -> List[torch.Tensor]:
+    """fsdp_unshard + fsdp_wait_unshard; returns the per-param full tensors (views)."""
+    sp = C.c_void_p(fp8_scales.data_ptr()) if fp8_scales is not None else C.c_void_p()
+    call("fsdp_all_gather_params", layer.handle, _dtype_code(dtype), sp, _stream(stream))
+    return layer.unsharded_params()
+
+
+def fsdp_reshard(layer: Layer, stream=None):
+    call("fsdp_reshard", layer.handle, _stream(stream))
+
+
+def reduce_scatter_grads(layer: Layer, grads: Sequence[torch.Tensor], reduce_dtype=torch.float32,
+                         mean: bool = True, accumulate: bool = False, stream=None):
+    """Post-backward: this rank's full grads -> its fp32 sharded grads (pre-divided by W
+    when mean).  The grads are kept referenced until fsdp_wait_reduce_scatter."""
+    gd = grads[0].dtype
+    if any(g.dtype != gd for g in grads):
+        raise ValueError("all grads of a unit must share a dtype")
+    arr = _ptr_array(grads)
+    call("fsdp_reduce_scatter_grads", layer.handle, arr, _dtype_code(gd), _dtype_code(reduce_dtype),
+         int(bool(mean)), int(bool(accumulate)), _stream(stream))
+    layer._pending_grads = list(grads)
+
+
+def fsdp_wait_reduce_scatter(layer: Layer, stream=None):
+    call("fsdp_wait_reduce_scatter", layer.handle, _stream(stream))
+    layer._pending_grads = None
+
+
+def zero_grad(layer: Layer, stream=None):
+    call("fsdp_zero_grad", layer.handle, _stream(stream))
+
+
+# ----------------------------------------------------------------------- stage entry points
+def stage_copy_in(layer: Layer, dtype, slot: torch.Tensor, fp8_scales: Optional[torch.Tensor] = None, stream=None):
+    sp = C.c_void_p(fp8_scales.data_ptr()) if fp8_scales is not None else C.c_void_p()
+    call("fsdp_stage_copy_in", layer.handle, _dtype_code(dtype), sp, C.c_void_p(slot.data_ptr()), _stream(stream))
+
+
+def stage_copy_out(layer: Layer, dtype, ag: torch.Tensor, outs: Sequence[torch.Tensor], stream=None):
+    call("fsdp_stage_copy_out", layer.handle, _dtype_code(dtype), C.c_void_p(ag.data_ptr()), _ptr_array(outs),
+         _stream(stream))
+
+
+def stage_local_amax(layer: Layer, amax_out: torch.Tensor, stream=None):
+    call("fsdp_stage_local_amax", layer.handle, C.c_void_p(amax_out.data_ptr()), _stream(stream))
+
+
+def stage_fp8_scale(layer: Layer, amax: torch.Tensor, scale_out: torch.Tensor, stream=None):
+    call("fsdp_stage_fp8_scale", layer.handle, C.c_void_p(amax.data_ptr()), C.c_void_p(scale_out.data_ptr()),
+         _stream(stream))
+
+
+def stage_rs_copy_in(layer: Layer, grads, reduce_dtype, mean: bool, rs_in: torch.Tensor, stream=None):
+    call("fsdp_stage_rs_copy_in", layer.handle, _ptr_array(grads), _dtype_code(grads[0].dtype),
+         _dtype_code(reduce_dtype), int(bool(mean)), C.c_void_p(rs_in.data_ptr()), _stream(stream))
+
+
+def stage_rs_copy_out(layer: Layer, rs_out: torch.Tensor, reduce_dtype, accumulate: bool, stream=None):
+    call("fsdp_stage_rs_copy_out", layer.handle, C.c_void_p(rs_out.data_ptr()), _dtype_code(reduce_dtype),
+         int(bool(accumulate)), _stream(stream))

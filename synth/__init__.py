@@ -193,7 +193,7 @@ def edge_values(n: int, seed: int = 0) -> np.ndarray:
     mid = mid * np.where(rng.integers(0, 2, size=n // 4) == 0, np.float32(1), np.float32(-1))
     pools.append(mid.astype(np.float32))
     # random finite bit patterns
-    r = rng.integers(0, 1 << 32, size=n - sum(len(x) for x in pools), dtype=np.uint64).astype(np.uint32)
+    r = rng.integers(0, 1 << 32, size=max(0, n - sum(len(x) for x in pools)), dtype=np.uint64).astype(np.uint32)
     rf = r.view(np.float32)
     rf = np.where(np.isfinite(rf), rf, np.float32(1.0))
     pools.append(rf.astype(np.float32))

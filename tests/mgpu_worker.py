@@ -1,0 +1,167 @@
+"""Multi-GPU parity worker (one process per GPU, launched by torchrun from
+tests/test_multigpu.py or by hand):
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port 29555 tests/mgpu_worker.py
+
+Every rank runs the real NCCL path through the C ABI and checks its own results against
+the CPU oracle's World(W) simulation of all W ranks:
+* unshard bf16 / float8 (precomputed scales): bit-exact on every rank;
+* reduce-scatter fp32 with /W: bit-exact on dyadic grads (any reduction order), and within
+  the R10 bound (elementwise vs sum |x_q| and normwise 1e-6) on normal grads;
+* bf16 reduce: R11 bound; accumulate mode; layout mismatch -> FSDP_ERR_SHAPE;
+* a prefetch pipeline over several units with random stream delays."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+import paper_2410_06511_b200 as F  # noqa: E402
+from oracle import World  # noqa: E402
+from oracle.world import BF16, FP8, FP32, rs_error_ok  # noqa: E402
+
+
+def u16(t):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    W = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mesh = F.Mesh.from_process_group(device=local)
+    checks = 0
+
+    units = [synth.model_units("toy")[0], synth.model_units("toy")[-1]] + \
+            [synth.ragged_unit(s, world_size=W) for s in range(4)]
+    for ui, u in enumerate(units):
+        shapes = [s for _, s, _ in u]
+        elig = [e for _, _, e in u]
+        P = [synth.param_values(ui, p, s) for p, s in enumerate(shapes)]
+        w = World(shapes, W, elig)
+        shards = w.shard(P)
+        layer = F.fsdp_shard(mesh, [torch.from_numpy(p) for p in P], elig)
+        assert layer.S == w.S
+        np.testing.assert_array_equal(layer.sharded_flat().cpu().numpy(), shards[rank])
+        # bf16 unshard
+        outs = F.all_gather_params(layer, torch.bfloat16)
+        _, fulls = w.unshard(shards, BF16)
+        for o, want in zip(outs, fulls):
+            np.testing.assert_array_equal(u16(o), want)
+        F.fsdp_reshard(layer)
+        # fp8 unshard with precomputed scales (one all-reduce(max))
+        F.precompute_fp8_scales(mesh, [layer])
+        amax, scale = w.precompute_fp8_scales(shards)
+        s_dev, a_dev = layer.fp8_scales()
+        np.testing.assert_array_equal(a_dev.cpu().numpy().view(np.uint32), amax.view(np.uint32))
+        np.testing.assert_array_equal(s_dev.cpu().numpy().view(np.uint32), scale.view(np.uint32))
+        outs = F.all_gather_params(layer, torch.float8_e4m3fn)
+        _, fulls = w.unshard(shards, FP8, scale)
+        for o, want in zip(outs, fulls):
+            got = o.view(torch.uint8).cpu().numpy() if o.dtype == torch.float8_e4m3fn else u16(o)
+            np.testing.assert_array_equal(got, want)
+        F.fsdp_reshard(layer)
+        # reduce-scatter: dyadic (bit-exact for any order), then normal data (bound)
+        for kind in ("dyadic", "normal"):
+            gen = synth.dyadic_grad_bf16_bits if kind == "dyadic" else synth.grad_bf16_bits
+            G = [[gen(ui, p, q, s) for p, s in enumerate(shapes)] for q in range(W)]
+            gt = [torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16) for x in G[rank]]
+            F.reduce_scatter_grads(layer, gt)
+            F.fsdp_wait_reduce_scatter(layer)
+            ref = w.reduce_scatter_grads(G, BF16, True)[rank]
+            for p in range(len(shapes)):
+                got = layer.sharded_grad(p).cpu().numpy()
+                if kind == "dyadic":
+                    np.testing.assert_array_equal(got, ref["exact"][p])
+                else:
+                    ok, ratio, nrel = rs_error_ok(got.reshape(-1), ref["exact"][p].reshape(-1),
+                                                  ref["mag"][p].reshape(-1), W)
+                    assert ok, (ui, p, ratio, nrel)
+            # accumulate: the second RS adds in fp32 onto the first
+            before = layer.sharded_grad_flat().clone()
+            F.reduce_scatter_grads(layer, gt, accumulate=True)
+            F.fsdp_wait_reduce_scatter(layer)
+            once = w.reduce_scatter_grads(G, BF16, True)[rank]["exact"]
+            for p in range(len(shapes)):
+                got = layer.sharded_grad(p).cpu().numpy()
+                prev = before[layer.metas[p]["elem_offset"]:layer.metas[p]["elem_offset"] + got.size].cpu().numpy()
+                if kind == "dyadic":
+                    np.testing.assert_array_equal(got.reshape(-1), (prev + once[p].reshape(-1)).astype(np.float32))
+        # bf16 reduce (reading R11): elementwise (W-1)*2^-8*mag + tiny, normwise 1e-2
+        G = [[synth.grad_bf16_bits(ui, p, q, s) for p, s in enumerate(shapes)] for q in range(W)]
+        gt = [torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16) for x in G[rank]]
+        F.reduce_scatter_grads(layer, gt, reduce_dtype=torch.bfloat16)
+        F.fsdp_wait_reduce_scatter(layer)
+        ref = w.reduce_scatter_grads(G, BF16, True)[rank]
+        for p in range(len(shapes)):
+            got = layer.sharded_grad(p).cpu().numpy().reshape(-1)
+            ex = ref["exact"][p].reshape(-1)
+            mg = ref["mag"][p].reshape(-1)
+            bound = (W - 1) * 2.0 ** -8 * mg + W * 2.0 ** -8 * mg + 2.0 ** -133
+            assert np.all(np.abs(got.astype(np.float64) - ex) <= bound), (ui, p)
+            if np.linalg.norm(ex) > 0:
+                assert np.linalg.norm(got - ex) / np.linalg.norm(ex) <= 1e-2
+        layer.destroy()
+        checks += 1
+
+    # layout disagreement across ranks is an error on every rank
+    bad = [(8 + rank, 4)]
+    try:
+        F.fsdp_shard(mesh, None, [False], shapes=bad)
+        raise AssertionError("layout mismatch not detected")
+    except F.FsdpError as e:
+        assert e.status_name == "FSDP_ERR_SHAPE", e
+
+    # prefetch pipeline with random delays on the compute stream
+    blocks = synth.model_units("toy")
+    layers, worlds, params = [], [], []
+    for ui, u in enumerate(blocks):
+        shapes = [s for _, s, _ in u]
+        elig = [e for _, _, e in u]
+        P = [synth.param_values(100 + ui, p, s) for p, s in enumerate(shapes)]
+        params.append(P)
+        worlds.append(World(shapes, W, elig))
+        layers.append(F.fsdp_shard(mesh, [torch.from_numpy(p) for p in P], elig))
+    comp = torch.cuda.Stream()
+    rng = np.random.default_rng(rank)
+    got = []
+    with torch.cuda.stream(comp):
+        F.fsdp_unshard(layers[0], stream=comp)
+        for i, l in enumerate(layers):
+            F.fsdp_wait_unshard(l, stream=comp)
+            if i + 1 < len(layers):
+                F.fsdp_unshard(layers[i + 1], stream=comp)
+            torch.cuda._sleep(int(rng.integers(1000, 300000)))
+            got.append([t.clone() for t in l.unsharded_params()])
+            F.fsdp_reshard(l, stream=comp)
+            g = [torch.full(s, float(i + 1 + rank), dtype=torch.bfloat16, device="cuda") for s in l.shapes]
+            F.reduce_scatter_grads(l, g, stream=comp)
+        for l in layers:
+            F.fsdp_wait_reduce_scatter(l, stream=comp)
+    comp.synchronize()
+    for i, l in enumerate(layers):
+        _, fulls = worlds[i].unshard(worlds[i].shard(params[i]), BF16)
+        for t, want in zip(got[i], fulls):
+            np.testing.assert_array_equal(u16(t), want)
+        want_g = np.float32(sum((i + 1 + q) / W for q in range(W)))
+        for p in range(l.P):
+            g = l.sharded_grad(p)
+            if g.numel():
+                assert torch.all(g == float(want_g)), (i, p)
+    mesh.synchronize(120000)
+    mesh.destroy()
+    dist.barrier()
+    dist.destroy_process_group()
+    print(f"RANK {rank}/{W} OK ({checks} units)", flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -104,8 +104,24 @@ typedef enum {
   FSDP_PROF_AMAX = 6,        /* K1                                            */
   FSDP_PROF_SCALE = 7,       /* K1b                                           */
   FSDP_PROF_ALL_REDUCE = 8,  /* NCCL all-reduce(max) of the amaxes            */
-  FSDP_PROF_NUM = 9
+  FSDP_PROF_UNSHARD_PUSH = 9,  /* P2P: fused copy-in + all-gather + copy-out   */
+  FSDP_PROF_RS_PULL = 10,      /* P2P: fused chunk + /W + reduce + copy-out    */
+  FSDP_PROF_STAGE_GRADS = 11,  /* P2P: caller grads -> symmetric staging       */
+  FSDP_PROF_HANDSHAKE = 12,    /* P2P: cross-GPU ready/done flag kernels       */
+  FSDP_PROF_NUM = 13
 } fsdp_prof_kind_t;
+
+/* How the collectives of a mesh run.
+ *  FSDP_ALGO_NCCL: copy-in kernel -> ncclAllGather -> copy-out kernel; chunk-cat kernel ->
+ *                  ncclReduceScatter (fp32).
+ *  FSDP_ALGO_P2P:  symmetric buffers mapped with CUDA IPC across the ranks' GPUs (NVLink /
+ *                  NVSwitch); the unshard is ONE push kernel (cast + store into every rank's
+ *                  unsharded tensors) and the reduce-scatter ONE pull kernel (read every
+ *                  rank's bf16 grad rows, /W, sum in ascending rank order in fp32), each
+ *                  bracketed by single-CTA flag handshakes.  Requires W <= 8 GPUs with
+ *                  peer access; identical results up to the reduce-scatter summation order
+ *                  (P2P: ascending rank, deterministic). */
+typedef enum { FSDP_ALGO_NCCL = 0, FSDP_ALGO_P2P = 1 } fsdp_algo_t;
 
 typedef struct {
   int64_t launches[FSDP_PROF_NUM];
@@ -151,6 +167,14 @@ fsdp_status_t fsdp_mesh_init_local(int32_t world_size, int32_t rank, int32_t cud
 fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* mesh);
 fsdp_status_t fsdp_mesh_info(const fsdp_mesh_t* mesh, int32_t* world_size, int32_t* rank,
                              int32_t* cuda_device);
+
+/* Selects the collective algorithm (fsdp_algo_t).  Collective: every rank must make the
+ * same call at the same point, with no layer unsharded / reduce-scatter pending.  The
+ * default after fsdp_mesh_init is FSDP_ALGO_P2P when W > 1, W <= 8 and every rank could
+ * map its peers' buffers (environment FSDP_B200_ALGO=nccl|p2p overrides), else NCCL.
+ * FSDP_ERR_UNAVAILABLE if P2P is requested but not possible. */
+fsdp_status_t fsdp_mesh_set_algo(fsdp_mesh_t* mesh, int32_t algo);
+fsdp_status_t fsdp_mesh_get_algo(const fsdp_mesh_t* mesh, int32_t* algo);
 
 /* Waits (host) until every internal stream of the mesh is idle, polling NCCL for
  * asynchronous errors.  Returns FSDP_ERR_NONFINITE if a precompute saw a non-finite

@@ -21,7 +21,8 @@ STATUS = {0: "FSDP_OK", 1: "FSDP_ERR_INVALID_ARGUMENT", 2: "FSDP_ERR_SHAPE", 3: 
           8: "FSDP_ERR_TIMEOUT", 9: "FSDP_ERR_NONFINITE", 10: "FSDP_ERR_UNAVAILABLE"}
 
 PROF_KINDS = ["copy_in", "all_gather", "copy_out", "rs_copy_in", "reduce_scatter", "rs_copy_out",
-              "amax", "scale", "all_reduce"]
+              "amax", "scale", "all_reduce", "unshard_push", "rs_pull", "stage_grads", "handshake"]
+ALGO_NCCL, ALGO_P2P = 0, 1
 
 
 class ParamDesc(C.Structure):
@@ -34,7 +35,7 @@ class ParamMeta(C.Structure):
 
 
 class Profile(C.Structure):
-    _fields_ = [("launches", C.c_int64 * 9), ("total_ms", C.c_double * 9), ("bytes", C.c_int64 * 9)]
+    _fields_ = [("launches", C.c_int64 * 13), ("total_ms", C.c_double * 13), ("bytes", C.c_int64 * 13)]
 
 
 class FsdpError(RuntimeError):
@@ -59,6 +60,8 @@ SIGNATURES = {
     "fsdp_mesh_destroy": [_VP],
     "fsdp_mesh_info": [_VP, C.POINTER(_I32), C.POINTER(_I32), C.POINTER(_I32)],
     "fsdp_mesh_synchronize": [_VP, _I64],
+    "fsdp_mesh_set_algo": [_VP, _I32],
+    "fsdp_mesh_get_algo": [_VP, C.POINTER(_I32)],
     "fsdp_profile_enable": [_VP, _I32],
     "fsdp_profile_read": [_VP, C.POINTER(Profile), _I32],
     "fsdp_shard": [_VP, _I32, C.POINTER(ParamDesc), _PP, C.POINTER(_VP)],

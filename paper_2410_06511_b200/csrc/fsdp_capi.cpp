@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -28,6 +29,7 @@
 #include "fsdp_b200.h"
 #include "kernels.h"
 #include "layout.h"
+#include "p2p.h"
 
 using fsdpk::Tile;
 using fsdpl::Layout;
@@ -143,6 +145,28 @@ struct ProfRec {
   int64_t bytes;
 };
 
+// A symmetric buffer: same size on every rank, peers' copies mapped with CUDA IPC.
+struct SymBuf {
+  void* local = nullptr;
+  size_t bytes = 0;
+  std::vector<void*> peers;   // peers[r] = rank r's buffer in this process (peers[rank] = local)
+};
+
+// A pooled symmetric slot of the P2P path (unsharded arena, or grad staging).  Slots are
+// chosen deterministically (same choice on every rank) and each use bumps the epoch the
+// cross-GPU flags are compared against.
+struct SymSlot {
+  SymBuf buf;
+  cudaEvent_t free_ev = nullptr;
+  bool in_use = false;
+  bool ever_used = false;
+  uint64_t epoch = 0;
+  int index = 0;
+};
+
+constexpr int kFlagSlots = 64;   // max symmetric slots per kind
+enum FlagKind { FK_AG_READY = 0, FK_AG_DONE = 1, FK_RS_READY = 2, FK_RS_DONE = 3, FK_NUM = 4 };
+
 enum LayerState { SHARDED = 0, UNSHARDING = 1, UNSHARDED = 2 };
 
 }  // namespace
@@ -181,6 +205,13 @@ struct fsdp_mesh {
   std::vector<cudaEvent_t> ev_pool;
   fsdp_profile_t prof_acc{};
   bool aborted = false;
+  // P2P (fused peer-memory) path
+  int algo = FSDP_ALGO_NCCL;
+  bool p2p_ok = false;
+  SymBuf flags;                              // uint64 [FK_NUM][kFlagSlots][kMaxRanks]
+  std::vector<SymSlot*> p2p_ag, p2p_rs;      // unsharded arenas, grad staging
+  uint64_t rs_rr = 0;                        // round robin over staging slots
+  int* d_barrier = nullptr;
 };
 
 struct fsdp_layer {
@@ -203,6 +234,13 @@ struct fsdp_layer {
   // reduce-scatter state
   bool rs_pending = false;
   cudaEvent_t ev_rcall = nullptr, ev_k5 = nullptr, ev_rs_done = nullptr;
+  // P2P path
+  DevTiles t_push_bf16, t_push_fp8, t_pull, t_stage_bf16, t_stage_fp32;
+  std::vector<int64_t> stg_off_el;   // full-grad staging: param p at element offset (128-aligned)
+  int64_t stg_elems = 0;
+  int64_t push_bytes_bf16 = 0, push_bytes_fp8 = 0, pull_elems = 0;
+  SymSlot* p2p_slot = nullptr;       // arena of the current P2P unshard
+  void* arena_base = nullptr;        // base of the unsharded tensors (either path)
 };
 
 namespace {
@@ -345,6 +383,130 @@ void clear_presets(fsdp_mesh* m) {
 
 int64_t dtype_size(fsdp_dtype_t d) { return d == FSDP_FLOAT32 ? 4 : (d == FSDP_BFLOAT16 ? 2 : 1); }
 
+// ---- symmetric memory over CUDA IPC (collective helpers; every rank calls them in the
+// same order, which the deterministic FSDP call sequence guarantees)
+void mesh_barrier(fsdp_mesh* m) {
+  NCCL_CHECK(ncclAllReduce(m->d_barrier, m->d_barrier, 1, ncclInt32, ncclSum, m->comm_ag, m->s_ag));
+  CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
+}
+
+// all ranks agree that `ok` holds everywhere
+bool mesh_all_ok(fsdp_mesh* m, bool ok) {
+  int v = ok ? 1 : 0;
+  CUDA_CHECK(cudaMemcpy(m->d_barrier, &v, sizeof(int), cudaMemcpyHostToDevice));
+  NCCL_CHECK(ncclAllReduce(m->d_barrier, m->d_barrier, 1, ncclInt32, ncclMin, m->comm_ag, m->s_ag));
+  CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
+  CUDA_CHECK(cudaMemcpy(&v, m->d_barrier, sizeof(int), cudaMemcpyDeviceToHost));
+  return v == 1;
+}
+
+// Collective: unmap the peers' copies, wait until every rank did, then free the local one.
+void sym_free(fsdp_mesh* m, SymBuf& b) {
+  for (int r = 0; r < m->W; ++r)
+    if (r != m->rank && r < (int)b.peers.size() && b.peers[r]) cudaIpcCloseMemHandle(b.peers[r]);
+  cudaGetLastError();
+  mesh_barrier(m);
+  if (b.local) cudaFree(b.local);
+  b = SymBuf();
+}
+
+// Returns false (on every rank) if any rank failed to allocate or map.
+bool sym_alloc(fsdp_mesh* m, SymBuf& b, size_t bytes) {
+  bool ok = cudaMalloc(&b.local, bytes + 256) == cudaSuccess;
+  cudaIpcMemHandle_t h{};
+  if (ok) ok = cudaMemset(b.local, 0, bytes + 256) == cudaSuccess;
+  if (ok) ok = cudaIpcGetMemHandle(&h, b.local) == cudaSuccess;
+  cudaGetLastError();
+  uint8_t* d = nullptr;
+  CUDA_CHECK(cudaMalloc(&d, sizeof(h) * m->W));
+  CUDA_CHECK(cudaMemcpy(d + sizeof(h) * m->rank, &h, sizeof(h), cudaMemcpyHostToDevice));
+  NCCL_CHECK(ncclAllGather(d + sizeof(h) * m->rank, d, sizeof(h), ncclUint8, m->comm_ag, m->s_ag));
+  CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
+  std::vector<cudaIpcMemHandle_t> hs(m->W);
+  CUDA_CHECK(cudaMemcpy(hs.data(), d, sizeof(h) * m->W, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  b.peers.assign(m->W, nullptr);
+  b.bytes = bytes;
+  if (ok) {
+    b.peers[m->rank] = b.local;
+    for (int r = 0; r < m->W && ok; ++r) {
+      if (r == m->rank) continue;
+      void* p = nullptr;
+      ok = cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      cudaGetLastError();
+      b.peers[r] = ok ? p : nullptr;
+    }
+  }
+  if (!mesh_all_ok(m, ok)) {
+    sym_free(m, b);
+    return false;
+  }
+  return true;
+}
+
+fsdpp::FlagPtrs flag_remote(fsdp_mesh* m, int kind, int slot) {
+  fsdpp::FlagPtrs f{};
+  const size_t off = ((size_t)kind * kFlagSlots + slot) * fsdpp::kMaxRanks;
+  for (int r = 0; r < m->W; ++r) f.p[r] = (unsigned long long*)m->flags.peers[r] + off;
+  return f;
+}
+unsigned long long* flag_local(fsdp_mesh* m, int kind, int slot) {
+  return (unsigned long long*)m->flags.local + ((size_t)kind * kFlagSlots + slot) * fsdpp::kMaxRanks;
+}
+
+// Deterministic choice: the lowest-index free slot (same on every rank, since in_use
+// depends only on the call sequence); grows / creates slots collectively.
+SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t bytes, int prefer = -1) {
+  SymSlot* s = nullptr;
+  while (prefer >= (int)pool.size() && (int)pool.size() < kFlagSlots) {
+    SymSlot* n = new SymSlot();
+    n->free_ev = new_event();
+    n->index = (int)pool.size();
+    pool.push_back(n);
+  }
+  if (prefer >= 0 && prefer < (int)pool.size() && !pool[prefer]->in_use) s = pool[prefer];
+  for (size_t i = 0; !s && i < pool.size(); ++i)
+    if (!pool[i]->in_use) s = pool[i];
+  if (!s) {
+    if ((int)pool.size() >= kFlagSlots) fail(FSDP_ERR_STATE, "too many unsharded layers / pending reduce-scatters at once");
+    s = new SymSlot();
+    s->free_ev = new_event();
+    s->index = (int)pool.size();
+    pool.push_back(s);
+  }
+  if (s->buf.bytes < bytes) {   // collective (re)allocation; setup-time only
+    if (s->ever_used) CUDA_CHECK(cudaEventSynchronize(s->free_ev));
+    CUDA_CHECK(cudaDeviceSynchronize());
+    mesh_barrier(m);
+    if (s->buf.local || !s->buf.peers.empty()) sym_free(m, s->buf);
+    if (!sym_alloc(m, s->buf, bytes)) fail(FSDP_ERR_OUT_OF_MEMORY, "symmetric buffer allocation/mapping failed");
+  }
+  s->in_use = true;
+  return s;
+}
+
+fsdpp::PeerPtrs peer_ptrs(const fsdp_mesh* m, const SymBuf& b) {
+  fsdpp::PeerPtrs p{};
+  for (int r = 0; r < m->W; ++r) p.p[r] = (uint8_t*)b.peers[r];
+  return p;
+}
+
+void p2p_teardown(fsdp_mesh* m) {
+  if (!m->p2p_ok) return;
+  CUDA_CHECK(cudaDeviceSynchronize());
+  mesh_barrier(m);   // every rank's kernels are done with every peer buffer
+  for (auto* pool : {&m->p2p_ag, &m->p2p_rs}) {
+    for (SymSlot* s : *pool) {
+      if (s->buf.local || !s->buf.peers.empty()) sym_free(m, s->buf);
+      if (s->free_ev) cudaEventDestroy(s->free_ev);
+      delete s;
+    }
+    pool->clear();
+  }
+  sym_free(m, m->flags);
+  m->p2p_ok = false;
+}
+
 // ---- K4 / K5 launches (fsdp_shard enforces P <= kMaxPtrs, one pointer array per launch)
 void launch_copy_out_all(fsdp_layer* l, bool fp8, const void* ag, void* const* outs, cudaStream_t st) {
   const DevTiles& T = fp8 ? l->t_cout_fp8 : l->t_cout_bf16;
@@ -441,6 +603,18 @@ static void mesh_common_init(fsdp_mesh* m) {
   CUDA_CHECK(cudaMemset(m->d_err, 0, sizeof(int)));
   m->ev_pre_call = new_event();
   m->ev_pre_done = new_event();
+  CUDA_CHECK(cudaMalloc(&m->d_barrier, sizeof(int)));
+  CUDA_CHECK(cudaMemset(m->d_barrier, 0, sizeof(int)));
+}
+
+// P2P capability: W in [2, 8] and every rank can map every peer's buffer (collective).
+static void p2p_init(fsdp_mesh* m) {
+  if (m->local || m->W < 2 || m->W > 8) return;
+  const size_t fbytes = sizeof(unsigned long long) * FK_NUM * kFlagSlots * fsdpp::kMaxRanks;
+  m->p2p_ok = sym_alloc(m, m->flags, fbytes);
+  const char* env = std::getenv("FSDP_B200_ALGO");
+  const bool want_nccl = env && std::string(env) == "nccl";
+  m->algo = (m->p2p_ok && !want_nccl) ? FSDP_ALGO_P2P : FSDP_ALGO_NCCL;
 }
 
 static fsdp_status_t mesh_init_impl(const uint8_t* id, int32_t W, int32_t rank, int32_t dev, bool local,
@@ -466,6 +640,7 @@ static fsdp_status_t mesh_init_impl(const uint8_t* id, int32_t W, int32_t rank, 
         std::memcpy(&u, id, sizeof(u));
         NCCL_CHECK(ncclCommInitRank(&m->comm_ag, W, u, rank));
         NCCL_CHECK(ncclCommSplit(m->comm_ag, 0, rank, &m->comm_rs, nullptr));
+        p2p_init(m);
       }
     } catch (...) {
       fsdp_mesh_destroy(m);
@@ -491,6 +666,7 @@ fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
     DeviceGuard g(m->device);
     for (cudaStream_t s : {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs})
       if (s) cudaStreamSynchronize(s);
+    if (!m->aborted) p2p_teardown(m);
     for (auto* pool : {&m->ag_slots, &m->rs_slots})
       for (Slot* s : *pool) { s->a.release(); s->b.release(); if (s->free_ev) cudaEventDestroy(s->free_ev); delete s; }
     clear_presets(m);
@@ -498,6 +674,7 @@ fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
     for (auto e : m->ev_pool) cudaEventDestroy(e);
     cudaFree(m->reg_acc); cudaFree(m->reg_amax); cudaFree(m->reg_scale); cudaFree(m->reg_elig);
     cudaFree(m->d_err);
+    cudaFree(m->d_barrier);
     if (m->ev_pre_call) cudaEventDestroy(m->ev_pre_call);
     if (m->ev_pre_done) cudaEventDestroy(m->ev_pre_done);
     if (m->comm_rs) { if (m->aborted) ncclCommAbort(m->comm_rs); else ncclCommDestroy(m->comm_rs); }
@@ -514,6 +691,24 @@ fsdp_status_t fsdp_mesh_info(const fsdp_mesh_t* m, int32_t* W, int32_t* rank, in
     if (W) *W = m->W;
     if (rank) *rank = m->rank;
     if (dev) *dev = m->device;
+  });
+}
+
+fsdp_status_t fsdp_mesh_set_algo(fsdp_mesh_t* m, int32_t algo) {
+  return guarded([&] {
+    check_mesh(m);
+    if (algo != FSDP_ALGO_NCCL && algo != FSDP_ALGO_P2P) fail(FSDP_ERR_INVALID_ARGUMENT, "unknown algo");
+    for (auto* l : m->layers)
+      if (l->state != SHARDED || l->rs_pending) fail(FSDP_ERR_STATE, "a layer is unsharded or has a pending reduce-scatter");
+    if (algo == FSDP_ALGO_P2P && !m->p2p_ok) fail(FSDP_ERR_UNAVAILABLE, "P2P needs 2 <= W <= 8 ranks whose GPUs can map each other's memory");
+    m->algo = algo;
+  });
+}
+
+fsdp_status_t fsdp_mesh_get_algo(const fsdp_mesh_t* m, int32_t* algo) {
+  return guarded([&] {
+    if (!m || !algo) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL argument");
+    *algo = m->algo;
   });
 }
 
@@ -627,6 +822,20 @@ fsdp_status_t fsdp_shard(fsdp_mesh_t* m, int32_t n, const fsdp_param_desc_t* des
       l->t_cout_bf16.upload(fsdpl::tiles_copy_out(Ly, false, &l->t_cout_bf16.first));
       l->t_cout_fp8.upload(fsdpl::tiles_copy_out(Ly, true, &l->t_cout_fp8.first));
       l->t_rsin.upload(fsdpl::tiles_rs_copy_in(Ly, &l->t_rsin.first));
+      l->stg_off_el = fsdpl::staging_offsets(Ly, &l->stg_elems);
+      if (m->p2p_ok) {
+        l->t_push_bf16.upload(fsdpl::tiles_push(Ly, false));
+        l->t_push_fp8.upload(fsdpl::tiles_push(Ly, true));
+        l->t_pull.upload(fsdpl::tiles_pull(Ly, l->stg_off_el));
+        l->t_stage_bf16.upload(fsdpl::tiles_stage(Ly, l->stg_off_el, 2));
+        l->t_stage_fp32.upload(fsdpl::tiles_stage(Ly, l->stg_off_el, 4));
+      }
+      for (int p = 0; p < n; ++p) {
+        const int64_t cnt = Ly.metas[p].row_count * Ly.metas[p].rest;
+        l->push_bytes_bf16 += (int64_t)(m->W - 1) * cnt * 2;
+        l->push_bytes_fp8 += (int64_t)(m->W - 1) * cnt * (Ly.fp8[p] ? 1 : 2);
+        l->pull_elems += cnt;
+      }
       for (int p = 0; p < n; ++p) {
         const int64_t es = Ly.fp8[p] ? 1 : 2;
         l->bytes_cin_fp8 += Ly.metas[p].padded_numel * (4 + es);
@@ -667,6 +876,8 @@ fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* l) {
     cudaFree(l->grad);
     cudaFree(l->d_idx_local);
     l->t_cin_fp8.release(); l->t_cout_bf16.release(); l->t_cout_fp8.release(); l->t_rsin.release();
+    l->t_push_bf16.release(); l->t_push_fp8.release(); l->t_pull.release(); l->t_stage_bf16.release();
+    l->t_stage_fp32.release();
     for (cudaEvent_t e : {l->ev_call, l->ev_cin, l->ev_ag, l->ev_done, l->ev_rcall, l->ev_k5, l->ev_rs_done})
       if (e) cudaEventDestroy(e);
     m->layers.erase(std::remove(m->layers.begin(), m->layers.end(), l), m->layers.end());
@@ -789,6 +1000,41 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
     DeviceGuard g(m->device);
     const int64_t sb = slot_bytes(l, fp8);
     const int64_t arena = fp8 ? l->L.arena_fp8 : l->L.arena_bf16;
+    if (m->algo == FSDP_ALGO_P2P) {
+      // fused path: ready handshake -> push (cast + store into every rank's arena) -> done
+      SymSlot* ss = acquire_sym_slot(m, m->p2p_ag, (size_t)arena);
+      const uint64_t epoch = ++ss->epoch;
+      cudaStream_t cs = as_stream(compute);
+      CUDA_CHECK(cudaEventRecord(l->ev_call, cs));
+      CUDA_CHECK(cudaStreamWaitEvent(m->s_ag, l->ev_call, 0));
+      if (ss->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_ag, ss->free_ev, 0));
+      {
+        ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_ag, 0);
+        CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_AG_READY, ss->index), flag_local(m, FK_AG_READY, ss->index),
+                                             m->W, m->rank, epoch, m->s_ag));
+        ph.done();
+      }
+      {
+        const DevTiles& T = fp8 ? l->t_push_fp8 : l->t_push_bf16;
+        ProfScope pp(m, FSDP_PROF_UNSHARD_PUSH, m->s_ag, fp8 ? l->push_bytes_fp8 : l->push_bytes_bf16);
+        CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, peer_ptrs(m, ss->buf), m->W, m->rank,
+                                              m->cfg, m->s_ag));
+        pp.done();
+      }
+      {
+        ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_ag, 0);
+        CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_AG_DONE, ss->index), flag_local(m, FK_AG_DONE, ss->index),
+                                             m->W, m->rank, epoch, m->s_ag));
+        ph.done();
+      }
+      CUDA_CHECK(cudaEventRecord(l->ev_done, m->s_ag));
+      l->p2p_slot = ss;
+      l->slot = nullptr;
+      l->arena_base = ss->buf.local;
+      l->ushard_dtype = dt;
+      l->state = UNSHARDING;
+      return;
+    }
     Slot* slot = acquire_slot(m, m->ag_slots, (size_t)(m->W * sb), (size_t)arena, 1);
     cudaStream_t cs = as_stream(compute);
     // copy-in after the caller's prior work (optimizer step on the shard) and after the
@@ -819,6 +1065,8 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
     }
     CUDA_CHECK(cudaEventRecord(l->ev_done, m->s_cout));
     l->slot = slot;
+    l->p2p_slot = nullptr;
+    l->arena_base = slot->b.p;
     l->ushard_dtype = dt;
     l->state = UNSHARDING;
   });
@@ -849,7 +1097,7 @@ fsdp_status_t fsdp_unsharded_param(const fsdp_layer_t* l, int32_t p, void** dev,
     if (l->state != UNSHARDED) fail(FSDP_ERR_STATE, "unsharded params are valid only between wait_unshard and reshard");
     const bool fp8 = l->ushard_dtype == FSDP_FLOAT8_E4M3FN;
     const auto& uoff = fp8 ? l->L.uoff_fp8 : l->L.uoff_bf16;
-    *dev = (uint8_t*)l->slot->b.p + uoff[p];
+    *dev = (uint8_t*)l->arena_base + uoff[p];
     if (dt) *dt = (fp8 && l->L.fp8[p]) ? FSDP_FLOAT8_E4M3FN : FSDP_BFLOAT16;
   });
 }
@@ -863,8 +1111,18 @@ fsdp_status_t fsdp_reshard(fsdp_layer_t* l, void* compute) {
     if (l->state == UNSHARDING) CUDA_CHECK(cudaStreamWaitEvent(cs, l->ev_done, 0));
     // the buffer is free once everything enqueued on `compute` so far (the consumers of
     // the unsharded params) has run; the next user's copy-in waits on this event
-    release_slot(l->slot, cs);
+    if (l->p2p_slot) {
+      // peers write into this arena only after this rank's next ready handshake on it,
+      // which the next unshard issues after waiting on free_ev
+      CUDA_CHECK(cudaEventRecord(l->p2p_slot->free_ev, cs));
+      l->p2p_slot->ever_used = true;
+      l->p2p_slot->in_use = false;
+      l->p2p_slot = nullptr;
+    } else {
+      release_slot(l->slot, cs);
+    }
     l->slot = nullptr;
+    l->arena_base = nullptr;
     l->state = SHARDED;
   });
 }
@@ -882,6 +1140,53 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
     const bool obf = rd == FSDP_BFLOAT16;
     const int64_t osz = obf ? 2 : 4;
     const int64_t S = l->L.S;
+    if (m->algo == FSDP_ALGO_P2P) {
+      // fused path: stage the caller's grads into this rank's symmetric staging -> ready
+      // handshake -> pull (every rank's rows of this rank, /W, ascending-rank fp32 sum,
+      // written into the grad buffer) -> done handshake (staging reusable)
+      const int64_t gsz = dtype_size(gd);
+      const int prefer = (int)(m->rs_rr++ % 2);   // deterministic round robin: copy of i+1 overlaps pull of i
+      SymSlot* ss = acquire_sym_slot(m, m->p2p_rs, (size_t)(l->stg_elems * gsz), prefer);
+      const uint64_t epoch = ++ss->epoch;
+      cudaStream_t cs = as_stream(compute);
+      CUDA_CHECK(cudaEventRecord(l->ev_rcall, cs));
+      CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, l->ev_rcall, 0));
+      if (ss->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, ss->free_ev, 0));
+      {
+        const DevTiles& T = gd == FSDP_BFLOAT16 ? l->t_stage_bf16 : l->t_stage_fp32;
+        fsdpk::PtrArray pa{};
+        for (int p = 0; p < l->P; ++p) pa.p[p] = grads[p];
+        ProfScope pst(m, FSDP_PROF_STAGE_GRADS, m->s_rsc, 2 * l->grad_numel_total * gsz);
+        CUDA_CHECK(fsdpp::launch_gather_copy(T.d, T.n, pa, ss->buf.local, m->cfg, m->s_rsc));
+        pst.done();
+      }
+      CUDA_CHECK(cudaEventRecord(l->ev_k5, m->s_rsc));
+      CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, l->ev_k5, 0));
+      {
+        ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_rs, 0);
+        CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_READY, ss->index), flag_local(m, FK_RS_READY, ss->index),
+                                             m->W, m->rank, epoch, m->s_rs));
+        ph.done();
+      }
+      {
+        ProfScope pp(m, FSDP_PROF_RS_PULL, m->s_rs, (int64_t)(m->W - 1) * l->pull_elems * gsz);
+        CUDA_CHECK(fsdpp::launch_rs_pull(l->t_pull.d, l->t_pull.n, peer_ptrs(m, ss->buf), gd == FSDP_BFLOAT16, l->grad,
+                                         mean != 0, accumulate != 0, obf, m->W, m->cfg, m->s_rs));
+        pp.done();
+      }
+      {
+        ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_rs, 0);
+        CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_DONE, ss->index), flag_local(m, FK_RS_DONE, ss->index),
+                                             m->W, m->rank, epoch, m->s_rs));
+        ph.done();
+      }
+      CUDA_CHECK(cudaEventRecord(l->ev_rs_done, m->s_rs));
+      CUDA_CHECK(cudaEventRecord(ss->free_ev, m->s_rs));
+      ss->ever_used = true;
+      ss->in_use = false;
+      l->rs_pending = true;
+      return;
+    }
     // fp32, no accumulation: the reduce-scatter (or, at W=1, K5 itself) writes straight
     // into the layer's grad buffer — the zero-copy "view" copy-out
     const bool direct = !obf && !accumulate;

@@ -168,3 +168,74 @@ void append_tiles_amax(const Layout& L, const float* shard_dev, int reg_base, st
 }
 
 }  // namespace fsdpl
+
+namespace fsdpl {
+
+std::vector<int64_t> staging_offsets(const Layout& L, int64_t* total) {
+  std::vector<int64_t> off(L.metas.size());
+  int64_t o = 0;
+  for (size_t p = 0; p < L.metas.size(); ++p) {
+    off[p] = o;
+    o += round_up(L.numel[p], 128);
+  }
+  *total = o;
+  return off;
+}
+
+std::vector<fsdpk::Tile> tiles_push(const Layout& L, bool fp8) {
+  std::vector<fsdpk::Tile> t;
+  for (size_t p = 0; p < L.metas.size(); ++p) {
+    const auto& m = L.metas[p];
+    const bool f8 = fp8 && L.fp8[p];
+    const int64_t es = f8 ? 1 : 2;
+    const int64_t base = (fp8 ? L.uoff_fp8[p] : L.uoff_bf16[p]) + m.row_begin * m.rest * es;
+    const int64_t cnt = m.row_count * m.rest;
+    for (int64_t j = 0; j < cnt; j += fsdpk::kTileElems) {
+      fsdpk::Tile x{};
+      x.src = (uint64_t)(m.elem_offset + j);
+      x.dst = (uint64_t)(base + j * es);
+      x.n = (uint32_t)std::min<int64_t>(fsdpk::kTileElems, cnt - j);
+      x.param = (uint32_t)p;
+      x.kind = f8 ? fsdpk::TK_FP8 : fsdpk::TK_BF16;
+      t.push_back(x);
+    }
+  }
+  return t;
+}
+
+std::vector<fsdpk::Tile> tiles_pull(const Layout& L, const std::vector<int64_t>& stg_off) {
+  std::vector<fsdpk::Tile> t;
+  for (size_t p = 0; p < L.metas.size(); ++p) {
+    const auto& m = L.metas[p];
+    const int64_t cnt = m.row_count * m.rest;
+    for (int64_t j = 0; j < cnt; j += fsdpk::kTileElems) {
+      fsdpk::Tile x{};
+      x.src = (uint64_t)(stg_off[p] + m.row_begin * m.rest + j);
+      x.dst = (uint64_t)(m.elem_offset + j);
+      x.n = (uint32_t)std::min<int64_t>(fsdpk::kTileElems, cnt - j);
+      x.param = (uint32_t)p;
+      x.kind = fsdpk::TK_COPY;
+      t.push_back(x);
+    }
+  }
+  return t;
+}
+
+std::vector<fsdpk::Tile> tiles_stage(const Layout& L, const std::vector<int64_t>& stg_off, int64_t gsize) {
+  std::vector<fsdpk::Tile> t;
+  for (size_t p = 0; p < L.metas.size(); ++p) {
+    const int64_t bytes = L.numel[p] * gsize;
+    for (int64_t j = 0; j < bytes; j += fsdpk::kTileBytes) {
+      fsdpk::Tile x{};
+      x.src = (uint64_t)j;
+      x.dst = (uint64_t)(stg_off[p] * gsize + j);
+      x.n = (uint32_t)std::min<int64_t>(fsdpk::kTileBytes, bytes - j);
+      x.param = (uint32_t)p;
+      x.kind = fsdpk::TK_COPY;
+      t.push_back(x);
+    }
+  }
+  return t;
+}
+
+}  // namespace fsdpl

@@ -44,4 +44,16 @@ std::vector<fsdpk::Tile> tiles_rs_copy_in(const Layout& L, std::vector<int>* fir
 void append_tiles_amax(const Layout& L, const float* shard_dev, int reg_base,
                        std::vector<fsdpk::Tile>* out);
 
+// ---- P2P path (p2p.h)
+// Full-grad staging layout: param p at element offset stg_off[p] (128-element aligned).
+std::vector<int64_t> staging_offsets(const Layout& L, int64_t* total_elems);
+// Push: this rank's real rows of param p: src = shard element offset, dst = byte offset of
+// those rows inside the unsharded arena (bf16 or fp8 arena), kind TK_BF16 / TK_FP8.
+std::vector<fsdpk::Tile> tiles_push(const Layout& L, bool fp8);
+// Pull: this rank's rows of param p: src = element offset into every rank's staging,
+// dst = element offset into the fp32 grad.
+std::vector<fsdpk::Tile> tiles_pull(const Layout& L, const std::vector<int64_t>& stg_off);
+// Staging gather: src = byte offset in grads[param], dst = byte offset in the staging.
+std::vector<fsdpk::Tile> tiles_stage(const Layout& L, const std::vector<int64_t>& stg_off, int64_t gsize);
+
 }  // namespace fsdpl

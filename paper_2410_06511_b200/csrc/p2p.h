@@ -1,0 +1,54 @@
+// Fused peer-memory (NVLink / NVSwitch) kernels of the unshard and the gradient
+// reduce-scatter (the paper's SymmetricMemory idea, P:147 / P:537,
+// applied to FSDP's collectives).  Buffers are symmetric: every rank allocates the same
+// sizes and maps its peers' copies with CUDA IPC, so a kernel can load/store any rank's
+// buffer directly.
+//
+//   unshard:  k_signal_wait(ready) -> k_unshard_push -> k_signal_wait(done)
+//             each rank casts its fp32 shard once (bf16 / e4m3 with per-tensor scale) and
+//             stores the result into EVERY rank's unsharded-parameter arena at its rows:
+//             copy-in + all-gather + copy-out in one kernel, no staging buffer.
+//   reduce:   k_gather_copy (caller grads -> own symmetric staging, skipped if the caller
+//             wrote there) -> k_signal_wait(ready) -> k_rs_pull -> k_signal_wait(done)
+//             each rank reads its row chunk from every rank's staged bf16 grads, divides
+//             each by W and sums in ascending rank order in fp32: the fp32
+//             reduce-scatter with bf16 (not fp32) bytes on the wire and a deterministic
+//             order.
+// Only the single-CTA signal/wait kernels spin; the data kernels never block SMs.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+
+namespace fsdpp {
+
+constexpr int kMaxRanks = 16;
+
+struct PeerPtrs { uint8_t* p[kMaxRanks]; };
+struct FlagPtrs { unsigned long long* p[kMaxRanks]; };
+
+// Thread r < W: st.release.sys flags_remote.p[r][my_rank] = epoch (signal rank r), after a
+// system-scope fence; then every thread r < W spins (ld.acquire.sys) until
+// flags_local[r] >= epoch (rank r signalled me).  One CTA.
+cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
+                               unsigned long long epoch, cudaStream_t st);
+
+// Push tiles: src = element offset into the fp32 shard, dst = byte offset into the arena,
+// n elements, kind TK_BF16 / TK_FP8 (scale = scales[param]).  Stores go to arena.p[d] for
+// every rank d (d = rank is the local arena), rotated by rank to spread NVLink traffic.
+cudaError_t launch_unshard_push(const fsdpk::Tile* tiles, int ntiles, const float* shard,
+                                const float* scales, PeerPtrs arena, int W, int rank,
+                                fsdpk::LaunchCfg cfg, cudaStream_t st);
+
+// Pull tiles: src = element offset into every rank's staging, dst = element offset into the
+// fp32 grad, n elements.  grad[dst+e] (+)= round?( sum_{q=0..W-1} (fp32(stage_q[src+e]) / W) ).
+cudaError_t launch_rs_pull(const fsdpk::Tile* tiles, int ntiles, PeerPtrs staging, bool grad_bf16,
+                           float* grad, bool mean, bool accumulate, bool bf16_reduce, int W,
+                           fsdpk::LaunchCfg cfg, cudaStream_t st);
+
+// Gather copy: dst + tile.dst <- srcs.p[param] + tile.src, n bytes (any alignment).
+cudaError_t launch_gather_copy(const fsdpk::Tile* tiles, int ntiles, const fsdpk::PtrArray& srcs,
+                               void* dst, fsdpk::LaunchCfg cfg, cudaStream_t st);
+
+}  // namespace fsdpp

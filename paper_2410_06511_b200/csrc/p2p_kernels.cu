@@ -1,0 +1,335 @@
+// Fused peer-memory kernels (see p2p.h): unshard push, reduce-scatter pull, the
+// signal/wait handshake and the grad staging gather.  sm_100a, no fast math.
+#include "p2p.h"
+
+#include "dev_util.cuh"
+
+namespace fsdpp {
+namespace {
+
+using namespace fsdpdev;
+using fsdpk::Tile;
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ------------------------------------------------------------------- handshake
+__global__ void k_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
+                              unsigned long long epoch) {
+  const int r = threadIdx.x;
+  __threadfence_system();   // order this GPU's earlier stores (previous kernels) before the flag
+  __syncthreads();
+  if (r < W) st_release_sys(remote.p[r] + rank, epoch);
+  if (r < W) {
+    while (ld_acquire_sys(local + r) < epoch) __nanosleep(64);
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+// ------------------------------------------------------------------- unshard push
+template <int V>   // floats per 16-byte output vector: 8 (bf16) or 16 (e4m3)
+__device__ __forceinline__ void load_floats(const float* p, uint32_t ph, float (&x)[V]) {
+  // p = aligned base (16 B); the V floats start at word ph (0..3)
+  constexpr int NQ = V / 4 + 1;
+  float w[NQ * 4];
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) {
+    if (i < V / 4 || ph != 0) {
+      const uint4 q = ld_stream(p + 4 * i);
+      w[4 * i] = __uint_as_float(q.x); w[4 * i + 1] = __uint_as_float(q.y);
+      w[4 * i + 2] = __uint_as_float(q.z); w[4 * i + 3] = __uint_as_float(q.w);
+    }
+  }
+  switch (ph) {
+    case 0:
+#pragma unroll
+      for (int i = 0; i < V; ++i) x[i] = w[i];
+      break;
+    case 1:
+#pragma unroll
+      for (int i = 0; i < V; ++i) x[i] = w[i + 1];
+      break;
+    case 2:
+#pragma unroll
+      for (int i = 0; i < V; ++i) x[i] = w[i + 2];
+      break;
+    default:
+#pragma unroll
+      for (int i = 0; i < V; ++i) x[i] = w[i + 3];
+      break;
+  }
+}
+
+__device__ __forceinline__ uint4 cvt_bf16x8(const float (&x)[8]) {
+  return make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]), pack_bf16x2(x[4], x[5]),
+                    pack_bf16x2(x[6], x[7]));
+}
+__device__ __forceinline__ uint4 cvt_e4m3x16(const float (&x)[16], float s) {
+  uint32_t w[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t lo = pack_e4m3x2(__fmul_rn(x[4 * j], s), __fmul_rn(x[4 * j + 1], s));
+    const uint32_t hi = pack_e4m3x2(__fmul_rn(x[4 * j + 2], s), __fmul_rn(x[4 * j + 3], s));
+    w[j] = lo | (hi << 16);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <bool kFp8>
+__device__ __forceinline__ void push_tile(const Tile& tl, const float* __restrict__ shard, float s,
+                                          const PeerPtrs& arena, int W, int rank) {
+  constexpr uint32_t es = kFp8 ? 1 : 2;
+  constexpr uint32_t V = 16 / es;
+  const float* src = shard + tl.src;
+  const uint64_t dst0 = tl.dst;
+  const uint32_t n = tl.n;
+  uint32_t h = (uint32_t)(((16u - (uint32_t)(dst0 & 15u)) & 15u) / es);
+  if (h > n) h = n;
+  const uint32_t nb = (n - h) / V;
+  const uint32_t ph = h & 3u;
+  const float* abase = src + (h - ph);
+  // body: full 16-byte vectors, stored to every rank's arena
+  for (uint32_t v = threadIdx.x; v < nb; v += kThreads) {
+    float x[V];
+    load_floats<V>(abase + V * v, ph, x);
+    uint4 o;
+    if constexpr (kFp8) o = cvt_e4m3x16(x, s);
+    else o = cvt_bf16x8(x);
+    const uint64_t off = dst0 + (uint64_t)h * es + 16ull * v;
+#pragma unroll 1
+    for (int i = 0; i < W; ++i) {
+      int d = rank + 1 + i;
+      d = d >= W ? d - W : d;
+      st_v4(arena.p[d] + off, o);
+    }
+  }
+  // head and tail elements (partial 16-byte vectors: element-sized stores only)
+  const uint32_t tail0 = h + nb * V;
+  for (uint32_t e = threadIdx.x; e < h + (n - tail0); e += kThreads) {
+    const uint32_t el = e < h ? e : tail0 + (e - h);
+    const uint64_t off = dst0 + (uint64_t)el * es;
+    if (kFp8) {
+      const uint8_t b = (uint8_t)(pack_e4m3x2(__fmul_rn(src[el], s), 0.0f) & 0xFFu);
+      for (int d = 0; d < W; ++d) arena.p[d][off] = b;
+    } else {
+      const uint16_t b = (uint16_t)(pack_bf16x2(src[el], 0.0f) & 0xFFFFu);
+      for (int d = 0; d < W; ++d) *reinterpret_cast<uint16_t*>(arena.p[d] + off) = b;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_unshard_push(const Tile* __restrict__ tiles, int ntiles,
+                                                           const float* __restrict__ shard,
+                                                           const float* __restrict__ scales, PeerPtrs arena,
+                                                           int W, int rank) {
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    if (tl.kind == fsdpk::TK_FP8) push_tile<true>(tl, shard, scales[tl.param], arena, W, rank);
+    else push_tile<false>(tl, shard, 0.0f, arena, W, rank);
+  }
+  __threadfence_system();
+}
+
+// ------------------------------------------------------------------- reduce-scatter pull
+// 4 consecutive grad elements (as fp32) from byte address p with phase k (bytes).
+template <bool kGradBf16, bool kAligned>
+__device__ __forceinline__ void load4(const uint8_t* p, uint32_t k, float (&x)[4]) {
+  if (kGradBf16) {
+    uint2 a;
+    if (kAligned) {
+      asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(a.x), "=r"(a.y) : "l"(p));
+    } else {   // k in {2,4,6}
+      const uint8_t* b = p - k;
+      uint2 u, w;
+      asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(u.x), "=r"(u.y) : "l"(b));
+      asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(w.x), "=r"(w.y) : "l"(b + 8));
+      const uint32_t sh = (k & 3u) * 8u;
+      if (k < 4) { a.x = __funnelshift_r(u.x, u.y, sh); a.y = __funnelshift_r(u.y, w.x, sh); }
+      else { a.x = __funnelshift_r(u.y, w.x, sh); a.y = __funnelshift_r(w.x, w.y, sh); }
+    }
+    x[0] = bf16_lo(a.x); x[1] = bf16_hi(a.x); x[2] = bf16_lo(a.y); x[3] = bf16_hi(a.y);
+  } else {
+    const uint4 a = load16<kAligned>(p, k);
+    x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y);
+    x[2] = __uint_as_float(a.z); x[3] = __uint_as_float(a.w);
+  }
+}
+
+struct PullOps {
+  float w, inv;
+  bool pow2, mean, acc, bf16r;
+  __device__ __forceinline__ float div(float x) const {
+    if (!mean) return x;
+    return pow2 ? __fmul_rn(x, inv) : __fdiv_rn(x, w);
+  }
+  __device__ __forceinline__ float rb(float x) const {   // bf16 rounding (bf16 reduce)
+    return bf16r ? bf16_lo(pack_bf16x2(x, 0.0f)) : x;
+  }
+};
+
+template <int W, bool kGradBf16, bool kAligned>
+__device__ __forceinline__ void pull_body(const PeerPtrs& st, uint64_t sb, float* __restrict__ g, uint32_t nv,
+                                          uint32_t k, PullOps ops) {
+  constexpr uint32_t gs = kGradBf16 ? 2 : 4;
+  constexpr int U = W <= 4 ? 4 : 2;
+  uint32_t v = threadIdx.x;
+  for (; v + (U - 1) * kThreads < nv; v += U * kThreads) {
+    float x[U][W][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < W; ++q)
+        load4<kGradBf16, kAligned>(st.p[q] + sb + (uint64_t)gs * 4 * (v + u * kThreads), k, x[u][q]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float a[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        a[j] = ops.rb(ops.div(x[u][0][j]));
+#pragma unroll
+        for (int q = 1; q < W; ++q) a[j] = __fadd_rn(a[j], ops.rb(ops.div(x[u][q][j])));
+        a[j] = ops.rb(a[j]);
+      }
+      float4* gp = reinterpret_cast<float4*>(g) + v + u * kThreads;
+      if (ops.acc) {
+        const float4 o = *gp;
+        a[0] = __fadd_rn(o.x, a[0]); a[1] = __fadd_rn(o.y, a[1]); a[2] = __fadd_rn(o.z, a[2]); a[3] = __fadd_rn(o.w, a[3]);
+      }
+      *gp = make_float4(a[0], a[1], a[2], a[3]);
+    }
+  }
+  for (; v < nv; v += kThreads) {
+    float x[W][4];
+#pragma unroll
+    for (int q = 0; q < W; ++q) load4<kGradBf16, kAligned>(st.p[q] + sb + (uint64_t)gs * 4 * v, k, x[q]);
+    float a[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      a[j] = ops.rb(ops.div(x[0][j]));
+#pragma unroll
+      for (int q = 1; q < W; ++q) a[j] = __fadd_rn(a[j], ops.rb(ops.div(x[q][j])));
+      a[j] = ops.rb(a[j]);
+    }
+    float4* gp = reinterpret_cast<float4*>(g) + v;
+    if (ops.acc) {
+      const float4 o = *gp;
+      a[0] = __fadd_rn(o.x, a[0]); a[1] = __fadd_rn(o.y, a[1]); a[2] = __fadd_rn(o.z, a[2]); a[3] = __fadd_rn(o.w, a[3]);
+    }
+    *gp = make_float4(a[0], a[1], a[2], a[3]);
+  }
+}
+
+template <int W, bool kGradBf16>
+__global__ void __launch_bounds__(kThreads) k_rs_pull(const Tile* __restrict__ tiles, int ntiles, PeerPtrs st,
+                                                      float* __restrict__ grad, PullOps ops) {
+  constexpr uint32_t gs = kGradBf16 ? 2 : 4;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    const uint64_t sb = tl.src * gs;      // byte offset into every rank's staging
+    float* g = grad + tl.dst;             // 16-byte aligned
+    const uint32_t n = tl.n;
+    const uint32_t nv = n / 4;
+    const uint32_t k = (uint32_t)(sb & (kGradBf16 ? 7u : 15u));
+    if (k == 0) pull_body<W, kGradBf16, true>(st, sb, g, nv, 0, ops);
+    else pull_body<W, kGradBf16, false>(st, sb, g, nv, k, ops);
+    for (uint32_t e = nv * 4 + threadIdx.x; e < n; e += kThreads) {
+      float a = 0.0f;
+      for (int q = 0; q < W; ++q) {
+        const uint8_t* p = st.p[q] + sb + (uint64_t)gs * e;
+        const float x = kGradBf16 ? __uint_as_float(((uint32_t)(*(const uint16_t*)p)) << 16) : *(const float*)p;
+        const float y = ops.rb(ops.div(x));
+        a = q == 0 ? y : __fadd_rn(a, y);
+      }
+      a = ops.rb(a);
+      g[e] = ops.acc ? __fadd_rn(g[e], a) : a;
+    }
+  }
+}
+
+// ------------------------------------------------------------------- gather copy
+__global__ void __launch_bounds__(kThreads) k_gather_copy(const Tile* __restrict__ tiles, int ntiles,
+                                                          fsdpk::PtrArray srcs, uint8_t* __restrict__ dst_base) {
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    const uint8_t* s = (const uint8_t*)srcs.p[tl.param] + tl.src;
+    uint8_t* d = dst_base + tl.dst;
+    uint32_t n = tl.n;
+    uint32_t head = (uint32_t)((16u - ((uintptr_t)d & 15u)) & 15u);
+    if (head > n) head = n;
+    if (threadIdx.x < head) d[threadIdx.x] = s[threadIdx.x];
+    s += head; d += head; n -= head;
+    const uint32_t nv = n >> 4;
+    const uint32_t k = (uint32_t)((uintptr_t)s & 15u);
+    if (k == 0) copy_body<true>(s, d, nv, 0);
+    else copy_body<false>(s, d, nv, k);
+    for (uint32_t e = nv * 16 + threadIdx.x; e < n; e += kThreads) d[e] = s[e];
+  }
+}
+
+inline int grid_for(int64_t items, fsdpk::LaunchCfg cfg) {
+  int64_t g = items < cfg.grid_cap ? items : cfg.grid_cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+template <bool kGradBf16>
+cudaError_t launch_pull_w(const Tile* tiles, int ntiles, PeerPtrs st, float* grad, PullOps ops, int W, int g,
+                          cudaStream_t s) {
+  switch (W) {
+    case 1: k_rs_pull<1, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 2: k_rs_pull<2, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 3: k_rs_pull<3, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 4: k_rs_pull<4, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 5: k_rs_pull<5, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 6: k_rs_pull<6, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 7: k_rs_pull<7, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 8: k_rs_pull<8, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
+                               unsigned long long epoch, cudaStream_t st) {
+  k_signal_wait<<<1, 32, 0, st>>>(remote, local, W, rank, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unshard_push(const Tile* tiles, int ntiles, const float* shard, const float* scales,
+                                PeerPtrs arena, int W, int rank, fsdpk::LaunchCfg cfg, cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  k_unshard_push<<<grid_for(ntiles, cfg), kThreads, 0, st>>>(tiles, ntiles, shard, scales, arena, W, rank);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool grad_bf16, float* grad, bool mean,
+                           bool accumulate, bool bf16_reduce, int W, fsdpk::LaunchCfg cfg, cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  PullOps ops;
+  ops.w = (float)W;
+  ops.inv = 1.0f / (float)W;
+  ops.pow2 = (W & (W - 1)) == 0;
+  ops.mean = mean;
+  ops.acc = accumulate;
+  ops.bf16r = bf16_reduce;
+  const int g = grid_for(ntiles, cfg);
+  return grad_bf16 ? launch_pull_w<true>(tiles, ntiles, staging, grad, ops, W, g, st)
+                   : launch_pull_w<false>(tiles, ntiles, staging, grad, ops, W, g, st);
+}
+
+cudaError_t launch_gather_copy(const Tile* tiles, int ntiles, const fsdpk::PtrArray& srcs, void* dst,
+                               fsdpk::LaunchCfg cfg, cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  k_gather_copy<<<grid_for(ntiles, cfg), kThreads, 0, st>>>(tiles, ntiles, srcs, (uint8_t*)dst);
+  return cudaGetLastError();
+}
+
+}  // namespace fsdpp

@@ -133,6 +133,16 @@ class Mesh:
         dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
         return cls(W, r, device, unique_id=obj[0])
 
+    @property
+    def algo(self) -> str:
+        a = C.c_int32()
+        call("fsdp_mesh_get_algo", self.handle, C.byref(a))
+        return "p2p" if a.value == capi.ALGO_P2P else "nccl"
+
+    def set_algo(self, algo: str):
+        """Collective: 'nccl' (copy-in -> NCCL -> copy-out) or 'p2p' (fused NVLink kernels)."""
+        call("fsdp_mesh_set_algo", self.handle, capi.ALGO_P2P if algo == "p2p" else capi.ALGO_NCCL)
+
     def synchronize(self, timeout_ms: int = 0):
         call("fsdp_mesh_synchronize", self.handle, int(timeout_ms))
 

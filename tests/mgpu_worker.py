@@ -38,6 +38,18 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     mesh = F.Mesh.from_process_group(device=local)
+    algos = ["p2p", "nccl"] if mesh.algo == "p2p" else ["nccl"]
+    for algo in algos:
+        mesh.set_algo(algo)
+        run_checks(mesh, W, rank, local, algo)
+    mesh.synchronize(120000)
+    mesh.destroy()
+    dist.barrier()
+    dist.destroy_process_group()
+    print(f"RANK {rank}/{W} OK (algos {algos})", flush=True)
+
+
+def run_checks(mesh, W, rank, local, algo):
     checks = 0
 
     units = [synth.model_units("toy")[0], synth.model_units("toy")[-1]] + \
@@ -81,6 +93,10 @@ def main():
                 got = layer.sharded_grad(p).cpu().numpy()
                 if kind == "dyadic":
                     np.testing.assert_array_equal(got, ref["exact"][p])
+                elif algo == "p2p":
+                    # the pull kernel sums fp32(g_q)/W in ascending rank order: bit-exact
+                    # to the oracle's ordered sum (SPEC.md:159 reduction order)
+                    np.testing.assert_array_equal(got, ref["order"][p])
                 else:
                     ok, ratio, nrel = rs_error_ok(got.reshape(-1), ref["exact"][p].reshape(-1),
                                                   ref["mag"][p].reshape(-1), W)
@@ -156,11 +172,10 @@ def main():
             g = l.sharded_grad(p)
             if g.numel():
                 assert torch.all(g == float(want_g)), (i, p)
+    for l in layers:
+        l.destroy()
     mesh.synchronize(120000)
-    mesh.destroy()
-    dist.barrier()
-    dist.destroy_process_group()
-    print(f"RANK {rank}/{W} OK ({checks} units)", flush=True)
+    print(f"rank {rank}/{W} algo={algo}: {checks} units + pipeline OK", flush=True)
 
 
 if __name__ == "__main__":

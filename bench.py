@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--serial", action="store_true", help="no prefetch: each unit isolated")
+    ap.add_argument("--algo", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="collectives: fused NVLink peer-memory kernels (p2p) or NCCL; auto = library default")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     return ap.parse_args()
 
@@ -134,6 +136,9 @@ def run_ours(args):
         mesh = F.Mesh.from_process_group(device=local)
     else:
         mesh = F.Mesh(1, 0, local, unique_id=F.get_unique_id())
+    if args.algo != "auto" and N > 1:
+        mesh.set_algo(args.algo)
+    algo = mesh.algo if N > 1 else "local (W=1: identity collectives)"
     wl = WORKLOADS[args.workload]
     units = unit_lists(wl["model"])
     if wl["cycle"]:   # 70B: cycle `cycle` distinct block instances (memory), SURVEY.md §8(d) row 4
@@ -219,19 +224,28 @@ def run_ours(args):
     algbw_rank = bytes_rank / (ms_max * 1e-3) / 1e9
     busbw_rank = algbw_rank * (W - 1) / W
 
-    # ---- roofline of the dominant kernel (largest total device time among ours)
+    # ---- roofline of the dominant kernel (largest total device time among ours).
+    # HBM-bound kernels are measured against the measured HBM copy peak; the fused P2P
+    # kernels are NVLink-bound: their bytes are the per-rank NVLink bytes, measured against
+    # the measured per-direction peer bandwidth (B200_PROFILING.md: 770 GB/s; 900 nominal).
     peak, peak_src = measured_peaks()
-    ours = ["copy_in", "copy_out", "rs_copy_in", "rs_copy_out", "amax", "scale"]
-    dom = max(ours, key=lambda k: prof[k]["ms"])
+    hbm_k = ["copy_in", "copy_out", "rs_copy_in", "rs_copy_out", "amax", "scale", "stage_grads"]
+    nvl_k = ["unshard_push", "rs_pull"]
+    ours = hbm_k + nvl_k + ["handshake"]
+    dom = max(hbm_k + nvl_k, key=lambda k: prof[k]["ms"])
     d = prof[dom]
     per_launch_bytes = d["bytes"] / max(d["launches"], 1)
     avg_ms = d["ms"] / max(d["launches"], 1)
     achieved = per_launch_bytes / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
+    if dom in nvl_k:
+        bound, peak, peak_src = "nvlink", 770.0, "measured peer copy per direction (B200_PROFILING.md; 900 nominal)"
+    else:
+        bound = "hbm"
     kernels = {}
     for k in ours + ["all_gather", "reduce_scatter", "all_reduce"]:
         if prof[k]["launches"]:
             kernels[k] = {"launches": prof[k]["launches"], "avg_us": round(prof[k]["ms"] / prof[k]["launches"] * 1e3, 2),
-                          "GBps": round(prof[k]["bytes"] / (prof[k]["ms"] * 1e-3) / 1e9, 1) if prof[k]["ms"] else None,
+                          "GBps": round(prof[k]["bytes"] / (prof[k]["ms"] * 1e-3) / 1e9, 1) if prof[k]["ms"] and prof[k]["bytes"] else None,
                           "share_of_step": round(prof[k]["ms"] / args.steps / ms_max, 4)}
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -262,13 +276,13 @@ def run_ours(args):
                                    f"({'32 blocks + root' if args.workload.startswith('llama3.1-8b') else 'see DESIGN.md'}), "
                                    f"{'fp8 e4m3' if wl['fp8'] else 'bf16'} all-gather / fp32 reduce-scatter, "
                                    f"{'serial' if args.serial else 'prefetch next unit'}",
-                       "world_size": W, "units": len(layers),
+                       "world_size": W, "units": len(layers), "collectives": algo,
                        "l2": "inputs larger than L2 (every unit's shard/grads/buffers are 100s of MB; 126 MB L2)",
                        "bytes_per_step_per_rank": bytes_rank},
             "per_rank": {"algbw_GBps": round(algbw_rank, 2), "busbw_GBps": round(busbw_rank, 2),
                          "busbw_frac_nvlink_900": round(busbw_rank / NVLINK_GBS, 4)},
             "kernels": kernels,
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+            "roofline": {"bound": bound, "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
                          "bytes_per_launch": int(per_launch_bytes), "traffic": traffic},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,

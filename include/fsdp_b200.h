@@ -289,6 +289,30 @@ fsdp_status_t fsdp_stage_rs_copy_in(const fsdp_layer_t* layer, const void* const
 fsdp_status_t fsdp_stage_rs_copy_out(fsdp_layer_t* layer, const void* rs_out_dev,
                                      fsdp_dtype_t reduce_dtype, int32_t accumulate, void* stream);
 
+/* ---- the P2P kernels without their handshakes (FSDP_ALGO_P2P) */
+/* Unsharded arena layout for param_dtype: byte offset of param p (256-byte aligned) and
+ * the arena size.  offsets: caller array of P entries (may be NULL). */
+fsdp_status_t fsdp_unsharded_layout(const fsdp_layer_t* layer, fsdp_dtype_t param_dtype,
+                                    int64_t* offsets, int64_t* total_bytes);
+/* K7 push: casts this rank's rows of every param (bf16, or e4m3fn with fp8_scales_dev[p] for
+ * eligible params when param_dtype is FLOAT8) and stores them at their place in each of the
+ * W arenas arenas_dev[0..W-1] (any device memory the current device can store to, e.g.
+ * peer-mapped).  Running it for every rank fills every arena with the full tensors. */
+fsdp_status_t fsdp_stage_unshard_push(const fsdp_layer_t* layer, fsdp_dtype_t param_dtype,
+                                      const float* fp8_scales_dev, void* const* arenas_dev,
+                                      void* stream);
+/* Grad staging layout: param p's full grad at element offset elem_offsets[p] (128-aligned). */
+fsdp_status_t fsdp_grad_staging_layout(const fsdp_layer_t* layer, int64_t* elem_offsets,
+                                       int64_t* total_elems);
+/* Copies this rank's full grads into a staging buffer of that layout (grad_dtype elements). */
+fsdp_status_t fsdp_stage_grads_to_staging(const fsdp_layer_t* layer, const void* const* full_grads_dev,
+                                          fsdp_dtype_t grad_dtype, void* staging_dev, void* stream);
+/* K8 pull: for this rank's rows, grad (+)= sum over q = 0..W-1 ascending of
+ * fp32(stagings_dev[q]) / W (mean) — bf16 reduce_dtype rounds every term and the sum to bf16. */
+fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* layer, const void* const* stagings_dev,
+                                 fsdp_dtype_t grad_dtype, fsdp_dtype_t reduce_dtype, int32_t mean,
+                                 int32_t accumulate, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

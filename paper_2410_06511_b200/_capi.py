@@ -88,6 +88,11 @@ SIGNATURES = {
     "fsdp_stage_fp8_scale": [_VP, _VP, _VP, _VP],
     "fsdp_stage_rs_copy_in": [_VP, _PP, _I32, _I32, _I32, _VP, _VP],
     "fsdp_stage_rs_copy_out": [_VP, _VP, _I32, _I32, _VP],
+    "fsdp_unsharded_layout": [_VP, _I32, C.POINTER(_I64), C.POINTER(_I64)],
+    "fsdp_stage_unshard_push": [_VP, _I32, _VP, _PP, _VP],
+    "fsdp_grad_staging_layout": [_VP, C.POINTER(_I64), C.POINTER(_I64)],
+    "fsdp_stage_grads_to_staging": [_VP, _PP, _I32, _VP, _VP],
+    "fsdp_stage_rs_pull": [_VP, _PP, _I32, _I32, _I32, _I32, _VP],
 }
 _OTHER = {
     "fsdp_abi_version": ([], C.c_int32),

@@ -89,4 +89,38 @@ __device__ __forceinline__ void copy_body(const uint8_t* s, uint8_t* d, uint32_t
 }
 
 
+__device__ __forceinline__ void st_v2(void* p, uint2 v) {
+  asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+
+__device__ __forceinline__ uint2 ld_stream8(const void* p) {
+  uint2 a;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(a.x), "=r"(a.y) : "l"(p));
+  return a;
+}
+
+// 4 consecutive grad elements (as fp32) at byte address p whose phase is k: bf16 grads are
+// read as one 8-byte load (k in {0,2,4,6}: two aligned loads + funnel shift when k != 0),
+// fp32 grads as one 16-byte load (k in {0,4,8,12}).
+template <bool kGradBf16, bool kAligned>
+__device__ __forceinline__ void load4(const uint8_t* p, uint32_t k, float (&x)[4]) {
+  if (kGradBf16) {
+    uint2 a;
+    if (kAligned) {
+      a = ld_stream8(p);
+    } else {
+      const uint8_t* b = p - k;
+      const uint2 u = ld_stream8(b), w = ld_stream8(b + 8);
+      const uint32_t sh = (k & 3u) * 8u;
+      if (k < 4) { a.x = __funnelshift_r(u.x, u.y, sh); a.y = __funnelshift_r(u.y, w.x, sh); }
+      else { a.x = __funnelshift_r(u.y, w.x, sh); a.y = __funnelshift_r(w.x, w.y, sh); }
+    }
+    x[0] = bf16_lo(a.x); x[1] = bf16_hi(a.x); x[2] = bf16_lo(a.y); x[3] = bf16_hi(a.y);
+  } else {
+    const uint4 a = load16<kAligned>(p, k);
+    x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y);
+    x[2] = __uint_as_float(a.z); x[3] = __uint_as_float(a.w);
+  }
+}
+
 }  // namespace fsdpdev

@@ -239,6 +239,7 @@ struct fsdp_layer {
   std::vector<int64_t> stg_off_el;   // full-grad staging: param p at element offset (128-aligned)
   int64_t stg_elems = 0;
   int64_t push_bytes_bf16 = 0, push_bytes_fp8 = 0, pull_elems = 0;
+  int64_t local_push_bf16 = 0, local_push_fp8 = 0;
   SymSlot* p2p_slot = nullptr;       // arena of the current P2P unshard
   void* arena_base = nullptr;        // base of the unsharded tensors (either path)
 };
@@ -823,17 +824,18 @@ fsdp_status_t fsdp_shard(fsdp_mesh_t* m, int32_t n, const fsdp_param_desc_t* des
       l->t_cout_fp8.upload(fsdpl::tiles_copy_out(Ly, true, &l->t_cout_fp8.first));
       l->t_rsin.upload(fsdpl::tiles_rs_copy_in(Ly, &l->t_rsin.first));
       l->stg_off_el = fsdpl::staging_offsets(Ly, &l->stg_elems);
-      if (m->p2p_ok) {
-        l->t_push_bf16.upload(fsdpl::tiles_push(Ly, false));
-        l->t_push_fp8.upload(fsdpl::tiles_push(Ly, true));
-        l->t_pull.upload(fsdpl::tiles_pull(Ly, l->stg_off_el));
-        l->t_stage_bf16.upload(fsdpl::tiles_stage(Ly, l->stg_off_el, 2));
-        l->t_stage_fp32.upload(fsdpl::tiles_stage(Ly, l->stg_off_el, 4));
-      }
+      l->t_push_bf16.upload(fsdpl::tiles_push(Ly, false));
+      l->t_push_fp8.upload(fsdpl::tiles_push(Ly, true));
+      l->t_pull.upload(fsdpl::tiles_pull(Ly, l->stg_off_el));
+      l->t_stage_bf16.upload(fsdpl::tiles_stage(Ly, l->stg_off_el, 2));
+      l->t_stage_fp32.upload(fsdpl::tiles_stage(Ly, l->stg_off_el, 4));
       for (int p = 0; p < n; ++p) {
         const int64_t cnt = Ly.metas[p].row_count * Ly.metas[p].rest;
-        l->push_bytes_bf16 += (int64_t)(m->W - 1) * cnt * 2;
-        l->push_bytes_fp8 += (int64_t)(m->W - 1) * cnt * (Ly.fp8[p] ? 1 : 2);
+        const int64_t es8 = Ly.fp8[p] ? 1 : 2;
+        l->push_bytes_bf16 += (int64_t)(m->W - 1) * cnt * 2;      // NVLink egress
+        l->push_bytes_fp8 += (int64_t)(m->W - 1) * cnt * es8;
+        l->local_push_bf16 += cnt * (4 + 2);                        // W=1: HBM read + write
+        l->local_push_fp8 += cnt * (4 + es8);
         l->pull_elems += cnt;
       }
       for (int p = 0; p < n; ++p) {
@@ -1031,6 +1033,30 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
       l->p2p_slot = ss;
       l->slot = nullptr;
       l->arena_base = ss->buf.local;
+      l->ushard_dtype = dt;
+      l->state = UNSHARDING;
+      return;
+    }
+    if (m->W == 1) {
+      // W = 1: the all-gather is the identity, so the unshard is ONE kernel that casts the
+      // shard straight into the unsharded tensors (the push kernel with the local arena only)
+      Slot* slot = acquire_slot(m, m->ag_slots, 0, (size_t)arena, 1);
+      cudaStream_t cs = as_stream(compute);
+      CUDA_CHECK(cudaEventRecord(l->ev_call, cs));
+      CUDA_CHECK(cudaStreamWaitEvent(m->s_cin, l->ev_call, 0));
+      if (slot->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_cin, slot->free_ev, 0));
+      fsdpp::PeerPtrs pp{};
+      pp.p[0] = (uint8_t*)slot->b.p;
+      const DevTiles& T = fp8 ? l->t_push_fp8 : l->t_push_bf16;
+      {
+        ProfScope pc(m, FSDP_PROF_COPY_IN, m->s_cin, fp8 ? l->local_push_fp8 : l->local_push_bf16);
+        CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, pp, 1, 0, m->cfg, m->s_cin));
+        pc.done();
+      }
+      CUDA_CHECK(cudaEventRecord(l->ev_done, m->s_cin));
+      l->slot = slot;
+      l->p2p_slot = nullptr;
+      l->arena_base = slot->b.p;
       l->ushard_dtype = dt;
       l->state = UNSHARDING;
       return;
@@ -1351,6 +1377,93 @@ fsdp_status_t fsdp_stage_rs_copy_out(fsdp_layer_t* l, const void* rs_out, fsdp_d
     CUDA_CHECK(fsdpk::launch_rs_copy_out(rs_out, rd == FSDP_BFLOAT16, l->grad, accumulate != 0, l->L.S,
                                          l->mesh->cfg, as_stream(stream)));
     po.done();
+  });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------- P2P stage entry points
+extern "C" {
+
+fsdp_status_t fsdp_unsharded_layout(const fsdp_layer_t* l, fsdp_dtype_t dt, int64_t* offsets, int64_t* total) {
+  return guarded([&] {
+    if (!l) fail(FSDP_ERR_INVALID_ARGUMENT, "layer is NULL");
+    if (dt != FSDP_BFLOAT16 && dt != FSDP_FLOAT8_E4M3FN) fail(FSDP_ERR_DTYPE, "param_dtype must be BFLOAT16 or FLOAT8_E4M3FN");
+    const bool fp8 = dt == FSDP_FLOAT8_E4M3FN;
+    const auto& u = fp8 ? l->L.uoff_fp8 : l->L.uoff_bf16;
+    if (offsets) std::copy(u.begin(), u.end(), offsets);
+    if (total) *total = fp8 ? l->L.arena_fp8 : l->L.arena_bf16;
+  });
+}
+
+fsdp_status_t fsdp_stage_unshard_push(const fsdp_layer_t* lc, fsdp_dtype_t dt, const float* scales,
+                                      void* const* arenas, void* stream) {
+  return guarded([&] {
+    fsdp_layer* l = const_cast<fsdp_layer*>(lc);
+    check_layer(l);
+    fsdp_mesh* m = l->mesh;
+    if (m->W > fsdpp::kMaxRanks) fail(FSDP_ERR_UNAVAILABLE, "world size above the P2P limit");
+    if (!arenas) fail(FSDP_ERR_INVALID_ARGUMENT, "arenas is NULL");
+    if (dt != FSDP_BFLOAT16 && dt != FSDP_FLOAT8_E4M3FN) fail(FSDP_ERR_DTYPE, "param_dtype must be BFLOAT16 or FLOAT8_E4M3FN");
+    const bool fp8 = dt == FSDP_FLOAT8_E4M3FN;
+    if (fp8 && !scales) scales = m->reg_scale + l->reg_base;
+    fsdpp::PeerPtrs pp{};
+    for (int r = 0; r < m->W; ++r) {
+      if (!arenas[r]) fail(FSDP_ERR_INVALID_ARGUMENT, "arenas[r] is NULL");
+      pp.p[r] = (uint8_t*)arenas[r];
+    }
+    DeviceGuard g(m->device);
+    const DevTiles& T = fp8 ? l->t_push_fp8 : l->t_push_bf16;
+    ProfScope ps(m, FSDP_PROF_UNSHARD_PUSH, as_stream(stream), fp8 ? l->push_bytes_fp8 : l->push_bytes_bf16);
+    CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, pp, m->W, m->rank, m->cfg, as_stream(stream)));
+    ps.done();
+  });
+}
+
+fsdp_status_t fsdp_grad_staging_layout(const fsdp_layer_t* l, int64_t* offsets, int64_t* total) {
+  return guarded([&] {
+    if (!l) fail(FSDP_ERR_INVALID_ARGUMENT, "layer is NULL");
+    if (offsets) std::copy(l->stg_off_el.begin(), l->stg_off_el.end(), offsets);
+    if (total) *total = l->stg_elems;
+  });
+}
+
+fsdp_status_t fsdp_stage_grads_to_staging(const fsdp_layer_t* lc, const void* const* grads, fsdp_dtype_t gd,
+                                          void* staging, void* stream) {
+  return guarded([&] {
+    fsdp_layer* l = const_cast<fsdp_layer*>(lc);
+    check_layer(l);
+    validate_grads(l, grads, gd, FSDP_FLOAT32);
+    if (!staging) fail(FSDP_ERR_INVALID_ARGUMENT, "staging is NULL");
+    DeviceGuard g(l->mesh->device);
+    const DevTiles& T = gd == FSDP_BFLOAT16 ? l->t_stage_bf16 : l->t_stage_fp32;
+    fsdpk::PtrArray pa{};
+    for (int p = 0; p < l->P; ++p) pa.p[p] = grads[p];
+    ProfScope ps(l->mesh, FSDP_PROF_STAGE_GRADS, as_stream(stream), 2 * l->grad_numel_total * dtype_size(gd));
+    CUDA_CHECK(fsdpp::launch_gather_copy(T.d, T.n, pa, staging, l->mesh->cfg, as_stream(stream)));
+    ps.done();
+  });
+}
+
+fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* l, const void* const* stagings, fsdp_dtype_t gd, fsdp_dtype_t rd,
+                                 int32_t mean, int32_t accumulate, void* stream) {
+  return guarded([&] {
+    check_layer(l);
+    fsdp_mesh* m = l->mesh;
+    if (m->W > 8) fail(FSDP_ERR_UNAVAILABLE, "the pull kernel supports W <= 8");
+    if (!stagings) fail(FSDP_ERR_INVALID_ARGUMENT, "stagings is NULL");
+    if (gd != FSDP_BFLOAT16 && gd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "grad_dtype must be BFLOAT16 or FLOAT32");
+    if (rd != FSDP_BFLOAT16 && rd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "reduce_dtype must be FLOAT32 or BFLOAT16");
+    fsdpp::PeerPtrs pp{};
+    for (int r = 0; r < m->W; ++r) {
+      if (!stagings[r]) fail(FSDP_ERR_INVALID_ARGUMENT, "stagings[r] is NULL");
+      pp.p[r] = (uint8_t*)stagings[r];
+    }
+    DeviceGuard g(m->device);
+    ProfScope ps(m, FSDP_PROF_RS_PULL, as_stream(stream), (int64_t)(m->W - 1) * l->pull_elems * dtype_size(gd));
+    CUDA_CHECK(fsdpp::launch_rs_pull(l->t_pull.d, l->t_pull.n, pp, gd == FSDP_BFLOAT16, l->grad, mean != 0,
+                                     accumulate != 0, rd == FSDP_BFLOAT16, m->W, m->cfg, as_stream(stream)));
+    ps.done();
   });
 }
 

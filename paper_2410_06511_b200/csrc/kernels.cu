@@ -24,35 +24,26 @@ namespace {
 using namespace fsdpdev;
 
 // ------------------------------------------------------------------- K2 copy-in bf16
+// 4 floats per thread per vector: each warp instruction loads 512 contiguous bytes and
+// stores 256 contiguous bytes.
 __global__ void __launch_bounds__(kThreads) k_copy_in_bf16(const float4* __restrict__ src,
-                                                           uint4* __restrict__ dst, int64_t n8) {
+                                                           uint2* __restrict__ dst, int64_t n4) {
+  constexpr int U = 2 * kUnroll;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  for (; i + (kUnroll - 1) * stride < n8; i += kUnroll * stride) {
-    uint4 a[kUnroll], b[kUnroll];
+  for (; i + (U - 1) * stride < n4; i += U * stride) {
+    uint4 a[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      a[u] = ld_stream(src + 2 * (i + u * stride));
-      b[u] = ld_stream(src + 2 * (i + u * stride) + 1);
-    }
+    for (int u = 0; u < U; ++u) a[u] = ld_stream(src + i + u * stride);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      uint4 o;
-      o.x = pack_bf16x2(__uint_as_float(a[u].x), __uint_as_float(a[u].y));
-      o.y = pack_bf16x2(__uint_as_float(a[u].z), __uint_as_float(a[u].w));
-      o.z = pack_bf16x2(__uint_as_float(b[u].x), __uint_as_float(b[u].y));
-      o.w = pack_bf16x2(__uint_as_float(b[u].z), __uint_as_float(b[u].w));
-      st_v4(dst + i + u * stride, o);
-    }
+    for (int u = 0; u < U; ++u)
+      st_v2(dst + i + u * stride, make_uint2(pack_bf16x2(__uint_as_float(a[u].x), __uint_as_float(a[u].y)),
+                                             pack_bf16x2(__uint_as_float(a[u].z), __uint_as_float(a[u].w))));
   }
-  for (; i < n8; i += stride) {
-    uint4 a = ld_stream(src + 2 * i), b = ld_stream(src + 2 * i + 1);
-    uint4 o;
-    o.x = pack_bf16x2(__uint_as_float(a.x), __uint_as_float(a.y));
-    o.y = pack_bf16x2(__uint_as_float(a.z), __uint_as_float(a.w));
-    o.z = pack_bf16x2(__uint_as_float(b.x), __uint_as_float(b.y));
-    o.w = pack_bf16x2(__uint_as_float(b.z), __uint_as_float(b.w));
-    st_v4(dst + i, o);
+  for (; i < n4; i += stride) {
+    const uint4 a = ld_stream(src + i);
+    st_v2(dst + i, make_uint2(pack_bf16x2(__uint_as_float(a.x), __uint_as_float(a.y)),
+                              pack_bf16x2(__uint_as_float(a.z), __uint_as_float(a.w))));
   }
 }
 
@@ -136,57 +127,38 @@ struct DivW {
   }
 };
 
-// 8 consecutive grad elements (as fp32) at byte address p with phase k.
-template <bool kGradBf16, bool kAligned>
-__device__ __forceinline__ void load8(const uint8_t* p, uint32_t k, float (&x)[8]) {
-  if (kGradBf16) {
-    const uint4 a = load16<kAligned>(p, k);
-    x[0] = bf16_lo(a.x); x[1] = bf16_hi(a.x); x[2] = bf16_lo(a.y); x[3] = bf16_hi(a.y);
-    x[4] = bf16_lo(a.z); x[5] = bf16_hi(a.z); x[6] = bf16_lo(a.w); x[7] = bf16_hi(a.w);
-  } else {
-    const uint4 a = load16<kAligned>(p, k), b = load16<kAligned>(p + 16, k);
-    x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y);
-    x[2] = __uint_as_float(a.z); x[3] = __uint_as_float(a.w);
-    x[4] = __uint_as_float(b.x); x[5] = __uint_as_float(b.y);
-    x[6] = __uint_as_float(b.z); x[7] = __uint_as_float(b.w);
-  }
-}
-
+// 4 elements per thread per vector: a warp's load instruction covers 256 B (bf16) / 512 B
+// (fp32) and its store instruction 512 B (fp32) / 256 B (bf16), both contiguous — no
+// half-filled sectors (the 8-element mapping wrote 2 x 16 B per thread at a 32 B stride).
 template <bool kOutBf16>
-__device__ __forceinline__ void store8(uint8_t* d, const float (&y)[8]) {
-  if (kOutBf16) {
-    st_v4(d, make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]), pack_bf16x2(y[4], y[5]),
-                        pack_bf16x2(y[6], y[7])));
-  } else {
-    st_v4(d, make_uint4(__float_as_uint(y[0]), __float_as_uint(y[1]), __float_as_uint(y[2]),
-                        __float_as_uint(y[3])));
-    st_v4(d + 16, make_uint4(__float_as_uint(y[4]), __float_as_uint(y[5]), __float_as_uint(y[6]),
-                             __float_as_uint(y[7])));
-  }
+__device__ __forceinline__ void store4(uint8_t* d, const float (&y)[4]) {
+  if (kOutBf16) st_v2(d, make_uint2(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3])));
+  else st_v4(d, make_uint4(__float_as_uint(y[0]), __float_as_uint(y[1]), __float_as_uint(y[2]), __float_as_uint(y[3])));
 }
 
 template <bool kGradBf16, bool kOutBf16, bool kAligned>
 __device__ __forceinline__ void rs_body(const uint8_t* s, uint8_t* d, uint32_t nv, uint32_t k, DivW div) {
-  constexpr uint32_t gs = kGradBf16 ? 16 : 32;   // source bytes per 8 elements
-  constexpr uint32_t os = kOutBf16 ? 16 : 32;    // output bytes per 8 elements
+  constexpr uint32_t gs = kGradBf16 ? 8 : 16;   // source bytes per 4 elements
+  constexpr uint32_t os = kOutBf16 ? 8 : 16;    // output bytes per 4 elements
+  constexpr int U = 2 * kUnroll;
   uint32_t v = threadIdx.x;
-  for (; v + (kUnroll - 1) * kThreads < nv; v += kUnroll * kThreads) {
-    float x[kUnroll][8];
+  for (; v + (U - 1) * kThreads < nv; v += U * kThreads) {
+    float x[U][4];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) load8<kGradBf16, kAligned>(s + gs * (v + u * kThreads), k, x[u]);
+    for (int u = 0; u < U; ++u) load4<kGradBf16, kAligned>(s + gs * (v + u * kThreads), k, x[u]);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) x[u][j] = div(x[u][j]);
-      store8<kOutBf16>(d + os * (v + u * kThreads), x[u]);
+      for (int j = 0; j < 4; ++j) x[u][j] = div(x[u][j]);
+      store4<kOutBf16>(d + os * (v + u * kThreads), x[u]);
     }
   }
   for (; v < nv; v += kThreads) {
-    float x[8];
-    load8<kGradBf16, kAligned>(s + gs * v, k, x);
+    float x[4];
+    load4<kGradBf16, kAligned>(s + gs * v, k, x);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = div(x[j]);
-    store8<kOutBf16>(d + os * v, x);
+    for (int j = 0; j < 4; ++j) x[j] = div(x[j]);
+    store4<kOutBf16>(d + os * v, x);
   }
 }
 
@@ -201,15 +173,15 @@ __global__ void __launch_bounds__(kThreads) k_rs_copy_in(const Tile* __restrict_
     uint8_t* d = rs_in + tl.dst * osz;   // 16-byte aligned (tiles start at 16-element offsets)
     const uint32_t n = tl.n;             // multiple of 16
     const uint32_t ns = tl.pad;          // valid source elements
-    const uint32_t nv = ns / 8;
+    const uint32_t nv = ns / 4;
     const uint8_t* s = (const uint8_t*)grads.p[tl.param] + tl.src * gsz;
     if (nv > 0) {
-      const uint32_t k = (uint32_t)((uintptr_t)s & 15u);
+      const uint32_t k = (uint32_t)((uintptr_t)s & (kGradBf16 ? 7u : 15u));
       if (k == 0) rs_body<kGradBf16, kOutBf16, true>(s, d, nv, 0, div);
       else rs_body<kGradBf16, kOutBf16, false>(s, d, nv, k, div);
     }
     const uint32_t zb = min((ns + 7u) & ~7u, n);
-    for (uint32_t e = nv * 8 + threadIdx.x; e < zb; e += kThreads) {
+    for (uint32_t e = nv * 4 + threadIdx.x; e < zb; e += kThreads) {
       float x = 0.0f;
       if (e < ns) {
         if (kGradBf16) x = __uint_as_float(((uint32_t)((const uint16_t*)s)[e]) << 16);
@@ -325,10 +297,10 @@ inline int grid_for(int64_t work_items, LaunchCfg cfg) {
 }  // namespace
 
 cudaError_t launch_copy_in_bf16(const float* shard, void* slot, int64_t S, LaunchCfg cfg, cudaStream_t st) {
-  const int64_t n8 = S / 8;
-  if (n8 == 0) return cudaSuccess;
-  k_copy_in_bf16<<<grid_for((n8 + kThreads - 1) / kThreads, cfg), kThreads, 0, st>>>(
-      reinterpret_cast<const float4*>(shard), reinterpret_cast<uint4*>(slot), n8);
+  const int64_t n4 = S / 4;
+  if (n4 == 0) return cudaSuccess;
+  k_copy_in_bf16<<<grid_for((n4 + kThreads - 1) / kThreads, cfg), kThreads, 0, st>>>(
+      reinterpret_cast<const float4*>(shard), reinterpret_cast<uint2*>(slot), n4);
   return cudaGetLastError();
 }
 

@@ -138,30 +138,6 @@ __global__ void __launch_bounds__(kThreads) k_unshard_push(const Tile* __restric
 }
 
 // ------------------------------------------------------------------- reduce-scatter pull
-// 4 consecutive grad elements (as fp32) from byte address p with phase k (bytes).
-template <bool kGradBf16, bool kAligned>
-__device__ __forceinline__ void load4(const uint8_t* p, uint32_t k, float (&x)[4]) {
-  if (kGradBf16) {
-    uint2 a;
-    if (kAligned) {
-      asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(a.x), "=r"(a.y) : "l"(p));
-    } else {   // k in {2,4,6}
-      const uint8_t* b = p - k;
-      uint2 u, w;
-      asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(u.x), "=r"(u.y) : "l"(b));
-      asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(w.x), "=r"(w.y) : "l"(b + 8));
-      const uint32_t sh = (k & 3u) * 8u;
-      if (k < 4) { a.x = __funnelshift_r(u.x, u.y, sh); a.y = __funnelshift_r(u.y, w.x, sh); }
-      else { a.x = __funnelshift_r(u.y, w.x, sh); a.y = __funnelshift_r(w.x, w.y, sh); }
-    }
-    x[0] = bf16_lo(a.x); x[1] = bf16_hi(a.x); x[2] = bf16_lo(a.y); x[3] = bf16_hi(a.y);
-  } else {
-    const uint4 a = load16<kAligned>(p, k);
-    x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y);
-    x[2] = __uint_as_float(a.z); x[3] = __uint_as_float(a.w);
-  }
-}
-
 struct PullOps {
   float w, inv;
   bool pow2, mean, acc, bf16r;

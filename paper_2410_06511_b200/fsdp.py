@@ -352,3 +352,36 @@ def stage_rs_copy_in(layer: Layer, grads, reduce_dtype, mean: bool, rs_in: torch
 def stage_rs_copy_out(layer: Layer, rs_out: torch.Tensor, reduce_dtype, accumulate: bool, stream=None):
     call("fsdp_stage_rs_copy_out", layer.handle, C.c_void_p(rs_out.data_ptr()), _dtype_code(reduce_dtype),
          int(bool(accumulate)), _stream(stream))
+
+
+# ----------------------------------------------------------------------- P2P stage entry points
+def unsharded_layout(layer: Layer, dtype=torch.bfloat16):
+    """(byte offset of every param in the unsharded arena, arena bytes)."""
+    offs = (C.c_int64 * max(layer.P, 1))()
+    tot = C.c_int64()
+    call("fsdp_unsharded_layout", layer.handle, _dtype_code(dtype), offs, C.byref(tot))
+    return [int(offs[p]) for p in range(layer.P)], tot.value
+
+
+def stage_unshard_push(layer: Layer, dtype, arenas: Sequence[torch.Tensor], fp8_scales: Optional[torch.Tensor] = None,
+                       stream=None):
+    sp = C.c_void_p(fp8_scales.data_ptr()) if fp8_scales is not None else C.c_void_p()
+    call("fsdp_stage_unshard_push", layer.handle, _dtype_code(dtype), sp, _ptr_array(arenas), _stream(stream))
+
+
+def grad_staging_layout(layer: Layer):
+    offs = (C.c_int64 * max(layer.P, 1))()
+    tot = C.c_int64()
+    call("fsdp_grad_staging_layout", layer.handle, offs, C.byref(tot))
+    return [int(offs[p]) for p in range(layer.P)], tot.value
+
+
+def stage_grads_to_staging(layer: Layer, grads: Sequence[torch.Tensor], staging: torch.Tensor, stream=None):
+    call("fsdp_stage_grads_to_staging", layer.handle, _ptr_array(grads), _dtype_code(grads[0].dtype),
+         C.c_void_p(staging.data_ptr()), _stream(stream))
+
+
+def stage_rs_pull(layer: Layer, stagings: Sequence[torch.Tensor], grad_dtype, reduce_dtype=torch.float32,
+                  mean: bool = True, accumulate: bool = False, stream=None):
+    call("fsdp_stage_rs_pull", layer.handle, _ptr_array(stagings), _dtype_code(grad_dtype),
+         _dtype_code(reduce_dtype), int(bool(mean)), int(bool(accumulate)), _stream(stream))

@@ -7,6 +7,6 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_ncu_list.log 2>&1
 echo "launch list rc=$?"
 $B --serial > gpurun_out/${TAG}_plain_serial.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k "regex:k_copy_in_bf16|k_copy_out|k_rs_copy_in" -s 3 -c 3 \
+ncu --set full --clock-control none --import-source on -k "regex:k_copy_in_bf16|k_unshard_push|k_copy_out|k_rs_copy_in" -s 3 -c 3 \
     -o gpurun_out/${TAG}_prof $B --serial > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "ncu full rc=$?"

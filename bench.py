@@ -308,25 +308,43 @@ def run_e2e(args, F, torch, dist, mesh, layers, grads, comp, dev, N, W, pdtype, 
     h2d = sum(sum(g.numel() for g in gs) * 2 for gs in grads)
     d2h = sum(4 * l.S for l in layers)
 
+    h2d_s = torch.cuda.Stream(device=dev)   # PCIe host->device (copy engine)
+    d2h_s = torch.cuda.Stream(device=dev)   # PCIe device->host, other direction, overlaps
+    n = len(layers)
+
     def step():
+        start = torch.cuda.Event()
+        start.record(comp)
+        h2d_s.wait_event(start)
+        ev_in = []
+        with torch.cuda.stream(h2d_s):
+            for i in range(n):           # this step's input: every unit's full grads, H2D
+                off = 0
+                for g in grads[i]:
+                    g.view(-1).copy_(h_in[off:off + g.numel()], non_blocking=True)
+                    off += g.numel()
+                e = torch.cuda.Event()
+                e.record(h2d_s)
+                ev_in.append(e)
         if wl["fp8"]:
             F.precompute_fp8_scales(mesh, layers, stream=comp)
-        n = len(layers)
         with torch.cuda.stream(comp):
             F.fsdp_unshard(layers[0], pdtype, stream=comp)
             for i in range(n):
-                off = 0
-                for g in grads[i]:       # this step's input: the unit's full grads, H2D
-                    g.view(-1).copy_(h_in[off:off + g.numel()], non_blocking=True)
-                    off += g.numel()
                 F.fsdp_wait_unshard(layers[i], stream=comp)
                 if i + 1 < n:
                     F.fsdp_unshard(layers[i + 1], pdtype, stream=comp)
                 F.fsdp_reshard(layers[i], stream=comp)
+                comp.wait_event(ev_in[i])
                 F.reduce_scatter_grads(layers[i], grads[i], stream=comp)
-            for l in layers:             # the step's result: every sharded grad, D2H
-                F.fsdp_wait_reduce_scatter(l, stream=comp)
-                h_out[:l.S].copy_(l.sharded_grad_flat(), non_blocking=True)
+                # the step's result: the unit's sharded fp32 grad, D2H as soon as it is reduced
+                F.fsdp_wait_reduce_scatter(layers[i], stream=d2h_s)
+                with torch.cuda.stream(d2h_s):
+                    h_out[:layers[i].S].copy_(layers[i].sharded_grad_flat(), non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(d2h_s)
+        comp.wait_event(done)
+        comp.wait_stream(h2d_s)
 
     step()
     comp.synchronize()

@@ -76,8 +76,8 @@ def test_rs_pull_emulated(kind, seed, W, gd, rd, mean, acc):
         torch.cuda.synchronize()
         for q in (0, W - 1):   # staging holds the full grads at the published offsets
             for p, g in enumerate(GT[q]):
-                np.testing.assert_array_equal(stag[q][offs[p]:offs[p] + g.numel()].cpu().numpy().view(np.uint8),
-                                              g.reshape(-1).cpu().numpy().view(np.uint8))
+                np.testing.assert_array_equal(stag[q][offs[p]:offs[p] + g.numel()].view(torch.uint8).cpu().numpy(),
+                                              g.reshape(-1).view(torch.uint8).cpu().numpy())
         rng = np.random.default_rng(seed)
         old = [rng.standard_normal(l.S).astype(np.float32) for l in emu.layers]
         for r, l in enumerate(emu.layers):

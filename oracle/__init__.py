@@ -28,10 +28,10 @@ reduce-scatter of non-dyadic data only the error bound is pinned (DESIGN.md §3 
 from .layout import ParamMeta, UnitLayout, unit_layout, round_up, ALIGN_ELEMS, ALIGN_BYTES
 from .casts import (bf16_rne_bits, bf16_bits_to_f32, e4m3_table, e4m3_decode,
                     e4m3_encode, E4M3_MAX, fp8_scale_from_amax, AMAX_EPS)
-from .world import World
+from .world import World, HsdpWorld
 
 __all__ = [
     "ParamMeta", "UnitLayout", "unit_layout", "round_up", "ALIGN_ELEMS", "ALIGN_BYTES",
     "bf16_rne_bits", "bf16_bits_to_f32", "e4m3_table", "e4m3_decode", "e4m3_encode",
-    "E4M3_MAX", "fp8_scale_from_amax", "AMAX_EPS", "World",
+    "E4M3_MAX", "fp8_scale_from_amax", "AMAX_EPS", "World", "HsdpWorld",
 ]

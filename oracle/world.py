@@ -127,15 +127,18 @@ class World:
 
     # ------------------------------------------------------------ a7: RS copy-in
     def rs_copy_in(self, grads: Sequence[np.ndarray], grad_dtype: str = BF16,
-                   mean: bool = True, reduce_dtype: str = FP32) -> np.ndarray:
+                   mean: bool = True, reduce_dtype: str = FP32, divisor: int | None = None) -> np.ndarray:
         """One rank's reduce-scatter input [W][S]: row-chunk r of every full grad, widened to
         fp32 and divided once by W, zero padding elsewhere (reading R1).
-        reduce_dtype bf16 (reading R11) rounds the pre-divided fp32 value to bf16."""
+        reduce_dtype bf16 (reading R11) rounds the pre-divided fp32 value to bf16.
+        `divisor` (default W) is the number of ranks the mean runs over: the whole
+        replicate x shard mesh under HSDP (reading R15)."""
         lay = self.layouts[0]
         buf = np.zeros(self.W * lay.S, dtype=np.float32)
+        div = np.float32(self.W if divisor is None else divisor)
         for p, g in enumerate(grads):
             g32 = bf16_bits_to_f32(g).reshape(-1) if grad_dtype == BF16 else np.asarray(g, np.float32).reshape(-1)
-            x = (g32 / np.float32(self.W)).astype(np.float32) if mean else g32
+            x = (g32 / div).astype(np.float32) if mean else g32
             for r in range(self.W):
                 m = self.layouts[r].params[p]
                 n = m.row_count * m.rest
@@ -214,3 +217,46 @@ def rs_error_ok(y: np.ndarray, exact: np.ndarray, mag: np.ndarray, W: int,
     nrm = float(np.linalg.norm(e))
     nrel = float(np.linalg.norm(y - e) / nrm) if nrm > 0 else float(np.linalg.norm(y - e))
     return (ratio <= 1.0 and nrel <= rel), ratio, nrel
+
+
+class HsdpWorld:
+    """HSDP (appendix:hsdp): a 2-D mesh of `replicate` replica groups x
+    `shard` ranks; global rank g = replica * shard + shard_rank (replica dim outer, reading
+    R15).  "each shard group runs FSDP and the replica group runs normal data parallel
+    ... with the addition of backward gradient allreduce across replica groups"
+    (PAPER.md:476): parameters are Shard(0) over the shard group, unshard is the shard
+    group's all-gather, and the gradient is pre-divided by the whole world size
+    (SPEC.md:381 "HSDP adds all_reduce(mean via pre-division) across the replicate dim"),
+    reduce-scattered inside each shard group, then all-reduced (sum) across replicas."""
+
+    def __init__(self, shapes, replicate: int, shard: int, fp8_eligible=None):
+        self.R, self.Ws = int(replicate), int(shard)
+        self.W = self.R * self.Ws
+        self.fsdp = World(shapes, self.Ws, fp8_eligible)   # one shard group (all replicas identical)
+
+    def shard_rank(self, g: int) -> int:
+        return g % self.Ws
+
+    def replica(self, g: int) -> int:
+        return g // self.Ws
+
+    def reduce_scatter_grads(self, grads_per_rank, grad_dtype: str = BF16, mean: bool = True):
+        """grads_per_rank[g] = global rank g's full grads.  Returns per global rank a dict of
+        per-param sharded grads: 'order' (shard-group sum in ascending shard rank, then the
+        replica sum in ascending replica), 'exact' (correctly rounded fp32 of the exact sum
+        of all W pre-divided terms), 'mag' (sum of their magnitudes)."""
+        w = self.fsdp
+        inputs = [w.rs_copy_in(g, grad_dtype, mean, FP32, divisor=self.W) for g in grads_per_rank]
+        # reduce-scatter inside every shard group
+        per_rep = [w.reduce_scatter(inputs[r * self.Ws:(r + 1) * self.Ws]) for r in range(self.R)]
+        S = w.S
+        out = []
+        for g in range(self.W):
+            s = self.shard_rank(g)
+            acc = per_rep[0][s]["order"].copy()
+            for r in range(1, self.R):          # all-reduce across the replica group
+                acc = (acc + per_rep[r][s]["order"]).astype(np.float32)
+            X = np.stack([inputs[q][s * S:(s + 1) * S].astype(np.float64) for q in range(self.W)])
+            res = dict(order=acc, exact=_exact_sum_to_f32(X), mag=np.abs(X).sum(axis=0))
+            out.append({k: w.rs_copy_out(v, s) for k, v in res.items()})
+        return out

@@ -203,3 +203,65 @@ def test_rs_bf16_reduce_bound():
             ok, ratio, nrel = rs_error_ok(res[r]["order"][p].reshape(-1), ref[r]["exact"][p].reshape(-1),
                                           ref[r]["mag"][p].reshape(-1), W, rel=(W - 1) * 2.0 ** -8 + 2.0 ** -8)
             assert ratio <= 1.0
+
+
+# ----------------------------------------------------------------------------- HSDP (f1)
+from oracle import HsdpWorld  # noqa: E402
+
+
+def _grads(kind, shapes, W, seed):
+    gen = synth.dyadic_grad_bf16_bits if kind == "dyadic" else synth.grad_bf16_bits
+    return [[gen(seed, p, q, s) for p, s in enumerate(shapes)] for q in range(W)]
+
+
+@pytest.mark.parametrize("R,Ws", [(1, 4), (2, 2), (2, 4), (4, 2), (4, 1)])   # W = 2^k: /W exact
+def test_hsdp_rs_bruteforce_dyadic(R, Ws):
+    """Sharded grad of global rank (r, s) == sum over ALL R*Ws ranks' grads / (R*Ws),
+    chunked on dim 0 over the shard group (torch.chunk) — PAPER.md:476."""
+    shapes, elig = _unit("ragged", 11, Ws)
+    h = HsdpWorld(shapes, R, Ws, elig)
+    G = _grads("dyadic", shapes, R * Ws, 11)
+    res = h.reduce_scatter_grads(G, BF16, True)
+    for p, shape in enumerate(shapes):
+        tot = np.zeros(shape, np.float64)
+        for q in range(R * Ws):
+            tot += bf16_bits_to_f32(G[q][p]).astype(np.float64)
+        tot /= R * Ws
+        chunks = list(torch.chunk(torch.from_numpy(tot), Ws, dim=0)) if shape[0] else []
+        for g in range(R * Ws):
+            s = g % Ws
+            want = chunks[s].numpy() if s < len(chunks) else np.zeros((0,) + shape[1:])
+            np.testing.assert_array_equal(res[g]["order"][p], want.astype(np.float32))
+            np.testing.assert_array_equal(res[g]["exact"][p], want.astype(np.float32))
+
+
+def test_hsdp_degenerate_and_spec_cross_config():
+    """R=1 is plain FSDP; "HSDP (replicate 2 x shard 2) equals FSDP 4": the
+    gathered gradient of HSDP(2x2) equals FSDP(4)'s (dyadic data: exact for any order)."""
+    shapes, elig = _unit("toy")
+    G4 = _grads("normal", shapes, 4, 0)
+    a = HsdpWorld(shapes, 1, 4, elig).reduce_scatter_grads(G4, BF16, True)
+    b = World(shapes, 4, elig).reduce_scatter_grads(G4, BF16, True)
+    for r in range(4):
+        for p in range(len(shapes)):
+            np.testing.assert_array_equal(a[r]["order"][p], b[r]["order"][p])
+    G = _grads("dyadic", shapes, 4, 1)
+    h = HsdpWorld(shapes, 2, 2, elig).reduce_scatter_grads(G, BF16, True)
+    f = World(shapes, 4, elig).reduce_scatter_grads(G, BF16, True)
+    for p in range(len(shapes)):
+        full_h = np.concatenate([h[s]["order"][p] for s in range(2)])
+        full_f = np.concatenate([f[r]["order"][p] for r in range(4)])
+        np.testing.assert_array_equal(full_h, full_f)
+        for s in range(2):   # replicas hold identical shards
+            np.testing.assert_array_equal(h[s]["order"][p], h[2 + s]["order"][p])
+
+
+def test_hsdp_normal_data_bound():
+    shapes, elig = _unit("ragged", 12, 4)
+    h = HsdpWorld(shapes, 2, 4, elig)
+    res = h.reduce_scatter_grads(_grads("normal", shapes, 8, 12), BF16, True)
+    for g in range(8):
+        for p in range(len(shapes)):
+            ok, ratio, _ = rs_error_ok(res[g]["order"][p].reshape(-1), res[g]["exact"][p].reshape(-1),
+                                       res[g]["mag"][p].reshape(-1), 8)
+            assert ratio <= 1.0

@@ -162,6 +162,22 @@ fsdp_status_t fsdp_mesh_init(const uint8_t id[FSDP_UNIQUE_ID_BYTES], int32_t wor
 fsdp_status_t fsdp_mesh_init_local(int32_t world_size, int32_t rank, int32_t cuda_device,
                                    fsdp_mesh_t** out);
 
+/* HSDP (hybrid sharded data parallel, P:472-478 appendix:hsdp): a 2-D mesh of world_size =
+ * replicate_size x shard_size ranks, replica dimension outer: rank g is shard rank
+ * g % shard_size of replica g / shard_size (R15).  Parameters are Shard(0) over
+ * the shard group (every layout call uses shard_size as W and the shard rank as rank);
+ * fsdp_unshard all-gathers within the shard group; fsdp_reduce_scatter_grads divides by
+ * world_size (mean over all ranks), reduce-scatters within the shard group
+ * and all-reduces (sum, fp32, NCCL) across the replica group ("the addition of backward
+ * gradient allreduce across replica groups").  Collective over all world_size
+ * ranks; shard_size must divide world_size; shard_size == world_size is plain FSDP. */
+fsdp_status_t fsdp_mesh_init_hsdp(const uint8_t id[FSDP_UNIQUE_ID_BYTES], int32_t world_size,
+                                  int32_t rank, int32_t shard_size, int32_t cuda_device,
+                                  fsdp_mesh_t** out);
+/* replicate_size and this rank's replica index (1 and 0 for a 1-D mesh). */
+fsdp_status_t fsdp_mesh_info_hsdp(const fsdp_mesh_t* mesh, int32_t* replicate_size,
+                                  int32_t* replica_index);
+
 /* Destroys the mesh (synchronizes its streams, frees its pools, destroys the comms).
  * All layers of the mesh must have been destroyed. */
 fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* mesh);

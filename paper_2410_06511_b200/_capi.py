@@ -57,6 +57,8 @@ SIGNATURES = {
     "fsdp_get_unique_id": [C.POINTER(C.c_uint8)],
     "fsdp_mesh_init": [C.POINTER(C.c_uint8), _I32, _I32, _I32, C.POINTER(_VP)],
     "fsdp_mesh_init_local": [_I32, _I32, _I32, C.POINTER(_VP)],
+    "fsdp_mesh_init_hsdp": [C.POINTER(C.c_uint8), _I32, _I32, _I32, _I32, C.POINTER(_VP)],
+    "fsdp_mesh_info_hsdp": [_VP, C.POINTER(_I32), C.POINTER(_I32)],
     "fsdp_mesh_destroy": [_VP],
     "fsdp_mesh_info": [_VP, C.POINTER(_I32), C.POINTER(_I32), C.POINTER(_I32)],
     "fsdp_mesh_synchronize": [_VP, _I64],

@@ -174,9 +174,11 @@ enum LayerState { SHARDED = 0, UNSHARDING = 1, UNSHARDED = 2 };
 struct fsdp_layer;
 
 struct fsdp_mesh {
-  int W = 1, rank = 0, device = 0;
+  int W = 1, rank = 0, device = 0;   // shard group size / shard rank
+  int R = 1, rep = 0;                // HSDP replicate group size / replica index
   bool local = true;
   ncclComm_t comm_ag = nullptr, comm_rs = nullptr;
+  ncclComm_t comm_world = nullptr, comm_rep = nullptr;   // HSDP only
   cudaStream_t s_cin = nullptr, s_ag = nullptr, s_cout = nullptr, s_rsc = nullptr, s_rs = nullptr;
   fsdpk::LaunchCfg cfg{};
   std::vector<Slot*> ag_slots, rs_slots;
@@ -520,7 +522,8 @@ void launch_rs_copy_in_all(fsdp_layer* l, const void* const* grads, bool grad_bf
                            bool mean, cudaStream_t st) {
   fsdpk::PtrArray pa{};
   for (int p = 0; p < l->P; ++p) pa.p[p] = grads[p];
-  CUDA_CHECK(fsdpk::launch_rs_copy_in(l->t_rsin.d, l->t_rsin.n, pa, grad_bf16, rs_in, out_bf16, mean, l->mesh->W,
+  CUDA_CHECK(fsdpk::launch_rs_copy_in(l->t_rsin.d, l->t_rsin.n, pa, grad_bf16, rs_in, out_bf16, mean,
+                                      l->mesh->W * l->mesh->R,
                                       l->mesh->cfg, st));
 }
 
@@ -622,19 +625,23 @@ static void p2p_init(fsdp_mesh* m) {
 }
 
 static fsdp_status_t mesh_init_impl(const uint8_t* id, int32_t W, int32_t rank, int32_t dev, bool local,
-                                    fsdp_mesh_t** out) {
+                                    fsdp_mesh_t** out, int32_t shard_size = 0) {
   return guarded([&] {
     if (!out) fail(FSDP_ERR_INVALID_ARGUMENT, "out is NULL");
     *out = nullptr;
     if (W < 1 || rank < 0 || rank >= W) fail(FSDP_ERR_INVALID_ARGUMENT, "invalid world_size/rank");
     if (!local && !id) fail(FSDP_ERR_INVALID_ARGUMENT, "unique id is NULL");
+    if (shard_size <= 0) shard_size = W;
+    if (W % shard_size != 0) fail(FSDP_ERR_INVALID_ARGUMENT, "shard_size must divide world_size");
     int ndev = 0;
     CUDA_CHECK(cudaGetDeviceCount(&ndev));
     if (dev < 0 || dev >= ndev) fail(FSDP_ERR_INVALID_ARGUMENT, "cuda_device out of range");
     DeviceGuard g(dev);
     auto* m = new fsdp_mesh();
-    m->W = W;
-    m->rank = rank;
+    m->W = shard_size;              // the Shard(0) degree
+    m->rank = rank % shard_size;    // shard rank (replica dimension outer, R15)
+    m->R = W / shard_size;
+    m->rep = rank / shard_size;
     m->device = dev;
     m->local = local;
     try {
@@ -642,8 +649,14 @@ static fsdp_status_t mesh_init_impl(const uint8_t* id, int32_t W, int32_t rank, 
       if (!local) {
         ncclUniqueId u;
         std::memcpy(&u, id, sizeof(u));
-        NCCL_CHECK(ncclCommInitRank(&m->comm_ag, W, u, rank));
-        NCCL_CHECK(ncclCommSplit(m->comm_ag, 0, rank, &m->comm_rs, nullptr));
+        if (m->R == 1) {
+          NCCL_CHECK(ncclCommInitRank(&m->comm_ag, W, u, rank));
+        } else {   // HSDP: world comm -> shard group (color = replica) and replica group (color = shard rank)
+          NCCL_CHECK(ncclCommInitRank(&m->comm_world, W, u, rank));
+          NCCL_CHECK(ncclCommSplit(m->comm_world, m->rep, m->rank, &m->comm_ag, nullptr));
+          NCCL_CHECK(ncclCommSplit(m->comm_world, m->rank, m->rep, &m->comm_rep, nullptr));
+        }
+        NCCL_CHECK(ncclCommSplit(m->comm_ag, 0, m->rank, &m->comm_rs, nullptr));
         p2p_init(m);
       }
     } catch (...) {
@@ -661,6 +674,23 @@ fsdp_status_t fsdp_mesh_init(const uint8_t id[FSDP_UNIQUE_ID_BYTES], int32_t wor
 
 fsdp_status_t fsdp_mesh_init_local(int32_t world_size, int32_t rank, int32_t cuda_device, fsdp_mesh_t** out) {
   return mesh_init_impl(nullptr, world_size, rank, cuda_device, true, out);
+}
+
+fsdp_status_t fsdp_mesh_init_hsdp(const uint8_t id[FSDP_UNIQUE_ID_BYTES], int32_t world_size, int32_t rank,
+                                  int32_t shard_size, int32_t cuda_device, fsdp_mesh_t** out) {
+  if (shard_size < 1) {
+    g_last_error = "shard_size must be >= 1";
+    return FSDP_ERR_INVALID_ARGUMENT;
+  }
+  return mesh_init_impl(id, world_size, rank, cuda_device, false, out, shard_size);
+}
+
+fsdp_status_t fsdp_mesh_info_hsdp(const fsdp_mesh_t* m, int32_t* R, int32_t* rep) {
+  return guarded([&] {
+    if (!m) fail(FSDP_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    if (R) *R = m->R;
+    if (rep) *rep = m->rep;
+  });
 }
 
 fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
@@ -683,6 +713,8 @@ fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
     if (m->ev_pre_done) cudaEventDestroy(m->ev_pre_done);
     if (m->comm_rs) { if (m->aborted) ncclCommAbort(m->comm_rs); else ncclCommDestroy(m->comm_rs); }
     if (m->comm_ag) { if (m->aborted) ncclCommAbort(m->comm_ag); else ncclCommDestroy(m->comm_ag); }
+    for (ncclComm_t c : {m->comm_rep, m->comm_world})
+      if (c) { if (m->aborted) ncclCommAbort(c); else ncclCommDestroy(c); }
     for (cudaStream_t s : {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs})
       if (s) cudaStreamDestroy(s);
     delete m;
@@ -1169,15 +1201,31 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
     const bool obf = rd == FSDP_BFLOAT16;
     const int64_t osz = obf ? 2 : 4;
     const int64_t S = l->L.S;
+    const bool hsdp = m->R > 1;            // + all-reduce across the replica group
+    const int divisor = m->W * m->R;       // mean over every rank of the mesh
+    // HSDP with accumulation: the shard-group result goes to a temp T, is all-reduced across
+    // replicas, then added to the grad (the all-reduce must not see the old grad)
+    const bool via_temp = hsdp && accumulate;
+    cudaStream_t cs = as_stream(compute);
+    auto replica_all_reduce = [&](float* buf) {
+      ProfScope pa(m, FSDP_PROF_ALL_REDUCE, m->s_rs, (int64_t)2 * (m->R - 1) * S * 4 / m->R);
+      NCCL_CHECK(ncclAllReduce(buf, buf, (size_t)S, ncclFloat32, ncclSum, m->comm_rep, m->s_rs));
+      pa.done();
+    };
+    auto add_temp_into_grad = [&](const float* T) {
+      ProfScope po(m, FSDP_PROF_RS_COPY_OUT, m->s_rs, S * 12);
+      CUDA_CHECK(fsdpk::launch_rs_copy_out(T, false, l->grad, true, S, m->cfg, m->s_rs));
+      po.done();
+    };
     if (m->algo == FSDP_ALGO_P2P) {
       // fused path: stage the caller's grads into this rank's symmetric staging -> ready
-      // handshake -> pull (every rank's rows of this rank, /W, ascending-rank fp32 sum,
+      // handshake -> pull (every rank's rows of this rank, /divisor, ascending-rank fp32 sum,
       // written into the grad buffer) -> done handshake (staging reusable)
       const int64_t gsz = dtype_size(gd);
       const int prefer = (int)(m->rs_rr++ % 2);   // deterministic round robin: copy of i+1 overlaps pull of i
       SymSlot* ss = acquire_sym_slot(m, m->p2p_rs, (size_t)(l->stg_elems * gsz), prefer);
+      Slot* tmp = via_temp ? acquire_slot(m, m->rs_slots, 0, (size_t)(S * 4), 1) : nullptr;
       const uint64_t epoch = ++ss->epoch;
-      cudaStream_t cs = as_stream(compute);
       CUDA_CHECK(cudaEventRecord(l->ev_rcall, cs));
       CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, l->ev_rcall, 0));
       if (ss->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, ss->free_ev, 0));
@@ -1191,6 +1239,12 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       }
       CUDA_CHECK(cudaEventRecord(l->ev_k5, m->s_rsc));
       CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, l->ev_k5, 0));
+      float* target = l->grad;
+      if (via_temp) {
+        if (tmp->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, tmp->free_ev, 0));
+        target = (float*)tmp->b.p;
+        CUDA_CHECK(cudaMemsetAsync(target, 0, sizeof(float) * S, m->s_rs));   // padding stays 0
+      }
       {
         ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_rs, 0);
         CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_READY, ss->index), flag_local(m, FK_RS_READY, ss->index),
@@ -1199,8 +1253,8 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       }
       {
         ProfScope pp(m, FSDP_PROF_RS_PULL, m->s_rs, (int64_t)(m->W - 1) * l->pull_elems * gsz);
-        CUDA_CHECK(fsdpp::launch_rs_pull(l->t_pull.d, l->t_pull.n, peer_ptrs(m, ss->buf), gd == FSDP_BFLOAT16, l->grad,
-                                         mean != 0, accumulate != 0, obf, m->W, m->cfg, m->s_rs));
+        CUDA_CHECK(fsdpp::launch_rs_pull(l->t_pull.d, l->t_pull.n, peer_ptrs(m, ss->buf), gd == FSDP_BFLOAT16, divisor,
+                                         target, mean != 0, accumulate != 0 && !hsdp, obf, m->W, m->cfg, m->s_rs));
         pp.done();
       }
       {
@@ -1209,20 +1263,27 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
                                              m->W, m->rank, epoch, m->s_rs));
         ph.done();
       }
-      CUDA_CHECK(cudaEventRecord(l->ev_rs_done, m->s_rs));
       CUDA_CHECK(cudaEventRecord(ss->free_ev, m->s_rs));
       ss->ever_used = true;
       ss->in_use = false;
+      if (hsdp) {
+        replica_all_reduce(target);
+        if (via_temp) {
+          add_temp_into_grad(target);
+          release_slot(tmp, m->s_rs);
+        }
+      }
+      CUDA_CHECK(cudaEventRecord(l->ev_rs_done, m->s_rs));
       l->rs_pending = true;
       return;
     }
-    // fp32, no accumulation: the reduce-scatter (or, at W=1, K5 itself) writes straight
-    // into the layer's grad buffer — the zero-copy "view" copy-out
+    // NCCL path.  fp32 without accumulation: the reduce-scatter (or, at W=1, K5 itself)
+    // writes straight into the layer's grad buffer — the zero-copy "view" copy-out
     const bool direct = !obf && !accumulate;
     const bool need_in = comm_ready(m) || !direct;
+    const size_t stage_b = (comm_ready(m) && !direct) ? (size_t)(S * osz) : 0;
     Slot* slot = acquire_slot(m, m->rs_slots, need_in ? (size_t)(m->W * S * osz) : 0,
-                              (comm_ready(m) && !direct) ? (size_t)(S * osz) : 0, 2);
-    cudaStream_t cs = as_stream(compute);
+                              via_temp ? std::max(stage_b, (size_t)(S * 4)) : stage_b, 2);
     CUDA_CHECK(cudaEventRecord(l->ev_rcall, cs));
     CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, l->ev_rcall, 0));
     if (slot->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, slot->free_ev, 0));
@@ -1244,10 +1305,24 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       pr.done();
       rs_out = out;
     }
-    if (!direct) {
-      ProfScope po(m, FSDP_PROF_RS_COPY_OUT, m->s_rs, S * (osz + 4 + (accumulate ? 4 : 0)));
-      CUDA_CHECK(fsdpk::launch_rs_copy_out(rs_out, obf, l->grad, accumulate != 0, S, m->cfg, m->s_rs));
-      po.done();
+    if (via_temp) {
+      // widen / copy the shard-group result into T (in place when it already is fp32 in
+      // the staging buffer), all-reduce T across replicas, add T into the grad
+      float* T = (float*)slot->b.p;
+      if (rs_out != (const void*)T || obf) {
+        ProfScope po(m, FSDP_PROF_RS_COPY_OUT, m->s_rs, S * (osz + 4));
+        CUDA_CHECK(fsdpk::launch_rs_copy_out(rs_out, obf, T, false, S, m->cfg, m->s_rs));
+        po.done();
+      }
+      replica_all_reduce(T);
+      add_temp_into_grad(T);
+    } else {
+      if (!direct) {
+        ProfScope po(m, FSDP_PROF_RS_COPY_OUT, m->s_rs, S * (osz + 4 + (accumulate ? 4 : 0)));
+        CUDA_CHECK(fsdpk::launch_rs_copy_out(rs_out, obf, l->grad, accumulate != 0, S, m->cfg, m->s_rs));
+        po.done();
+      }
+      if (hsdp) replica_all_reduce(l->grad);
     }
     CUDA_CHECK(cudaEventRecord(l->ev_rs_done, m->s_rs));
     release_slot(slot, m->s_rs);
@@ -1464,7 +1539,7 @@ fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* l, const void* const* stagings, f
     }
     DeviceGuard g(m->device);
     ProfScope ps(m, FSDP_PROF_RS_PULL, as_stream(stream), (int64_t)(m->W - 1) * l->pull_elems * dtype_size(gd));
-    CUDA_CHECK(fsdpp::launch_rs_pull(l->t_pull.d, l->t_pull.n, pp, gd == FSDP_BFLOAT16, l->grad, mean != 0,
+    CUDA_CHECK(fsdpp::launch_rs_pull(l->t_pull.d, l->t_pull.n, pp, gd == FSDP_BFLOAT16, m->W * m->R, l->grad, mean != 0,
                                      accumulate != 0, rd == FSDP_BFLOAT16, m->W, m->cfg, as_stream(stream)));
     ps.done();
   });

@@ -43,7 +43,7 @@ cudaError_t launch_unshard_push(const fsdpk::Tile* tiles, int ntiles, const floa
 
 // Pull tiles: src = element offset into every rank's staging, dst = element offset into the
 // fp32 grad, n elements.  grad[dst+e] (+)= round?( sum_{q=0..W-1} (fp32(stage_q[src+e]) / W) ).
-cudaError_t launch_rs_pull(const fsdpk::Tile* tiles, int ntiles, PeerPtrs staging, bool grad_bf16,
+cudaError_t launch_rs_pull(const fsdpk::Tile* tiles, int ntiles, PeerPtrs staging, bool grad_bf16, int divisor,
                            float* grad, bool mean, bool accumulate, bool bf16_reduce, int W,
                            fsdpk::LaunchCfg cfg, cudaStream_t st);
 

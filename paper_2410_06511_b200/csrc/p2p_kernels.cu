@@ -286,13 +286,13 @@ cudaError_t launch_unshard_push(const Tile* tiles, int ntiles, const float* shar
   return cudaGetLastError();
 }
 
-cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool grad_bf16, float* grad, bool mean,
+cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool grad_bf16, int divisor, float* grad, bool mean,
                            bool accumulate, bool bf16_reduce, int W, fsdpk::LaunchCfg cfg, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
   PullOps ops;
-  ops.w = (float)W;
-  ops.inv = 1.0f / (float)W;
-  ops.pow2 = (W & (W - 1)) == 0;
+  ops.w = (float)divisor;
+  ops.inv = 1.0f / (float)divisor;
+  ops.pow2 = (divisor & (divisor - 1)) == 0;
   ops.mean = mean;
   ops.acc = accumulate;
   ops.bf16r = bf16_reduce;

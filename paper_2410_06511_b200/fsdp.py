@@ -106,7 +106,9 @@ class Mesh:
     """1-D data-parallel mesh (fsdp_mesh_t).  world_size defaults to all ranks."""
 
     def __init__(self, world_size: int, rank: int, device: int, unique_id: Optional[bytes] = None,
-                 local: bool = False):
+                 local: bool = False, shard_size: Optional[int] = None):
+        """world_size ranks; shard_size < world_size makes an HSDP mesh of world_size //
+        shard_size replica groups x shard_size ranks."""
         self.world_size, self.rank, self.device = int(world_size), int(rank), int(device)
         self.local = local
         h = C.c_void_p()
@@ -116,14 +118,25 @@ class Mesh:
             if unique_id is None or len(unique_id) != capi.FSDP_UNIQUE_ID_BYTES:
                 raise ValueError("unique_id of 128 bytes required")
             idb = (C.c_uint8 * capi.FSDP_UNIQUE_ID_BYTES).from_buffer_copy(unique_id)
-            call("fsdp_mesh_init", idb, self.world_size, self.rank, self.device, C.byref(h))
+            if shard_size is not None and shard_size != world_size:
+                call("fsdp_mesh_init_hsdp", idb, self.world_size, self.rank, int(shard_size), self.device, C.byref(h))
+            else:
+                call("fsdp_mesh_init", idb, self.world_size, self.rank, self.device, C.byref(h))
         self.handle = h
         self.layers: List["Layer"] = []
+        R = C.c_int32()
+        rep = C.c_int32()
+        call("fsdp_mesh_info_hsdp", h, C.byref(R), C.byref(rep))
+        self.replicate_size, self.replica = R.value, rep.value
+        self.shard_size = self.world_size // self.replicate_size
+        self.shard_rank = self.rank % self.shard_size
 
     @classmethod
-    def from_process_group(cls, group=None, device: Optional[int] = None) -> "Mesh":
+    def from_process_group(cls, group=None, device: Optional[int] = None,
+                           shard_size: Optional[int] = None) -> "Mesh":
         """Collective: rank 0 creates the NCCL unique id, torch.distributed broadcasts it
-        (the binding's only torch.distributed use), every rank initialises the mesh."""
+        (the binding's only torch.distributed use), every rank initialises the mesh.
+        shard_size (data_parallel_shard_degree) defaults to all ranks."""
         import torch.distributed as dist
         if device is None:
             device = torch.cuda.current_device()
@@ -131,7 +144,7 @@ class Mesh:
         r = dist.get_rank(group)
         obj = [get_unique_id() if r == 0 else None]
         dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
-        return cls(W, r, device, unique_id=obj[0])
+        return cls(W, r, device, unique_id=obj[0], shard_size=shard_size)
 
     @property
     def algo(self) -> str:

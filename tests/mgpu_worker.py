@@ -44,9 +44,60 @@ def main():
         run_checks(mesh, W, rank, local, algo)
     mesh.synchronize(120000)
     mesh.destroy()
+    for Ws in sorted({d for d in (1, 2, W // 2) if 1 <= d < W and W % d == 0}):
+        run_hsdp_checks(W, rank, local, Ws)
     dist.barrier()
     dist.destroy_process_group()
-    print(f"RANK {rank}/{W} OK (algos {algos})", flush=True)
+    print(f"RANK {rank}/{W} OK (algos {algos}, hsdp)", flush=True)
+
+
+def run_hsdp_checks(W, rank, local, Ws):
+    """HSDP: R = W / Ws replica groups of Ws ranks; vs oracle HsdpWorld."""
+    from oracle import HsdpWorld
+    R = W // Ws
+    mesh = F.Mesh.from_process_group(device=local, shard_size=Ws)
+    assert (mesh.replicate_size, mesh.shard_size) == (R, Ws)
+    s = mesh.shard_rank
+    algos = ["p2p", "nccl"] if mesh.algo == "p2p" else ["nccl"]
+    for algo in algos:
+        mesh.set_algo(algo)
+        for ui, u in enumerate([synth.model_units("toy")[0], synth.ragged_unit(5, world_size=Ws)]):
+            shapes = [sh for _, sh, _ in u]
+            elig = [e for _, _, e in u]
+            P = [synth.param_values(ui, p, sh) for p, sh in enumerate(shapes)]
+            h = HsdpWorld(shapes, R, Ws, elig)
+            w = h.fsdp
+            layer = F.fsdp_shard(mesh, [torch.from_numpy(p) for p in P], elig)
+            np.testing.assert_array_equal(layer.sharded_flat().cpu().numpy(), w.shard(P)[s])
+            outs = F.all_gather_params(layer, torch.bfloat16)   # within the shard group
+            _, fulls = w.unshard(w.shard(P), BF16)
+            for o, want in zip(outs, fulls):
+                np.testing.assert_array_equal(u16(o), want)
+            F.fsdp_reshard(layer)
+            for kind in ("dyadic", "normal"):
+                gen = synth.dyadic_grad_bf16_bits if kind == "dyadic" else synth.grad_bf16_bits
+                G = [[gen(ui, p, q, sh) for p, sh in enumerate(shapes)] for q in range(W)]
+                gt = [torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16) for x in G[rank]]
+                ref = h.reduce_scatter_grads(G, BF16, True)[rank]
+                for acc in (False, True):
+                    before = layer.sharded_grad_flat().clone()
+                    F.reduce_scatter_grads(layer, gt, accumulate=acc)
+                    F.fsdp_wait_reduce_scatter(layer)
+                    for p in range(len(shapes)):
+                        got = layer.sharded_grad(p).cpu().numpy()
+                        m = layer.metas[p]
+                        prev = before[m["elem_offset"]:m["elem_offset"] + got.size].cpu().numpy().reshape(got.shape)
+                        if kind == "dyadic":
+                            want = (prev + ref["exact"][p]).astype(np.float32) if acc else ref["exact"][p]
+                            np.testing.assert_array_equal(got, want)
+                        elif not acc:
+                            ok, ratio, nrel = rs_error_ok(got.reshape(-1), ref["exact"][p].reshape(-1),
+                                                          ref["mag"][p].reshape(-1), W)
+                            assert ok, (algo, Ws, ui, p, ratio, nrel)
+            layer.destroy()
+        print(f"rank {rank}/{W} hsdp {R}x{Ws} algo={algo}: OK", flush=True)
+    mesh.synchronize(120000)
+    mesh.destroy()
 
 
 def run_checks(mesh, W, rank, local, algo):

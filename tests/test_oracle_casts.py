@@ -130,3 +130,32 @@ def test_nan_outside_domain():
         bf16_rne_bits(np.array([np.nan], np.float32))
     with pytest.raises(ValueError):
         e4m3_encode(np.array([np.nan], np.float32))
+
+
+# ----------------------------------------------------------------------------- delayed scaling (f4)
+def test_delayed_scaling_worked_example():
+    from oracle.scaling import DelayedScaling
+    ex = json.load(open(os.path.join(GOLDEN, "fp8_delayed_scaling.json")))
+    d = DelayedScaling(1, ex["history_len"])
+    got = [float(d.step(np.array([a], np.float32), [True])[0]) for a in ex["amax"]]
+    assert got == ex["scale"]
+
+
+def test_delayed_scaling_properties():
+    from oracle.scaling import DelayedScaling
+    rng = np.random.default_rng(0)
+    # constant amax -> constant scale equal to the dynamic one
+    d = DelayedScaling(2, 16)
+    for _ in range(20):
+        s = d.step(np.array([3.0, 0.7], np.float32), [True, True])
+        np.testing.assert_array_equal(s, fp8_scale_from_amax(np.array([3.0, 0.7], np.float32)))
+    # history length 1: the scale lags the amax by exactly one step
+    d = DelayedScaling(1, 1)
+    a = rng.uniform(0.1, 10, 30).astype(np.float32)
+    s = [d.step(a[i:i + 1], [True])[0] for i in range(30)]
+    assert s[0] == fp8_scale_from_amax(a[0])
+    for i in range(1, 30):
+        assert s[i] == fp8_scale_from_amax(a[i - 1])
+    # non-eligible params get no scale
+    d = DelayedScaling(2, 4)
+    assert d.step(np.array([1.0, 1.0], np.float32), [True, False])[1] == 0.0

@@ -233,6 +233,14 @@ fsdp_status_t fsdp_sharded_flat(const fsdp_layer_t* layer, float** dev);
  * and leaves s_p = 0 for that param. */
 fsdp_status_t fsdp_precompute_fp8_scales(fsdp_mesh_t* mesh, fsdp_layer_t* const* layers,
                                          int32_t n_layers, void* stream);
+/* Delayed scaling ("dynamic, delayed, and static"): the same amax
+ * pass and all-reduce(max), then per eligible param s_p = fp32(448 / fp64(max(H_p, 1e-12)))
+ * where H_p is the max of the param's amax history (the last history_len amaxes,
+ * initialised with the first observed amax), and the current amax is pushed into the
+ * history after use.  history_len in [1, 64], fixed by the first call.  Static scaling =
+ * passing caller scales to fsdp_unshard. */
+fsdp_status_t fsdp_precompute_fp8_scales_delayed(fsdp_mesh_t* mesh, fsdp_layer_t* const* layers,
+                                                 int32_t n_layers, int32_t history_len, void* stream);
 /* Device arrays of P floats (entries of non-eligible params are 0). */
 fsdp_status_t fsdp_fp8_scales(const fsdp_layer_t* layer, const float** scales_dev,
                               const float** amax_dev);

@@ -73,6 +73,7 @@ SIGNATURES = {
     "fsdp_sharded_param": [_VP, _I32, C.POINTER(_VP)],
     "fsdp_sharded_flat": [_VP, C.POINTER(_VP)],
     "fsdp_precompute_fp8_scales": [_VP, _PP, _I32, _VP],
+    "fsdp_precompute_fp8_scales_delayed": [_VP, _PP, _I32, _I32, _VP],
     "fsdp_fp8_scales": [_VP, C.POINTER(_VP), C.POINTER(_VP)],
     "fsdp_unshard": [_VP, _I32, _VP, _VP],
     "fsdp_wait_unshard": [_VP, _VP],

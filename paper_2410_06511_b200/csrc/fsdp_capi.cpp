@@ -165,6 +165,7 @@ struct SymSlot {
 };
 
 constexpr int kFlagSlots = 64;   // max symmetric slots per kind
+constexpr int kHistMax = 64;     // max delayed-scaling amax history length
 enum FlagKind { FK_AG_READY = 0, FK_AG_DONE = 1, FK_RS_READY = 2, FK_RS_DONE = 3, FK_NUM = 4 };
 
 enum LayerState { SHARDED = 0, UNSHARDING = 1, UNSHARDED = 2 };
@@ -189,6 +190,10 @@ struct fsdp_mesh {
   float* reg_amax = nullptr;
   float* reg_scale = nullptr;
   uint8_t* reg_elig = nullptr;
+  float* reg_hist = nullptr;      // delayed scaling: [reg_cap][kHistMax] amax history
+  int32_t* reg_pos = nullptr;
+  uint8_t* reg_hinit = nullptr;
+  int hist_len = 0;               // fixed at the first delayed precompute
   int* d_err = nullptr;
   cudaEvent_t ev_pre_call = nullptr, ev_pre_done = nullptr;
   std::vector<fsdp_layer*> layers;
@@ -372,8 +377,25 @@ void ensure_registry(fsdp_mesh* m, int need) {
     CUDA_CHECK(cudaMemcpy(scale, m->reg_scale, sizeof(float) * m->reg_size, cudaMemcpyDeviceToDevice));
     CUDA_CHECK(cudaMemcpy(elig, m->reg_elig, m->reg_size, cudaMemcpyDeviceToDevice));
   }
+  // delayed-scaling state: amax history [cap][kHistMax], ring position, initialised flag
+  float* hist;
+  int32_t* pos;
+  uint8_t* hinit;
+  CUDA_CHECK(cudaMalloc(&hist, sizeof(float) * (size_t)cap * kHistMax));
+  CUDA_CHECK(cudaMalloc(&pos, sizeof(int32_t) * cap));
+  CUDA_CHECK(cudaMalloc(&hinit, cap));
+  CUDA_CHECK(cudaMemset(hist, 0, sizeof(float) * (size_t)cap * kHistMax));
+  CUDA_CHECK(cudaMemset(pos, 0, sizeof(int32_t) * cap));
+  CUDA_CHECK(cudaMemset(hinit, 0, cap));
+  if (m->reg_size) {
+    CUDA_CHECK(cudaMemcpy(hist, m->reg_hist, sizeof(float) * (size_t)m->reg_size * kHistMax, cudaMemcpyDeviceToDevice));
+    CUDA_CHECK(cudaMemcpy(pos, m->reg_pos, sizeof(int32_t) * m->reg_size, cudaMemcpyDeviceToDevice));
+    CUDA_CHECK(cudaMemcpy(hinit, m->reg_hinit, m->reg_size, cudaMemcpyDeviceToDevice));
+  }
   cudaFree(m->reg_acc); cudaFree(m->reg_amax); cudaFree(m->reg_scale); cudaFree(m->reg_elig);
+  cudaFree(m->reg_hist); cudaFree(m->reg_pos); cudaFree(m->reg_hinit);
   m->reg_acc = acc; m->reg_amax = amax; m->reg_scale = scale; m->reg_elig = elig;
+  m->reg_hist = hist; m->reg_pos = pos; m->reg_hinit = hinit;
   m->reg_cap = cap;
   for (auto* ps : m->presets) { ps->tiles.release(); cudaFree(ps->idx); delete ps; }
   m->presets.clear();
@@ -707,6 +729,7 @@ fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
     for (auto& r : m->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : m->ev_pool) cudaEventDestroy(e);
     cudaFree(m->reg_acc); cudaFree(m->reg_amax); cudaFree(m->reg_scale); cudaFree(m->reg_elig);
+    cudaFree(m->reg_hist); cudaFree(m->reg_pos); cudaFree(m->reg_hinit);
     cudaFree(m->d_err);
     cudaFree(m->d_barrier);
     if (m->ev_pre_call) cudaEventDestroy(m->ev_pre_call);
@@ -957,9 +980,14 @@ fsdp_status_t fsdp_sharded_flat(const fsdp_layer_t* l, float** dev) {
 }
 
 // ------------------------------------------------------------------------- fp8 scales
-fsdp_status_t fsdp_precompute_fp8_scales(fsdp_mesh_t* m, fsdp_layer_t* const* layers, int32_t n, void* stream) {
+// history_len == 0: dynamic scaling; > 0: delayed scaling with that amax history length.
+static fsdp_status_t precompute_impl(fsdp_mesh_t* m, fsdp_layer_t* const* layers, int32_t n, void* stream,
+                                     int32_t history_len) {
   return guarded([&] {
     check_mesh(m);
+    if (history_len < 0 || history_len > kHistMax) fail(FSDP_ERR_INVALID_ARGUMENT, "history_len must be in [1, 64]");
+    if (history_len > 0 && m->hist_len > 0 && history_len != m->hist_len)
+      fail(FSDP_ERR_INVALID_ARGUMENT, "the amax history length is fixed at the first delayed precompute");
     if (n < 0 || (n > 0 && !layers)) fail(FSDP_ERR_INVALID_ARGUMENT, "layers is NULL");
     for (int i = 0; i < n; ++i) {
       if (!layers[i] || layers[i]->mesh != m) fail(FSDP_ERR_INVALID_ARGUMENT, "layer does not belong to this mesh");
@@ -1007,13 +1035,33 @@ fsdp_status_t fsdp_precompute_fp8_scales(fsdp_mesh_t* m, fsdp_layer_t* const* la
     }
     {
       ProfScope pk(m, FSDP_PROF_SCALE, m->s_rs, (int64_t)ps->nidx * 12);
-      CUDA_CHECK(fsdpk::launch_fp8_scale(ps->idx, ps->nidx, m->reg_acc, m->reg_amax, m->reg_scale, m->reg_elig,
-                                         m->d_err, true, m->s_rs));
+      if (history_len == 0) {
+        CUDA_CHECK(fsdpk::launch_fp8_scale(ps->idx, ps->nidx, m->reg_acc, m->reg_amax, m->reg_scale, m->reg_elig,
+                                           m->d_err, true, m->s_rs));
+      } else {
+        m->hist_len = history_len;
+        CUDA_CHECK(fsdpk::launch_fp8_scale_delayed(ps->idx, ps->nidx, m->reg_acc, m->reg_amax, m->reg_scale,
+                                                   m->reg_elig, m->reg_hist, m->reg_pos, m->reg_hinit, history_len,
+                                                   kHistMax, m->d_err, m->s_rs));
+      }
       pk.done();
     }
     CUDA_CHECK(cudaEventRecord(m->ev_pre_done, m->s_rs));
     CUDA_CHECK(cudaStreamWaitEvent(st, m->ev_pre_done, 0));
   });
+}
+
+fsdp_status_t fsdp_precompute_fp8_scales(fsdp_mesh_t* m, fsdp_layer_t* const* layers, int32_t n, void* stream) {
+  return precompute_impl(m, layers, n, stream, 0);
+}
+
+fsdp_status_t fsdp_precompute_fp8_scales_delayed(fsdp_mesh_t* m, fsdp_layer_t* const* layers, int32_t n,
+                                                 int32_t history_len, void* stream) {
+  if (history_len < 1) {
+    g_last_error = "history_len must be >= 1";
+    return FSDP_ERR_INVALID_ARGUMENT;
+  }
+  return precompute_impl(m, layers, n, stream, history_len);
 }
 
 fsdp_status_t fsdp_fp8_scales(const fsdp_layer_t* l, const float** scales_dev, const float** amax_dev) {

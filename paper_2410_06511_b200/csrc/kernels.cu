@@ -287,6 +287,32 @@ __global__ void k_fp8_scale(const int32_t* __restrict__ idx, int n, uint32_t* __
   if (reset) acc[j] = 0u;
 }
 
+__global__ void k_fp8_scale_delayed(const int32_t* __restrict__ idx, int n, uint32_t* __restrict__ acc,
+                                    float* __restrict__ amax_out, float* __restrict__ scale_out,
+                                    const uint8_t* __restrict__ eligible, float* __restrict__ hist,
+                                    int32_t* __restrict__ pos, uint8_t* __restrict__ init, int H, int hmax,
+                                    int* __restrict__ err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int j = idx[i];
+  const float a = __uint_as_float(acc[j]);
+  amax_out[j] = a;
+  acc[j] = 0u;
+  if (!eligible[j]) { scale_out[j] = 0.0f; return; }
+  if (!isfinite(a)) { atomicExch(err, 1); scale_out[j] = 0.0f; return; }
+  float* h = hist + (size_t)j * hmax;
+  if (!init[j]) {                       // history initialised with the first observed amax
+    for (int k = 0; k < H; ++k) h[k] = a;
+    pos[j] = 0;
+    init[j] = 1;
+  }
+  float m = h[0];
+  for (int k = 1; k < H; ++k) m = fmaxf(m, h[k]);   // max of the history ...
+  scale_out[j] = __double2float_rn(__ddiv_rn(448.0, (double)fmaxf(m, 1e-12f)));
+  h[pos[j]] = a;                                       // ... updated after use
+  pos[j] = pos[j] + 1 == H ? 0 : pos[j] + 1;
+}
+
 inline int grid_for(int64_t work_items, LaunchCfg cfg) {
   int64_t g = work_items;
   if (g > cfg.grid_cap) g = cfg.grid_cap;
@@ -363,4 +389,15 @@ cudaError_t launch_fp8_scale(const int32_t* idx, int n, uint32_t* acc_bits, floa
   return cudaGetLastError();
 }
 
+}  // namespace fsdpk
+
+namespace fsdpk {
+cudaError_t launch_fp8_scale_delayed(const int32_t* idx, int n, uint32_t* acc_bits, float* amax_out, float* scale_out,
+                                     const uint8_t* eligible, float* hist, int32_t* pos, uint8_t* hist_init, int H,
+                                     int hmax, int* err_flag, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_fp8_scale_delayed<<<(n + 127) / 128, 128, 0, st>>>(idx, n, acc_bits, amax_out, scale_out, eligible, hist, pos,
+                                                         hist_init, H, hmax, err_flag);
+  return cudaGetLastError();
+}
 }  // namespace fsdpk

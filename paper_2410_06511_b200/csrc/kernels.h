@@ -59,5 +59,12 @@ cudaError_t launch_amax(const Tile* tiles, int ntiles, uint32_t* acc_bits, Launc
 cudaError_t launch_fp8_scale(const int32_t* idx, int n, uint32_t* acc_bits, float* amax_out,
                              float* scale_out, const uint8_t* eligible, int* err_flag,
                              bool reset_acc, cudaStream_t st);
+// K1b delayed scaling: for every idx j with eligible[j]: if the history
+// hist[j*hmax .. +H) is not initialised, fill it with a = acc[j]; scale[j] = fp32(448 /
+// fp64(max(max(hist), 1e-12))); then hist[pos[j]] = a, pos[j] = (pos[j]+1) % H ("updated
+// after use").  amax_out[j] = a; acc[j] = 0.
+cudaError_t launch_fp8_scale_delayed(const int32_t* idx, int n, uint32_t* acc_bits, float* amax_out,
+                                     float* scale_out, const uint8_t* eligible, float* hist, int32_t* pos,
+                                     uint8_t* hist_init, int H, int hmax, int* err_flag, cudaStream_t st);
 
 }  // namespace fsdpk

@@ -288,9 +288,14 @@ def fsdp_shard(mesh: Mesh, params, fp8_eligible: Optional[Sequence[bool]] = None
     return layer
 
 
-def precompute_fp8_scales(mesh: Mesh, layers: Sequence[Layer], stream=None):
+def precompute_fp8_scales(mesh: Mesh, layers: Sequence[Layer], stream=None, history_len: int = 0):
+    """Per-tensor fp8 scales of every eligible param of `layers`: dynamic
+    scaling by default, delayed scaling over an amax history when history_len > 0."""
     arr = (C.c_void_p * max(len(layers), 1))(*[l.handle.value for l in layers])
-    call("fsdp_precompute_fp8_scales", mesh.handle, arr, len(layers), _stream(stream))
+    if history_len > 0:
+        call("fsdp_precompute_fp8_scales_delayed", mesh.handle, arr, len(layers), int(history_len), _stream(stream))
+    else:
+        call("fsdp_precompute_fp8_scales", mesh.handle, arr, len(layers), _stream(stream))
 
 
 def fsdp_unshard(layer: Layer, dtype=torch.bfloat16, fp8_scales: Optional[torch.Tensor] = None, stream=None):

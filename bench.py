@@ -53,6 +53,13 @@ def parse():
     ap.add_argument("--serial", action="store_true", help="no prefetch: each unit isolated")
     ap.add_argument("--algo", default="auto", choices=["auto", "nccl", "p2p"],
                     help="collectives: fused NVLink peer-memory kernels (p2p) or NCCL; auto = library default")
+    ap.add_argument("--step", default="unit", choices=["unit", "train"],
+                    help="unit: every FSDP unit once through unshard -> reshard -> reduce-scatter; "
+                         "train: the paper's training-step pattern (forward unshards with prefetch, the last "
+                         "block kept unsharded, backward re-unshards in reverse + reduce-scatter, P:424-431)")
+    ap.add_argument("--zero2", action="store_true",
+                    help="with --step train: reshard_after_forward=False for every block (ZeRO-2, P:636)")
+    ap.add_argument("--shard-size", type=int, default=0, help="HSDP: data_parallel_shard_degree (default all ranks)")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     return ap.parse_args()
 
@@ -133,7 +140,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if N > 1:
         dist.init_process_group("nccl", device_id=dev)
-        mesh = F.Mesh.from_process_group(device=local)
+        mesh = F.Mesh.from_process_group(device=local, shard_size=args.shard_size or None)
     else:
         mesh = F.Mesh(1, 0, local, unique_id=F.get_unique_id())
     if args.algo != "auto" and N > 1:
@@ -160,11 +167,9 @@ def run_ours(args):
         grads.append([(torch.randn(s, generator=gen, device=dev) * 1e-3).to(torch.bfloat16) for s in shapes])
     torch.cuda.synchronize()
     comp = torch.cuda.Stream(device=dev)
-    W = N
+    W = mesh.shard_size if N > 1 else 1     # Shard(0) degree (HSDP: shard group size)
 
-    def step():
-        if wl["fp8"]:
-            F.precompute_fp8_scales(mesh, layers, stream=comp)
+    def step_unit():
         n = len(layers)
         if not args.serial:
             F.fsdp_unshard(layers[0], pdtype, stream=comp)
@@ -181,9 +186,54 @@ def run_ours(args):
         for l in layers:
             F.fsdp_wait_reduce_scatter(l, stream=comp)
 
-    # algorithmic bytes per step per rank
+    # --step train: root (last unit) wraps the blocks; forward unshards root then
+    # every block with the next prefetched, reshards each block after use except the last
+    # — or none under ZeRO-2 — and keeps the root unsharded through the
+    # forward; backward re-unshards what was resharded in reverse order (prefetching the
+    # previous block), reduce-scatters each block's grads and finally the root's.
+    blocks, root = layers[:-1], layers[-1]
+    kept = set(range(len(blocks))) if args.zero2 else {len(blocks) - 1}
+
+    def step_train():
+        F.fsdp_unshard(root, pdtype, stream=comp)
+        F.fsdp_wait_unshard(root, stream=comp)
+        F.fsdp_unshard(blocks[0], pdtype, stream=comp)
+        for i, b in enumerate(blocks):                      # forward
+            F.fsdp_wait_unshard(b, stream=comp)
+            if i + 1 < len(blocks):
+                F.fsdp_unshard(blocks[i + 1], pdtype, stream=comp)
+            if i not in kept:
+                F.fsdp_reshard(b, stream=comp)
+        F.fsdp_reshard(root, stream=comp)
+        F.fsdp_unshard(root, pdtype, stream=comp)            # backward: output layer first
+        F.fsdp_wait_unshard(root, stream=comp)
+        order = list(range(len(blocks)))[::-1]
+        if order[0] not in kept:
+            F.fsdp_unshard(blocks[order[0]], pdtype, stream=comp)
+        for j, i in enumerate(order):
+            b = blocks[i]
+            F.fsdp_wait_unshard(b, stream=comp)
+            if j + 1 < len(order) and order[j + 1] not in kept:
+                F.fsdp_unshard(blocks[order[j + 1]], pdtype, stream=comp)   # backward prefetch
+            F.fsdp_reshard(b, stream=comp)
+            F.reduce_scatter_grads(b, grads[i], stream=comp)
+        F.fsdp_reshard(root, stream=comp)
+        F.reduce_scatter_grads(root, grads[-1], stream=comp)
+        for l in layers:
+            F.fsdp_wait_reduce_scatter(l, stream=comp)
+
+    def step():
+        if wl["fp8"]:
+            F.precompute_fp8_scales(mesh, layers, stream=comp)
+        (step_train if args.step == "train" else step_unit)()
+
+    # algorithmic bytes per step per rank: all-gather outputs + fp32 RS inputs
     slot_b = [(l.S_bytes_fp8 if wl["fp8"] else 2 * l.S) for l in layers]
-    bytes_rank = sum(W * sb + 4 * W * l.S for sb, l in zip(slot_b, layers))
+    if args.step == "train":
+        n_unshard = [2 if (i not in kept) else 1 for i in range(len(blocks))] + [2]
+    else:
+        n_unshard = [1] * len(layers)
+    bytes_rank = sum(k * W * sb + 4 * W * l.S for k, sb, l in zip(n_unshard, slot_b, layers))
 
     def barrier():
         if N > 1:
@@ -259,7 +309,8 @@ def run_ours(args):
     # ---- e2e through the public API with host buffers (pinned), copies inside the timing
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, F, torch, dist, mesh, layers, grads, comp, dev, N, W, pdtype, wl, bytes_rank,
+        bytes_unit = sum(W * sb + 4 * W * l.S for sb, l in zip(slot_b, layers))   # e2e runs the unit step
+        e2e = run_e2e(args, F, torch, dist, mesh, layers, grads, comp, dev, N, W, pdtype, wl, bytes_unit,
                       barrier)
 
     line = None
@@ -276,7 +327,8 @@ def run_ours(args):
                                    f"({'32 blocks + root' if args.workload.startswith('llama3.1-8b') else 'see DESIGN.md'}), "
                                    f"{'fp8 e4m3' if wl['fp8'] else 'bf16'} all-gather / fp32 reduce-scatter, "
                                    f"{'serial' if args.serial else 'prefetch next unit'}",
-                       "world_size": W, "units": len(layers), "collectives": algo,
+                       "world_size": N, "shard_size": W, "units": len(layers), "collectives": algo,
+                       "step": args.step + (" zero2" if args.zero2 else ""),
                        "l2": "inputs larger than L2 (every unit's shard/grads/buffers are 100s of MB; 126 MB L2)",
                        "bytes_per_step_per_rank": bytes_rank},
             "per_rank": {"algbw_GBps": round(algbw_rank, 2), "busbw_GBps": round(busbw_rank, 2),

@@ -273,6 +273,27 @@ def run_ours(args):
     value = N * bytes_rank / (ms_max * 1e-3) / 1e9
     algbw_rank = bytes_rank / (ms_max * 1e-3) / 1e9
     busbw_rank = algbw_rank * (W - 1) / W
+    prof_step = prof
+
+    # ---- roofline pass: the same step with every unit issued serially (no prefetch), so
+    # no two of our kernels overlap and each kernel's event-timed duration is its own
+    # (in the prefetch step the unshard of unit i+1 and the reduce-scatter of unit i share
+    # HBM / NVLink, which inflates both durations while the step as a whole runs faster)
+    roof_steps = max(2, min(args.steps, 4))
+    serial_saved = args.serial
+    args.serial = args.step == "unit"
+    step()
+    comp.synchronize()
+    barrier()
+    mesh.profile_enable(True)
+    mesh.profile_read(reset=True)
+    for _ in range(roof_steps):
+        step()
+    comp.synchronize()
+    prof = mesh.profile_read(reset=True)
+    mesh.profile_enable(False)
+    args.serial = serial_saved
+    barrier()
 
     # ---- roofline of the dominant kernel (largest total device time among ours).
     # HBM-bound kernels are measured against the measured HBM copy peak; the fused P2P
@@ -291,12 +312,17 @@ def run_ours(args):
         bound, peak, peak_src = "nvlink", 770.0, "measured peer copy per direction (B200_PROFILING.md; 900 nominal)"
     else:
         bound = "hbm"
-    kernels = {}
-    for k in ours + ["all_gather", "reduce_scatter", "all_reduce"]:
-        if prof[k]["launches"]:
-            kernels[k] = {"launches": prof[k]["launches"], "avg_us": round(prof[k]["ms"] / prof[k]["launches"] * 1e3, 2),
-                          "GBps": round(prof[k]["bytes"] / (prof[k]["ms"] * 1e-3) / 1e9, 1) if prof[k]["ms"] and prof[k]["bytes"] else None,
-                          "share_of_step": round(prof[k]["ms"] / args.steps / ms_max, 4)}
+    def ktable(pr, nsteps, step_ms):
+        out = {}
+        for k in ours + ["all_gather", "reduce_scatter", "all_reduce"]:
+            if pr[k]["launches"]:
+                out[k] = {"launches": pr[k]["launches"], "avg_us": round(pr[k]["ms"] / pr[k]["launches"] * 1e3, 2),
+                          "GBps": round(pr[k]["bytes"] / (pr[k]["ms"] * 1e-3) / 1e9, 1) if pr[k]["ms"] and pr[k]["bytes"] else None,
+                          "share_of_step": round(pr[k]["ms"] / nsteps / step_ms, 4) if step_ms else None}
+        return out
+
+    kernels = ktable(prof_step, args.steps, ms_max)            # in the timed (prefetch) step
+    kernels_serial = ktable(prof, roof_steps, None)           # roofline pass
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
@@ -304,7 +330,10 @@ def run_ours(args):
             traffic = json.load(open(tfile)).get(f"{args.workload}/w{N}", {}).get(dom)
         except Exception:
             traffic = None
-    gpu_launches = sum(prof[k]["launches"] for k in ours)
+    gpu_launches = sum(prof_step[k]["launches"] for k in ours)
+    # whole-step HBM efficiency of our kernels in the timed step (sum of their algorithmic
+    # HBM bytes / step time), meaningful where no NVLink kernel runs (W = 1)
+    step_hbm = sum(prof_step[k]["bytes"] for k in hbm_k) / args.steps / (ms_max * 1e-3) / 1e9
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the timing
     e2e = None
@@ -334,9 +363,12 @@ def run_ours(args):
             "per_rank": {"algbw_GBps": round(algbw_rank, 2), "busbw_GBps": round(busbw_rank, 2),
                          "busbw_frac_nvlink_900": round(busbw_rank / NVLINK_GBS, 4)},
             "kernels": kernels,
+            "kernels_serial": kernels_serial,
             "roofline": {"bound": bound, "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
-                         "bytes_per_launch": int(per_launch_bytes), "traffic": traffic},
+                         "bytes_per_launch": int(per_launch_bytes), "traffic": traffic,
+                         "pass": f"serial issue, {roof_steps} steps after the timed region (CUDA events on the launching streams)",
+                         "step_hbm_GBps": round(step_hbm, 1), "step_hbm_frac": round(step_hbm / measured_peaks()[0], 4)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,
         }
     for l in layers:

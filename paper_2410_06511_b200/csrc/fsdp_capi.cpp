@@ -625,9 +625,11 @@ static void mesh_common_init(fsdp_mesh* m) {
   int sms = 0;
   CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device));
   // persistent grids: CTAs per SM (256 threads each); FSDP_B200_CTAS_PER_SM tunes it
-  int per_sm = 4;
+  int per_sm = 0;   // 0: each kernel's tuned value (kernels.h)
   if (const char* e = std::getenv("FSDP_B200_CTAS_PER_SM")) per_sm = std::max(1, std::min(16, std::atoi(e)));
-  m->cfg.grid_cap = sms * per_sm;
+  m->cfg.sms = sms;
+  m->cfg.per_sm = per_sm;
+  m->cfg.grid_cap = sms * (per_sm > 0 ? per_sm : 4);
   CUDA_CHECK(cudaMalloc(&m->d_err, sizeof(int)));
   CUDA_CHECK(cudaMemset(m->d_err, 0, sizeof(int)));
   m->ev_pre_call = new_event();

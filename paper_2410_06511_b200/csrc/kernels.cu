@@ -313,9 +313,9 @@ __global__ void k_fp8_scale_delayed(const int32_t* __restrict__ idx, int n, uint
   pos[j] = pos[j] + 1 == H ? 0 : pos[j] + 1;
 }
 
-inline int grid_for(int64_t work_items, LaunchCfg cfg) {
+inline int grid_for(int64_t work_items, LaunchCfg cfg, int tuned = kCtasCopy) {
   int64_t g = work_items;
-  if (g > cfg.grid_cap) g = cfg.grid_cap;
+  if (g > cfg.cap(tuned)) g = cfg.cap(tuned);
   if (g < 1) g = 1;
   return (int)g;
 }
@@ -353,7 +353,7 @@ cudaError_t launch_rs_copy_in(const Tile* tiles, int ntiles, const PtrArray& gra
   div.pow2 = (world_size & (world_size - 1)) == 0;
   div.inv = 1.0f / (float)world_size;
   div.mean = mean;
-  const int g = grid_for(ntiles, cfg);
+  const int g = grid_for(ntiles, cfg, kCtasRsCopyIn);
   uint8_t* d = (uint8_t*)rs_in;
   if (grad_bf16 && !out_bf16) k_rs_copy_in<true, false><<<g, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
   else if (grad_bf16 && out_bf16) k_rs_copy_in<true, true><<<g, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);

@@ -29,8 +29,17 @@ constexpr uint32_t kTileElems = 16384;   // K3/K5/K1 tile size in elements
 constexpr uint32_t kTileBytes = 65536;   // K4 tile size in bytes
 
 struct LaunchCfg {
-  int grid_cap;   // max CTAs (SMs * resident CTAs per SM)
+  int grid_cap;     // max CTAs when the kernel has no tuned value (SMs * 4)
+  int sms = 148;    // multiprocessor count
+  int per_sm = 0;   // > 0: FSDP_B200_CTAS_PER_SM override for every kernel
+  // persistent grid of a kernel whose measured best is `tuned` CTAs per SM
+  int cap(int tuned) const { return sms * (per_sm > 0 ? per_sm : tuned); }
 };
+
+// CTAs per SM (256 threads each) measured best on B200 (profiles/r02, 8B layout)
+constexpr int kCtasRsCopyIn = 2;
+constexpr int kCtasPush = 6;
+constexpr int kCtasCopy = 4;
 
 // K2: slot[i] = bf16_rne(shard[i]) for i < S (S % 16 == 0, both 16B aligned).
 cudaError_t launch_copy_in_bf16(const float* shard, void* slot, int64_t S, LaunchCfg cfg,

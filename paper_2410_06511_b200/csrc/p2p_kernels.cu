@@ -249,8 +249,9 @@ __global__ void __launch_bounds__(kThreads) k_gather_copy(const Tile* __restrict
   }
 }
 
-inline int grid_for(int64_t items, fsdpk::LaunchCfg cfg) {
-  int64_t g = items < cfg.grid_cap ? items : cfg.grid_cap;
+inline int grid_for(int64_t items, fsdpk::LaunchCfg cfg, int tuned = fsdpk::kCtasCopy) {
+  const int64_t cap = cfg.cap(tuned);
+  int64_t g = items < cap ? items : cap;
   return (int)(g < 1 ? 1 : g);
 }
 
@@ -282,7 +283,8 @@ cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W
 cudaError_t launch_unshard_push(const Tile* tiles, int ntiles, const float* shard, const float* scales,
                                 PeerPtrs arena, int W, int rank, fsdpk::LaunchCfg cfg, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
-  k_unshard_push<<<grid_for(ntiles, cfg), kThreads, 0, st>>>(tiles, ntiles, shard, scales, arena, W, rank);
+  k_unshard_push<<<grid_for(ntiles, cfg, fsdpk::kCtasPush), kThreads, 0, st>>>(tiles, ntiles, shard, scales, arena,
+                                                                               W, rank);
   return cudaGetLastError();
 }
 

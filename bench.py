@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--zero2", action="store_true",
                     help="with --step train: reshard_after_forward=False for every block (ZeRO-2, P:636)")
     ap.add_argument("--shard-size", type=int, default=0, help="HSDP: data_parallel_shard_degree (default all ranks)")
+    ap.add_argument("--grads", default="auto", choices=["auto", "torch", "library"],
+                    help="where the full grads live: torch tensors (the RS stages them), or the layer's "
+                         "own symmetric grad buffers (zero-copy; auto = library under P2P)")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     return ap.parse_args()
 
@@ -155,6 +158,7 @@ def run_ours(args):
     # ---- setup: shard (synthetic seeded params written straight into the shards)
     layers, grads = [], []
     gen = torch.Generator(device=dev).manual_seed(241006511 + rank)
+    lib_grads = args.grads == "library" or (args.grads == "auto" and N > 1 and mesh.algo == "p2p")
     for ui, (shapes, elig) in enumerate(units):
         l = F.fsdp_shard(mesh, None, elig, shapes=shapes)
         flat = l.sharded_flat()
@@ -164,7 +168,13 @@ def run_ours(args):
             if n:
                 flat[m["elem_offset"]:m["elem_offset"] + n].normal_(0.0, 0.02, generator=gen)
         layers.append(l)
-        grads.append([(torch.randn(s, generator=gen, device=dev) * 1e-3).to(torch.bfloat16) for s in shapes])
+        g = [(torch.randn(s, generator=gen, device=dev) * 1e-3).to(torch.bfloat16) for s in shapes]
+        if lib_grads:   # the backward would write its grads straight into the layer's buffer
+            bufs = l.full_grad_buffers(torch.bfloat16)
+            for b, x in zip(bufs, g):
+                b.copy_(x)
+            g = bufs
+        grads.append(g)
     torch.cuda.synchronize()
     comp = torch.cuda.Stream(device=dev)
     W = mesh.shard_size if N > 1 else 1     # Shard(0) degree (HSDP: shard group size)
@@ -358,6 +368,7 @@ def run_ours(args):
                                    f"{'serial' if args.serial else 'prefetch next unit'}",
                        "world_size": N, "shard_size": W, "units": len(layers), "collectives": algo,
                        "step": args.step + (" zero2" if args.zero2 else ""),
+                       "grads": "layer symmetric grad buffers (zero-copy RS)" if lib_grads else "torch tensors (RS stages them)",
                        "l2": "inputs larger than L2 (every unit's shard/grads/buffers are 100s of MB; 126 MB L2)",
                        "bytes_per_step_per_rank": bytes_rank},
             "per_rank": {"algbw_GBps": round(algbw_rank, 2), "busbw_GBps": round(busbw_rank, 2),

@@ -282,6 +282,16 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* layer, const void* const* 
                                         fsdp_dtype_t grad_dtype, fsdp_dtype_t reduce_dtype,
                                         int32_t mean, int32_t accumulate, void* compute);
 fsdp_status_t fsdp_wait_reduce_scatter(fsdp_layer_t* layer, void* compute);
+/* Zero-copy gradients: the layer's own full-gradient buffer (all params, grad_dtype, each
+ * param contiguous with its desc shape at a 256-byte aligned offset); *dev = param p's
+ * tensor.  The buffer is allocated by the first call — symmetric (mapped into every peer)
+ * when the mesh can run FSDP_ALGO_P2P, which makes that first call collective, and so is
+ * fsdp_layer_destroy of a layer that has one.  When every full_grads[p] given to
+ * fsdp_reduce_scatter_grads is this buffer's tensor (on all ranks alike), the P2P path
+ * skips the staging copy and peers read the gradients in place.  Valid until destroy;
+ * writable again after fsdp_wait_reduce_scatter.  FSDP_ERR_DTYPE if a later call asks
+ * for another grad_dtype. */
+fsdp_status_t fsdp_full_grad_buffer(fsdp_layer_t* layer, fsdp_dtype_t grad_dtype, int32_t p, void** dev);
 /* fp32 sharded grad of param p: (*dev)[0 .. row_count*rest) (views into the layer's
  * grad buffer, same flat layout as the shard). */
 fsdp_status_t fsdp_sharded_grad(const fsdp_layer_t* layer, int32_t p, float** dev);

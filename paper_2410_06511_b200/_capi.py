@@ -82,6 +82,7 @@ SIGNATURES = {
     "fsdp_reshard": [_VP, _VP],
     "fsdp_reduce_scatter_grads": [_VP, _PP, _I32, _I32, _I32, _I32, _VP],
     "fsdp_wait_reduce_scatter": [_VP, _VP],
+    "fsdp_full_grad_buffer": [_VP, _I32, _I32, C.POINTER(_VP)],
     "fsdp_sharded_grad": [_VP, _I32, C.POINTER(_VP)],
     "fsdp_sharded_grad_flat": [_VP, C.POINTER(_VP)],
     "fsdp_zero_grad": [_VP, _VP],

@@ -164,7 +164,8 @@ struct SymSlot {
   int index = 0;
 };
 
-constexpr int kFlagSlots = 64;   // max symmetric slots per kind
+constexpr int kFlagSlots = 512;  // flag slots per kind: pooled slots first, then layer grad buffers
+constexpr int kPoolSlots = 64;   // max pooled symmetric slots (arenas / staging) per pool
 constexpr int kHistMax = 64;     // max delayed-scaling amax history length
 enum FlagKind { FK_AG_READY = 0, FK_AG_DONE = 1, FK_RS_READY = 2, FK_RS_DONE = 3, FK_NUM = 4 };
 
@@ -218,6 +219,7 @@ struct fsdp_mesh {
   SymBuf flags;                              // uint64 [FK_NUM][kFlagSlots][kMaxRanks]
   std::vector<SymSlot*> p2p_ag, p2p_rs;      // unsharded arenas, grad staging
   uint64_t rs_rr = 0;                        // round robin over staging slots
+  int gbuf_seq = 0;                          // flag slots of layer grad buffers: kPoolSlots + seq
   int* d_barrier = nullptr;
 };
 
@@ -248,6 +250,9 @@ struct fsdp_layer {
   int64_t push_bytes_bf16 = 0, push_bytes_fp8 = 0, pull_elems = 0;
   int64_t local_push_bf16 = 0, local_push_fp8 = 0;
   SymSlot* p2p_slot = nullptr;       // arena of the current P2P unshard
+  SymSlot* gbuf = nullptr;           // zero-copy full-grad buffer (fsdp_full_grad_buffer)
+  bool gbuf_sym = false;
+  fsdp_dtype_t gbuf_dtype = FSDP_BFLOAT16;
   void* arena_base = nullptr;        // base of the unsharded tensors (either path)
 };
 
@@ -483,7 +488,7 @@ unsigned long long* flag_local(fsdp_mesh* m, int kind, int slot) {
 // depends only on the call sequence); grows / creates slots collectively.
 SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t bytes, int prefer = -1) {
   SymSlot* s = nullptr;
-  while (prefer >= (int)pool.size() && (int)pool.size() < kFlagSlots) {
+  while (prefer >= (int)pool.size() && (int)pool.size() < kPoolSlots) {
     SymSlot* n = new SymSlot();
     n->free_ev = new_event();
     n->index = (int)pool.size();
@@ -493,7 +498,7 @@ SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t byte
   for (size_t i = 0; !s && i < pool.size(); ++i)
     if (!pool[i]->in_use) s = pool[i];
   if (!s) {
-    if ((int)pool.size() >= kFlagSlots) fail(FSDP_ERR_STATE, "too many unsharded layers / pending reduce-scatters at once");
+    if ((int)pool.size() >= kPoolSlots) fail(FSDP_ERR_STATE, "too many unsharded layers / pending reduce-scatters at once");
     s = new SymSlot();
     s->free_ev = new_event();
     s->index = (int)pool.size();
@@ -940,6 +945,13 @@ fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* l) {
     l->t_cin_fp8.release(); l->t_cout_bf16.release(); l->t_cout_fp8.release(); l->t_rsin.release();
     l->t_push_bf16.release(); l->t_push_fp8.release(); l->t_pull.release(); l->t_stage_bf16.release();
     l->t_stage_fp32.release();
+    if (l->gbuf) {
+      if (l->gbuf_sym) sym_free(m, l->gbuf->buf);   // collective
+      else cudaFree(l->gbuf->buf.local);
+      if (l->gbuf->free_ev) cudaEventDestroy(l->gbuf->free_ev);
+      delete l->gbuf;
+      l->gbuf = nullptr;
+    }
     for (cudaEvent_t e : {l->ev_call, l->ev_cin, l->ev_ag, l->ev_done, l->ev_rcall, l->ev_k5, l->ev_rs_done})
       if (e) cudaEventDestroy(e);
     m->layers.erase(std::remove(m->layers.begin(), m->layers.end(), l), m->layers.end());
@@ -1272,23 +1284,36 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       // handshake -> pull (every rank's rows of this rank, /divisor, ascending-rank fp32 sum,
       // written into the grad buffer) -> done handshake (staging reusable)
       const int64_t gsz = dtype_size(gd);
-      const int prefer = (int)(m->rs_rr++ % 2);   // deterministic round robin: copy of i+1 overlaps pull of i
-      SymSlot* ss = acquire_sym_slot(m, m->p2p_rs, (size_t)(l->stg_elems * gsz), prefer);
+      // zero copy: the caller's grads already live in this layer's symmetric grad buffer
+      bool zc = l->gbuf && l->gbuf_sym && gd == l->gbuf_dtype;
+      for (int p = 0; zc && p < l->P; ++p)
+        zc = l->L.numel[p] == 0 || grads[p] == (const void*)((uint8_t*)l->gbuf->buf.local + l->stg_off_el[p] * gsz);
+      SymSlot* ss = nullptr;
+      if (zc) {
+        ss = l->gbuf;
+      } else {
+        const int prefer = (int)(m->rs_rr++ % 2);   // deterministic round robin: copy of i+1 overlaps pull of i
+        ss = acquire_sym_slot(m, m->p2p_rs, (size_t)(l->stg_elems * gsz), prefer);
+      }
       Slot* tmp = via_temp ? acquire_slot(m, m->rs_slots, 0, (size_t)(S * 4), 1) : nullptr;
       const uint64_t epoch = ++ss->epoch;
       CUDA_CHECK(cudaEventRecord(l->ev_rcall, cs));
-      CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, l->ev_rcall, 0));
-      if (ss->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, ss->free_ev, 0));
-      {
-        const DevTiles& T = gd == FSDP_BFLOAT16 ? l->t_stage_bf16 : l->t_stage_fp32;
-        fsdpk::PtrArray pa{};
-        for (int p = 0; p < l->P; ++p) pa.p[p] = grads[p];
-        ProfScope pst(m, FSDP_PROF_STAGE_GRADS, m->s_rsc, 2 * l->grad_numel_total * gsz);
-        CUDA_CHECK(fsdpp::launch_gather_copy(T.d, T.n, pa, ss->buf.local, m->cfg, m->s_rsc));
-        pst.done();
+      if (zc) {
+        CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, l->ev_rcall, 0));
+      } else {
+        CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, l->ev_rcall, 0));
+        if (ss->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, ss->free_ev, 0));
+        {
+          const DevTiles& T = gd == FSDP_BFLOAT16 ? l->t_stage_bf16 : l->t_stage_fp32;
+          fsdpk::PtrArray pa{};
+          for (int p = 0; p < l->P; ++p) pa.p[p] = grads[p];
+          ProfScope pst(m, FSDP_PROF_STAGE_GRADS, m->s_rsc, 2 * l->grad_numel_total * gsz);
+          CUDA_CHECK(fsdpp::launch_gather_copy(T.d, T.n, pa, ss->buf.local, m->cfg, m->s_rsc));
+          pst.done();
+        }
+        CUDA_CHECK(cudaEventRecord(l->ev_k5, m->s_rsc));
+        CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, l->ev_k5, 0));
       }
-      CUDA_CHECK(cudaEventRecord(l->ev_k5, m->s_rsc));
-      CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, l->ev_k5, 0));
       float* target = l->grad;
       if (via_temp) {
         if (tmp->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, tmp->free_ev, 0));
@@ -1592,6 +1617,43 @@ fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* l, const void* const* stagings, f
     CUDA_CHECK(fsdpp::launch_rs_pull(l->t_pull.d, l->t_pull.n, pp, gd == FSDP_BFLOAT16, m->W * m->R, l->grad, mean != 0,
                                      accumulate != 0, rd == FSDP_BFLOAT16, m->W, m->cfg, as_stream(stream)));
     ps.done();
+  });
+}
+
+fsdp_status_t fsdp_full_grad_buffer(fsdp_layer_t* l, fsdp_dtype_t gd, int32_t p, void** dev) {
+  return guarded([&] {
+    check_layer(l);
+    check_param(l, p);
+    if (!dev) fail(FSDP_ERR_INVALID_ARGUMENT, "dev is NULL");
+    if (gd != FSDP_BFLOAT16 && gd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "grad_dtype must be BFLOAT16 or FLOAT32");
+    fsdp_mesh* m = l->mesh;
+    const int64_t gsz = dtype_size(gd);
+    if (!l->gbuf) {
+      DeviceGuard g(m->device);
+      auto* s = new SymSlot();
+      s->free_ev = new_event();
+      const size_t bytes = (size_t)std::max<int64_t>(l->stg_elems, 128) * gsz;
+      if (m->p2p_ok) {   // collective: every rank maps every peer's buffer
+        if (kPoolSlots + m->gbuf_seq >= kFlagSlots) fail(FSDP_ERR_UNAVAILABLE, "too many layer grad buffers");
+        s->index = kPoolSlots + m->gbuf_seq++;
+        if (!sym_alloc(m, s->buf, bytes)) {
+          cudaEventDestroy(s->free_ev);
+          delete s;
+          fail(FSDP_ERR_OUT_OF_MEMORY, "symmetric grad buffer allocation/mapping failed");
+        }
+        l->gbuf_sym = true;
+      } else {
+        CUDA_CHECK(cudaMalloc(&s->buf.local, bytes + 256));
+        CUDA_CHECK(cudaMemset(s->buf.local, 0, bytes + 256));
+        s->buf.bytes = bytes;
+        l->gbuf_sym = false;
+      }
+      l->gbuf = s;
+      l->gbuf_dtype = gd;
+    } else if (gd != l->gbuf_dtype) {
+      fail(FSDP_ERR_DTYPE, "the layer's grad buffer was created with another grad_dtype");
+    }
+    *dev = (uint8_t*)l->gbuf->buf.local + l->stg_off_el[p] * gsz;
   });
 }
 

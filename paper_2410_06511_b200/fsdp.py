@@ -236,6 +236,17 @@ class Layer:
     def unsharded_params(self) -> List[torch.Tensor]:
         return [self.unsharded_param(p) for p in range(self.P)]
 
+    def full_grad_buffers(self, dtype=torch.bfloat16) -> List[torch.Tensor]:
+        """Zero-copy gradients: views of the layer's own (symmetric, under P2P) full-grad
+        buffer, one tensor per param with its full shape.  Writing the backward's grads
+        here lets reduce_scatter_grads skip its staging copy (collective on first call)."""
+        out = []
+        for p in range(self.P):
+            ptr = C.c_void_p()
+            call("fsdp_full_grad_buffer", self.handle, _dtype_code(dtype), p, C.byref(ptr))
+            out.append(_view(ptr.value, self.shapes[p], dtype, self.device))
+        return out
+
     def fp8_scales(self):
         s = C.c_void_p()
         a = C.c_void_p()

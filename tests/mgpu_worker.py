@@ -176,6 +176,16 @@ def run_checks(mesh, W, rank, local, algo):
             assert np.all(np.abs(got.astype(np.float64) - ex) <= bound), (ui, p)
             if np.linalg.norm(ex) > 0:
                 assert np.linalg.norm(got - ex) / np.linalg.norm(ex) <= 1e-2
+        # zero-copy grads: written into the layer's own (symmetric) grad buffer, reduced in place
+        G = [[synth.dyadic_grad_bf16_bits(ui + 50, p, q, sh) for p, sh in enumerate(shapes)] for q in range(W)]
+        bufs = layer.full_grad_buffers(torch.bfloat16)
+        for b, x in zip(bufs, G[rank]):
+            b.copy_(torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16).reshape(b.shape))
+        F.reduce_scatter_grads(layer, bufs)
+        F.fsdp_wait_reduce_scatter(layer)
+        ref = w.reduce_scatter_grads(G, BF16, True)[rank]
+        for p in range(len(shapes)):
+            np.testing.assert_array_equal(layer.sharded_grad(p).cpu().numpy(), ref["exact"][p])
         layer.destroy()
         checks += 1
 

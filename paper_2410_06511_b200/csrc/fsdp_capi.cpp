@@ -634,6 +634,7 @@ static void mesh_common_init(fsdp_mesh* m) {
   if (const char* e = std::getenv("FSDP_B200_CTAS_PER_SM")) per_sm = std::max(1, std::min(16, std::atoi(e)));
   m->cfg.sms = sms;
   m->cfg.per_sm = per_sm;
+  if (const char* e = std::getenv("FSDP_B200_VARIANT")) m->cfg.variant = std::atoi(e);
   m->cfg.grid_cap = sms * (per_sm > 0 ? per_sm : 4);
   CUDA_CHECK(cudaMalloc(&m->d_err, sizeof(int)));
   CUDA_CHECK(cudaMemset(m->d_err, 0, sizeof(int)));

@@ -202,7 +202,78 @@ __device__ __forceinline__ void pull_body(const PeerPtrs& st, uint64_t sb, float
   }
 }
 
-template <int W, bool kGradBf16>
+// 8 elements per thread per vector: one 16-byte load per source (bf16) — half the NVLink
+// read requests of the 4-element mapping — and two 16-byte fp32 stores.
+template <bool kGradBf16, bool kAligned>
+__device__ __forceinline__ void load8e(const uint8_t* p, uint32_t k, float (&x)[8]) {
+  if (kGradBf16) {
+    const uint4 a = load16<kAligned>(p, k);
+    x[0] = bf16_lo(a.x); x[1] = bf16_hi(a.x); x[2] = bf16_lo(a.y); x[3] = bf16_hi(a.y);
+    x[4] = bf16_lo(a.z); x[5] = bf16_hi(a.z); x[6] = bf16_lo(a.w); x[7] = bf16_hi(a.w);
+  } else {
+    const uint4 a = load16<kAligned>(p, k), b = load16<kAligned>(p + 16, k);
+    x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y); x[2] = __uint_as_float(a.z); x[3] = __uint_as_float(a.w);
+    x[4] = __uint_as_float(b.x); x[5] = __uint_as_float(b.y); x[6] = __uint_as_float(b.z); x[7] = __uint_as_float(b.w);
+  }
+}
+
+template <int W, bool kGradBf16, bool kAligned>
+__device__ __forceinline__ void pull_body8(const PeerPtrs& st, uint64_t sb, float* __restrict__ g, uint32_t nv,
+                                           uint32_t k, PullOps ops) {
+  constexpr uint32_t gs = kGradBf16 ? 2 : 4;
+  constexpr int U = W <= 4 ? 2 : 1;
+  uint32_t v = threadIdx.x;
+  for (; v + (U - 1) * kThreads < nv; v += U * kThreads) {
+    float x[U][W][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < W; ++q)
+        load8e<kGradBf16, kAligned>(st.p[q] + sb + (uint64_t)gs * 8 * (v + u * kThreads), k, x[u][q]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float a[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        a[j] = ops.rb(ops.div(x[u][0][j]));
+#pragma unroll
+        for (int q = 1; q < W; ++q) a[j] = __fadd_rn(a[j], ops.rb(ops.div(x[u][q][j])));
+        a[j] = ops.rb(a[j]);
+      }
+      float4* gp = reinterpret_cast<float4*>(g) + 2 * (v + u * kThreads);
+      if (ops.acc) {
+        const float4 o0 = gp[0], o1 = gp[1];
+        a[0] = __fadd_rn(o0.x, a[0]); a[1] = __fadd_rn(o0.y, a[1]); a[2] = __fadd_rn(o0.z, a[2]); a[3] = __fadd_rn(o0.w, a[3]);
+        a[4] = __fadd_rn(o1.x, a[4]); a[5] = __fadd_rn(o1.y, a[5]); a[6] = __fadd_rn(o1.z, a[6]); a[7] = __fadd_rn(o1.w, a[7]);
+      }
+      gp[0] = make_float4(a[0], a[1], a[2], a[3]);
+      gp[1] = make_float4(a[4], a[5], a[6], a[7]);
+    }
+  }
+  for (; v < nv; v += kThreads) {
+    float x[W][8];
+#pragma unroll
+    for (int q = 0; q < W; ++q) load8e<kGradBf16, kAligned>(st.p[q] + sb + (uint64_t)gs * 8 * v, k, x[q]);
+    float a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      a[j] = ops.rb(ops.div(x[0][j]));
+#pragma unroll
+      for (int q = 1; q < W; ++q) a[j] = __fadd_rn(a[j], ops.rb(ops.div(x[q][j])));
+      a[j] = ops.rb(a[j]);
+    }
+    float4* gp = reinterpret_cast<float4*>(g) + 2 * v;
+    if (ops.acc) {
+      const float4 o0 = gp[0], o1 = gp[1];
+      a[0] = __fadd_rn(o0.x, a[0]); a[1] = __fadd_rn(o0.y, a[1]); a[2] = __fadd_rn(o0.z, a[2]); a[3] = __fadd_rn(o0.w, a[3]);
+      a[4] = __fadd_rn(o1.x, a[4]); a[5] = __fadd_rn(o1.y, a[5]); a[6] = __fadd_rn(o1.z, a[6]); a[7] = __fadd_rn(o1.w, a[7]);
+    }
+    gp[0] = make_float4(a[0], a[1], a[2], a[3]);
+    gp[1] = make_float4(a[4], a[5], a[6], a[7]);
+  }
+}
+
+template <int W, bool kGradBf16, int VEC>
 __global__ void __launch_bounds__(kThreads) k_rs_pull(const Tile* __restrict__ tiles, int ntiles, PeerPtrs st,
                                                       float* __restrict__ grad, PullOps ops) {
   constexpr uint32_t gs = kGradBf16 ? 2 : 4;
@@ -211,11 +282,17 @@ __global__ void __launch_bounds__(kThreads) k_rs_pull(const Tile* __restrict__ t
     const uint64_t sb = tl.src * gs;      // byte offset into every rank's staging
     float* g = grad + tl.dst;             // 16-byte aligned
     const uint32_t n = tl.n;
-    const uint32_t nv = n / 4;
-    const uint32_t k = (uint32_t)(sb & (kGradBf16 ? 7u : 15u));
-    if (k == 0) pull_body<W, kGradBf16, true>(st, sb, g, nv, 0, ops);
-    else pull_body<W, kGradBf16, false>(st, sb, g, nv, k, ops);
-    for (uint32_t e = nv * 4 + threadIdx.x; e < n; e += kThreads) {
+    const uint32_t nv = n / VEC;
+    if (VEC == 8) {
+      const uint32_t k = (uint32_t)(sb & 15u);
+      if (k == 0) pull_body8<W, kGradBf16, true>(st, sb, g, nv, 0, ops);
+      else pull_body8<W, kGradBf16, false>(st, sb, g, nv, k, ops);
+    } else {
+      const uint32_t k = (uint32_t)(sb & (kGradBf16 ? 7u : 15u));
+      if (k == 0) pull_body<W, kGradBf16, true>(st, sb, g, nv, 0, ops);
+      else pull_body<W, kGradBf16, false>(st, sb, g, nv, k, ops);
+    }
+    for (uint32_t e = nv * VEC + threadIdx.x; e < n; e += kThreads) {
       float a = 0.0f;
       for (int q = 0; q < W; ++q) {
         const uint8_t* p = st.p[q] + sb + (uint64_t)gs * e;
@@ -255,21 +332,28 @@ inline int grid_for(int64_t items, fsdpk::LaunchCfg cfg, int tuned = fsdpk::kCta
   return (int)(g < 1 ? 1 : g);
 }
 
-template <bool kGradBf16>
-cudaError_t launch_pull_w(const Tile* tiles, int ntiles, PeerPtrs st, float* grad, PullOps ops, int W, int g,
-                          cudaStream_t s) {
+template <bool kGradBf16, int V>
+cudaError_t launch_pull_wv(const Tile* tiles, int ntiles, PeerPtrs st, float* grad, PullOps ops, int W, int g,
+                           cudaStream_t s) {
   switch (W) {
-    case 1: k_rs_pull<1, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 2: k_rs_pull<2, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 3: k_rs_pull<3, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 4: k_rs_pull<4, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 5: k_rs_pull<5, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 6: k_rs_pull<6, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 7: k_rs_pull<7, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 8: k_rs_pull<8, kGradBf16><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 1: k_rs_pull<1, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 2: k_rs_pull<2, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 3: k_rs_pull<3, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 4: k_rs_pull<4, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 5: k_rs_pull<5, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 6: k_rs_pull<6, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 7: k_rs_pull<7, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 8: k_rs_pull<8, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+template <bool kGradBf16>
+cudaError_t launch_pull_w(const Tile* tiles, int ntiles, PeerPtrs st, float* grad, PullOps ops, int W, int g,
+                          cudaStream_t s, bool vec8) {
+  return vec8 ? launch_pull_wv<kGradBf16, 8>(tiles, ntiles, st, grad, ops, W, g, s)
+              : launch_pull_wv<kGradBf16, 4>(tiles, ntiles, st, grad, ops, W, g, s);
 }
 
 }  // namespace
@@ -299,8 +383,9 @@ cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool
   ops.acc = accumulate;
   ops.bf16r = bf16_reduce;
   const int g = grid_for(ntiles, cfg);
-  return grad_bf16 ? launch_pull_w<true>(tiles, ntiles, staging, grad, ops, W, g, st)
-                   : launch_pull_w<false>(tiles, ntiles, staging, grad, ops, W, g, st);
+  const bool vec8 = (cfg.variant & 1) != 0;
+  return grad_bf16 ? launch_pull_w<true>(tiles, ntiles, staging, grad, ops, W, g, st, vec8)
+                   : launch_pull_w<false>(tiles, ntiles, staging, grad, ops, W, g, st, vec8);
 }
 
 cudaError_t launch_gather_copy(const Tile* tiles, int ntiles, const fsdpk::PtrArray& srcs, void* dst,

@@ -38,6 +38,7 @@ def main():
     mesh = F.Mesh.from_process_group(device=local)
     comp = torch.cuda.Stream(device=dev)
     lines = []
+    algos = ["p2p", "nccl"] if mesh.algo == "p2p" else ["nccl"]
 
     def timed(fn):
         for _ in range(3):
@@ -58,7 +59,7 @@ def main():
         T = 1 << lg
         unit = synth.sweep_unit(T, W)
         shapes = [s for _, s, _ in unit]
-        for algo in (["p2p", "nccl"] if mesh.algo == "p2p" else ["nccl"]):
+        for algo in algos:
             mesh.set_algo(algo)
             layer = F.fsdp_shard(mesh, None, [False] * len(shapes), shapes=shapes)
             layer.sharded_flat().normal_(0, 0.02)

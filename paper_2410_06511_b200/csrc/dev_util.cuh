@@ -99,6 +99,39 @@ __device__ __forceinline__ uint2 ld_stream8(const void* p) {
   return a;
 }
 
+// L1-allocating variants for the misaligned phase of peer (NVLink) reads: the two aligned
+// blocks a lane loads overlap its neighbour's, and peer data bypasses L2 (cached in L1
+// only), so without L1 allocation every remote byte would cross NVLink twice.
+__device__ __forceinline__ uint2 ld_l1_8(const void* p) {
+  uint2 a;
+  asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(a.x), "=r"(a.y) : "l"(p));
+  return a;
+}
+__device__ __forceinline__ uint4 ld_l1_16(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+// 4 consecutive peer grad elements (as fp32), misaligned phase k != 0, L1-allocating loads.
+template <bool kGradBf16>
+__device__ __forceinline__ void load4_peer_misaligned(const uint8_t* p, uint32_t k, float (&x)[4]) {
+  if (kGradBf16) {
+    const uint8_t* b = p - k;
+    const uint2 u = ld_l1_8(b), w = ld_l1_8(b + 8);
+    const uint32_t sh = (k & 3u) * 8u;
+    uint2 a;
+    if (k < 4) { a.x = __funnelshift_r(u.x, u.y, sh); a.y = __funnelshift_r(u.y, w.x, sh); }
+    else { a.x = __funnelshift_r(u.y, w.x, sh); a.y = __funnelshift_r(w.x, w.y, sh); }
+    x[0] = bf16_lo(a.x); x[1] = bf16_hi(a.x); x[2] = bf16_lo(a.y); x[3] = bf16_hi(a.y);
+  } else {
+    const uint8_t* b = p - k;
+    const uint4 a = extract16(ld_l1_16(b), ld_l1_16(b + 16), k);
+    x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y);
+    x[2] = __uint_as_float(a.z); x[3] = __uint_as_float(a.w);
+  }
+}
+
 // 4 consecutive grad elements (as fp32) at byte address p whose phase is k: bf16 grads are
 // read as one 8-byte load (k in {0,2,4,6}: two aligned loads + funnel shift when k != 0),
 // fp32 grads as one 16-byte load (k in {0,4,8,12}).

@@ -138,6 +138,20 @@ __global__ void __launch_bounds__(kThreads) k_unshard_push(const Tile* __restric
 }
 
 // ------------------------------------------------------------------- reduce-scatter pull
+// Peer loads of the pull: aligned -> one streaming load; misaligned -> L1-allocating pair
+// (see dev_util.cuh load4_peer_misaligned).
+template <bool kGradBf16, bool kAligned>
+__device__ __forceinline__ void pload4(const uint8_t* p, uint32_t k, float (&x)[4]) {
+  if (kAligned) load4<kGradBf16, true>(p, 0, x);
+  else load4_peer_misaligned<kGradBf16>(p, k, x);
+}
+
+template <bool kAligned>
+__device__ __forceinline__ uint4 pload16(const uint8_t* p, uint32_t k) {
+  if (kAligned) return ld_stream(p);
+  return extract16(ld_l1_16(p - k), ld_l1_16(p - k + 16), k);
+}
+
 struct PullOps {
   float w, inv;
   bool pow2, mean, acc, bf16r;
@@ -162,7 +176,7 @@ __device__ __forceinline__ void pull_body(const PeerPtrs& st, uint64_t sb, float
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int q = 0; q < W; ++q)
-        load4<kGradBf16, kAligned>(st.p[q] + sb + (uint64_t)gs * 4 * (v + u * kThreads), k, x[u][q]);
+        pload4<kGradBf16, kAligned>(st.p[q] + sb + (uint64_t)gs * 4 * (v + u * kThreads), k, x[u][q]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       float a[4];
@@ -184,7 +198,7 @@ __device__ __forceinline__ void pull_body(const PeerPtrs& st, uint64_t sb, float
   for (; v < nv; v += kThreads) {
     float x[W][4];
 #pragma unroll
-    for (int q = 0; q < W; ++q) load4<kGradBf16, kAligned>(st.p[q] + sb + (uint64_t)gs * 4 * v, k, x[q]);
+    for (int q = 0; q < W; ++q) pload4<kGradBf16, kAligned>(st.p[q] + sb + (uint64_t)gs * 4 * v, k, x[q]);
     float a[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -207,11 +221,11 @@ __device__ __forceinline__ void pull_body(const PeerPtrs& st, uint64_t sb, float
 template <bool kGradBf16, bool kAligned>
 __device__ __forceinline__ void load8e(const uint8_t* p, uint32_t k, float (&x)[8]) {
   if (kGradBf16) {
-    const uint4 a = load16<kAligned>(p, k);
+    const uint4 a = pload16<kAligned>(p, k);
     x[0] = bf16_lo(a.x); x[1] = bf16_hi(a.x); x[2] = bf16_lo(a.y); x[3] = bf16_hi(a.y);
     x[4] = bf16_lo(a.z); x[5] = bf16_hi(a.z); x[6] = bf16_lo(a.w); x[7] = bf16_hi(a.w);
   } else {
-    const uint4 a = load16<kAligned>(p, k), b = load16<kAligned>(p + 16, k);
+    const uint4 a = pload16<kAligned>(p, k), b = pload16<kAligned>(p + 16, k);
     x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y); x[2] = __uint_as_float(a.z); x[3] = __uint_as_float(a.w);
     x[4] = __uint_as_float(b.x); x[5] = __uint_as_float(b.y); x[6] = __uint_as_float(b.z); x[7] = __uint_as_float(b.w);
   }

@@ -19,8 +19,6 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
-#include <map>
-#include <mutex>
 #include <new>
 #include <string>
 #include <thread>

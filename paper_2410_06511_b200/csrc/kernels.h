@@ -20,7 +20,7 @@ struct Tile {
 };
 static_assert(sizeof(Tile) == 32, "Tile must be 32 bytes");
 
-enum TileKind : uint32_t { TK_COPY = 0, TK_ZERO = 1, TK_FP8 = 2, TK_BF16 = 3 };
+enum TileKind : uint32_t { TK_COPY = 0, TK_FP8 = 2, TK_BF16 = 3 };
 
 constexpr int kMaxPtrs = 512;  // pointers per launch (4 KB kernel parameter)
 struct PtrArray { const void* p[kMaxPtrs]; };

@@ -95,19 +95,38 @@ __device__ __forceinline__ void push_tile(const Tile& tl, const float* __restric
   const uint32_t nb = (n - h) / V;
   const uint32_t ph = h & 3u;
   const float* abase = src + (h - ph);
-  // body: full 16-byte vectors, stored to every rank's arena
-  for (uint32_t v = threadIdx.x; v < nb; v += kThreads) {
+  // body: full 16-byte vectors, stored to every rank's arena; two vectors per thread per
+  // iteration so both vectors' loads are in flight before the stores
+  uint32_t v = threadIdx.x;
+  for (; v + kThreads < nb; v += 2 * kThreads) {
+    float x0[V], x1[V];
+    load_floats<V>(abase + V * v, ph, x0);
+    load_floats<V>(abase + V * (v + kThreads), ph, x1);
+    uint4 o0, o1;
+    if constexpr (kFp8) { o0 = cvt_e4m3x16(x0, s); o1 = cvt_e4m3x16(x1, s); }
+    else { o0 = cvt_bf16x8(x0); o1 = cvt_bf16x8(x1); }
+    const uint64_t off0 = dst0 + (uint64_t)h * es + 16ull * v;
+    const uint64_t off1 = off0 + 16ull * kThreads;
+    // arena.p is pre-rotated on the host (p[i] = rank (rank+1+i) % W's arena) so every rank
+    // starts on a different peer; constant indices keep the pointers out of local memory
+#pragma unroll
+    for (int i = 0; i < kMaxRanks; ++i) {
+      if (i >= W) break;
+      st_v4(arena.p[i] + off0, o0);
+      st_v4(arena.p[i] + off1, o1);
+    }
+  }
+  for (; v < nb; v += kThreads) {
     float x[V];
     load_floats<V>(abase + V * v, ph, x);
     uint4 o;
     if constexpr (kFp8) o = cvt_e4m3x16(x, s);
     else o = cvt_bf16x8(x);
     const uint64_t off = dst0 + (uint64_t)h * es + 16ull * v;
-#pragma unroll 1
-    for (int i = 0; i < W; ++i) {
-      int d = rank + 1 + i;
-      d = d >= W ? d - W : d;
-      st_v4(arena.p[d] + off, o);
+#pragma unroll
+    for (int i = 0; i < kMaxRanks; ++i) {
+      if (i >= W) break;
+      st_v4(arena.p[i] + off, o);
     }
   }
   // head and tail elements (partial 16-byte vectors: element-sized stores only)
@@ -117,10 +136,18 @@ __device__ __forceinline__ void push_tile(const Tile& tl, const float* __restric
     const uint64_t off = dst0 + (uint64_t)el * es;
     if (kFp8) {
       const uint8_t b = (uint8_t)(pack_e4m3x2(__fmul_rn(src[el], s), 0.0f) & 0xFFu);
-      for (int d = 0; d < W; ++d) arena.p[d][off] = b;
+#pragma unroll
+      for (int d = 0; d < kMaxRanks; ++d) {
+        if (d >= W) break;
+        arena.p[d][off] = b;
+      }
     } else {
       const uint16_t b = (uint16_t)(pack_bf16x2(src[el], 0.0f) & 0xFFFFu);
-      for (int d = 0; d < W; ++d) *reinterpret_cast<uint16_t*>(arena.p[d] + off) = b;
+#pragma unroll
+      for (int d = 0; d < kMaxRanks; ++d) {
+        if (d >= W) break;
+        *reinterpret_cast<uint16_t*>(arena.p[d] + off) = b;
+      }
     }
   }
 }
@@ -168,7 +195,7 @@ template <int W, bool kGradBf16, bool kAligned>
 __device__ __forceinline__ void pull_body(const PeerPtrs& st, uint64_t sb, float* __restrict__ g, uint32_t nv,
                                           uint32_t k, PullOps ops) {
   constexpr uint32_t gs = kGradBf16 ? 2 : 4;
-  constexpr int U = W <= 4 ? 4 : 2;
+  constexpr int U = W <= 2 ? 4 : (W <= 4 ? 2 : 1);   // ~8-16 loads in flight per thread, no spills
   uint32_t v = threadIdx.x;
   for (; v + (U - 1) * kThreads < nv; v += U * kThreads) {
     float x[U][W][4];
@@ -381,7 +408,9 @@ cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W
 cudaError_t launch_unshard_push(const Tile* tiles, int ntiles, const float* shard, const float* scales,
                                 PeerPtrs arena, int W, int rank, fsdpk::LaunchCfg cfg, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
-  k_unshard_push<<<grid_for(ntiles, cfg, fsdpk::kCtasPush), kThreads, 0, st>>>(tiles, ntiles, shard, scales, arena,
+  PeerPtrs rot{};   // destination order starts at the next rank: spreads NVLink traffic
+  for (int i = 0; i < W; ++i) rot.p[i] = arena.p[(rank + 1 + i) % W];
+  k_unshard_push<<<grid_for(ntiles, cfg, fsdpk::kCtasPush), kThreads, 0, st>>>(tiles, ntiles, shard, scales, rot,
                                                                                W, rank);
   return cudaGetLastError();
 }

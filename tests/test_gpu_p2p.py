@@ -43,10 +43,14 @@ def test_unshard_push_emulated(kind, seed, W, fp8):
         _, fulls = w.unshard(shards, FP8 if fp8 else BF16, scale)
         for d in range(W):
             a = arenas[d].cpu().numpy()
+            written = np.zeros(a.size, dtype=bool)
             for p, want in enumerate(fulls):
                 nb = want.size * want.itemsize
                 got = a[offs[p]:offs[p] + nb].view(want.dtype).reshape(want.shape)
                 np.testing.assert_array_equal(got, want)
+                written[offs[p]:offs[p] + nb] = True
+            # guard band: no byte outside the params' tensors (alignment gaps, tail) was written
+            assert np.all(a[~written] == 0xA5)
     finally:
         emu.close()
 
@@ -96,5 +100,11 @@ def test_rs_pull_emulated(kind, seed, W, gd, rd, mean, acc):
                     prev = old[r][m["elem_offset"]:m["elem_offset"] + got.size].reshape(got.shape)
                     want = (prev + want).astype(np.float32)
                 np.testing.assert_array_equal(got.view(np.uint32), want.astype(np.float32).view(np.uint32))
+            # guard band: padding rows and alignment gaps of the grad buffer are untouched
+            flat = l.sharded_grad_flat().cpu().numpy()
+            real = np.zeros(l.S, dtype=bool)
+            for m in l.metas:
+                real[m["elem_offset"]:m["elem_offset"] + m["row_count"] * m["rest"]] = True
+            np.testing.assert_array_equal(flat[~real].view(np.uint32), old[r][~real].view(np.uint32))
     finally:
         emu.close()

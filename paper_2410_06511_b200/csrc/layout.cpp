@@ -77,11 +77,14 @@ std::vector<fsdpk::Tile> tiles_copy_in_fp8(const Layout& L) {
   for (size_t p = 0; p < L.metas.size(); ++p) {
     const auto& m = L.metas[p];
     const int64_t es = L.fp8[p] ? 1 : 2;
-    for (int64_t j = 0; j < m.padded_numel; j += fsdpk::kTileElems) {
+    // cover the whole 16-byte aligned slot segment: the shard is zero beyond n_p up to
+    // round_up(n_p, 16) >= round_up(n_p * es, 16) / es, so the gap bytes become 0 too
+    const int64_t cover = round_up(m.padded_numel * es, kAlignBytes) / es;
+    for (int64_t j = 0; j < cover; j += fsdpk::kTileElems) {
       fsdpk::Tile x{};
       x.src = (uint64_t)(m.elem_offset + j);
       x.dst = (uint64_t)(m.fp8_byte_offset + j * es);
-      x.n = (uint32_t)std::min<int64_t>(fsdpk::kTileElems, m.padded_numel - j);
+      x.n = (uint32_t)std::min<int64_t>(fsdpk::kTileElems, cover - j);
       x.param = (uint32_t)p;
       x.kind = L.fp8[p] ? fsdpk::TK_FP8 : fsdpk::TK_BF16;
       t.push_back(x);

@@ -632,6 +632,9 @@ static void mesh_common_init(fsdp_mesh* m) {
   if (const char* e = std::getenv("FSDP_B200_CTAS_PER_SM")) per_sm = std::max(1, std::min(16, std::atoi(e)));
   m->cfg.sms = sms;
   m->cfg.per_sm = per_sm;
+  // default: TMA bulk push (bit 2) and, for zero-copy reduce-scatters, TMA bulk pull (bit 1)
+  // — measured best at W=2/4 (profiles/r06); FSDP_B200_VARIANT overrides (0 = plain ld/st)
+  m->cfg.variant = 6;
   if (const char* e = std::getenv("FSDP_B200_VARIANT")) m->cfg.variant = std::atoi(e);
   m->cfg.grid_cap = sms * (per_sm > 0 ? per_sm : 4);
   CUDA_CHECK(cudaMalloc(&m->d_err, sizeof(int)));
@@ -1327,8 +1330,10 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       }
       {
         ProfScope pp(m, FSDP_PROF_RS_PULL, m->s_rs, (int64_t)(m->W - 1) * l->pull_elems * gsz);
+        fsdpk::LaunchCfg pcfg = m->cfg;
+        if (!zc) pcfg.variant &= ~2;   // bulk pull only without a concurrent staging copy (profiles/r06)
         CUDA_CHECK(fsdpp::launch_rs_pull(l->t_pull.d, l->t_pull.n, peer_ptrs(m, ss->buf), gd == FSDP_BFLOAT16, divisor,
-                                         target, mean != 0, accumulate != 0 && !hsdp, obf, m->W, m->cfg, m->s_rs));
+                                         target, mean != 0, accumulate != 0 && !hsdp, obf, m->W, pcfg, m->s_rs));
         pp.done();
       }
       {

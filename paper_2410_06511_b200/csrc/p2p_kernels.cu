@@ -347,6 +347,183 @@ __global__ void __launch_bounds__(kThreads) k_rs_pull(const Tile* __restrict__ t
   }
 }
 
+// ------------------------------------------------------------------- TMA bulk variants
+// Pull: the TMA engine brings each rank's chunk (4 KB) of the tile into shared memory
+// (cp.async.bulk global->shared, mbarrier complete_tx, 2 stages), threads reduce from smem.
+// Push: threads cast a 4 KB output chunk into smem once, one thread bulk-stores it into
+// every rank's arena (cp.async.bulk shared->global, W stores per chunk, 2 stages).
+constexpr uint32_t kBulkChunk = 4096;
+
+template <int W, bool kGradBf16>
+__global__ void __launch_bounds__(kThreads) k_rs_pull_bulk(const Tile* __restrict__ tiles, int ntiles, PeerPtrs st,
+                                                           float* __restrict__ grad, PullOps ops) {
+  extern __shared__ __align__(128) uint8_t smem[];   // [2][W][kBulkChunk]
+  __shared__ uint64_t full[2];
+  constexpr uint32_t gs = kGradBf16 ? 2 : 4;
+  constexpr uint32_t CE = kBulkChunk / gs;             // elements per chunk
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t it = 0;   // chunks consumed by this CTA so far (stage = it & 1, parity = (it >> 1) & 1)
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    const uint64_t sb = tl.src * gs;
+    float* g = grad + tl.dst;
+    const uint32_t n = tl.n;
+    if ((sb & 15u) != 0 || ((n * gs) & 15u) != 0) {   // bulk needs 16-byte granularity
+      const uint32_t k = (uint32_t)(sb & (kGradBf16 ? 7u : 15u));
+      const uint32_t nv = n / 4;
+      if (k == 0) pull_body<W, kGradBf16, true>(st, sb, g, nv, 0, ops);
+      else pull_body<W, kGradBf16, false>(st, sb, g, nv, k, ops);
+      for (uint32_t e = nv * 4 + threadIdx.x; e < n; e += kThreads) {
+        float a = 0.0f;
+        for (int q = 0; q < W; ++q) {
+          const uint8_t* p = st.p[q] + sb + (uint64_t)gs * e;
+          const float x = kGradBf16 ? __uint_as_float(((uint32_t)(*(const uint16_t*)p)) << 16) : *(const float*)p;
+          const float y = ops.rb(ops.div(x));
+          a = q == 0 ? y : __fadd_rn(a, y);
+        }
+        a = ops.rb(a);
+        g[e] = ops.acc ? __fadd_rn(g[e], a) : a;
+      }
+      continue;
+    }
+    const uint32_t nch = (n + CE - 1) / CE;
+    auto issue = [&](uint32_t c, uint32_t i) {
+      const uint32_t s = i & 1u;
+      const uint32_t bytes = min(CE, n - c * CE) * gs;
+      mbar_arrive_expect_tx(&full[s], W * bytes);
+#pragma unroll
+      for (int q = 0; q < W; ++q)
+        bulk_g2s(smem + ((size_t)s * W + q) * kBulkChunk, st.p[q] + sb + (uint64_t)c * kBulkChunk, bytes, &full[s]);
+    };
+    if (threadIdx.x == 0) {
+      issue(0, it);
+      if (nch > 1) issue(1, it + 1);
+    }
+    for (uint32_t c = 0; c < nch; ++c) {
+      const uint32_t i = it + c, s = i & 1u;
+      mbar_wait(&full[s], (i >> 1) & 1u);
+      const uint32_t ne = min(CE, n - c * CE);
+      float* gc = g + (size_t)c * CE;
+      for (uint32_t e4 = threadIdx.x; e4 * 4 < ne; e4 += kThreads) {
+        float a[4];
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          const uint8_t* sp = smem + ((size_t)s * W + q) * kBulkChunk + (size_t)e4 * 4 * gs;
+          float x[4];
+          if (kGradBf16) {
+            const uint2 u = *reinterpret_cast<const uint2*>(sp);
+            x[0] = bf16_lo(u.x); x[1] = bf16_hi(u.x); x[2] = bf16_lo(u.y); x[3] = bf16_hi(u.y);
+          } else {
+            const float4 u = *reinterpret_cast<const float4*>(sp);
+            x[0] = u.x; x[1] = u.y; x[2] = u.z; x[3] = u.w;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float y = ops.rb(ops.div(x[j]));
+            a[j] = q == 0 ? y : __fadd_rn(a[j], y);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a[j] = ops.rb(a[j]);
+        float4* gp = reinterpret_cast<float4*>(gc) + e4;
+        if (ops.acc) {
+          const float4 o = *gp;
+          a[0] = __fadd_rn(o.x, a[0]); a[1] = __fadd_rn(o.y, a[1]); a[2] = __fadd_rn(o.z, a[2]); a[3] = __fadd_rn(o.w, a[3]);
+        }
+        *gp = make_float4(a[0], a[1], a[2], a[3]);
+      }
+      __syncthreads();   // everyone is done with stage s before the TMA refills it
+      if (threadIdx.x == 0 && c + 2 < nch) issue(c + 2, i + 2);
+    }
+    it += nch;
+  }
+}
+
+template <bool kFp8>
+__device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __restrict__ shard, float s,
+                                               const PeerPtrs& arena, int W, uint8_t* stage_buf, uint32_t& it) {
+  constexpr uint32_t es = kFp8 ? 1 : 2;
+  constexpr uint32_t V = 16 / es;                    // elements per 16-byte vector
+  constexpr uint32_t CV = kBulkChunk / 16;           // vectors per chunk (= kThreads)
+  const float* src = shard + tl.src;
+  const uint64_t dst0 = tl.dst;
+  const uint32_t n = tl.n;
+  uint32_t h = (uint32_t)(((16u - (uint32_t)(dst0 & 15u)) & 15u) / es);
+  if (h > n) h = n;
+  const uint32_t nb = (n - h) / V;
+  const uint32_t ph = h & 3u;
+  const float* abase = src + (h - ph);
+  const uint64_t body0 = dst0 + (uint64_t)h * es;   // 16-byte aligned
+  const uint32_t nch = (nb + CV - 1) / CV;
+  for (uint32_t c = 0; c < nch; ++c, ++it) {
+    uint8_t* buf = stage_buf + (size_t)(it & 1u) * kBulkChunk;
+    if (threadIdx.x == 0) bulk_wait_read_le1();       // the chunk written 2 iterations ago was read
+    __syncthreads();
+    const uint32_t v = c * CV + threadIdx.x;
+    if (v < nb) {
+      float x[V];
+      load_floats<V>(abase + V * v, ph, x);
+      uint4 o;
+      if constexpr (kFp8) o = cvt_e4m3x16(x, s);
+      else o = cvt_bf16x8(x);
+      *reinterpret_cast<uint4*>(buf + 16 * threadIdx.x) = o;
+    }
+    fence_proxy_async_smem();                         // generic smem writes -> async proxy
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = 16u * min(CV, nb - c * CV);
+#pragma unroll
+      for (int d = 0; d < kMaxRanks; ++d) {
+        if (d >= W) break;
+        bulk_s2g(arena.p[d] + body0 + (uint64_t)c * kBulkChunk, buf, bytes);
+      }
+      bulk_commit();
+    }
+  }
+  // head and tail elements (partial 16-byte vectors: element-sized stores only)
+  const uint32_t tail0 = h + nb * V;
+  for (uint32_t e = threadIdx.x; e < h + (n - tail0); e += kThreads) {
+    const uint32_t el = e < h ? e : tail0 + (e - h);
+    const uint64_t off = dst0 + (uint64_t)el * es;
+    if (kFp8) {
+      const uint8_t b = (uint8_t)(pack_e4m3x2(__fmul_rn(src[el], s), 0.0f) & 0xFFu);
+#pragma unroll
+      for (int d = 0; d < kMaxRanks; ++d) {
+        if (d >= W) break;
+        arena.p[d][off] = b;
+      }
+    } else {
+      const uint16_t b = (uint16_t)(pack_bf16x2(src[el], 0.0f) & 0xFFFFu);
+#pragma unroll
+      for (int d = 0; d < kMaxRanks; ++d) {
+        if (d >= W) break;
+        *reinterpret_cast<uint16_t*>(arena.p[d] + off) = b;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_unshard_push_bulk(const Tile* __restrict__ tiles, int ntiles,
+                                                                const float* __restrict__ shard,
+                                                                const float* __restrict__ scales, PeerPtrs arena,
+                                                                int W) {
+  __shared__ __align__(128) uint8_t stage_buf[2 * kBulkChunk];
+  uint32_t it = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    if (tl.kind == fsdpk::TK_FP8) push_tile_bulk<true>(tl, shard, scales[tl.param], arena, W, stage_buf, it);
+    else push_tile_bulk<false>(tl, shard, 0.0f, arena, W, stage_buf, it);
+  }
+  if (threadIdx.x == 0) bulk_wait0();                 // every bulk store has completed
+  __syncthreads();
+  __threadfence_system();
+}
+
 // ------------------------------------------------------------------- gather copy
 __global__ void __launch_bounds__(kThreads) k_gather_copy(const Tile* __restrict__ tiles, int ntiles,
                                                           fsdpk::PtrArray srcs, uint8_t* __restrict__ dst_base) {
@@ -390,11 +567,39 @@ cudaError_t launch_pull_wv(const Tile* tiles, int ntiles, PeerPtrs st, float* gr
   return cudaGetLastError();
 }
 
+template <int W, bool kGradBf16>
+cudaError_t launch_pull_bulk_w(const Tile* tiles, int ntiles, PeerPtrs st, float* grad, PullOps ops, int g,
+                               cudaStream_t s) {
+  const size_t smem = 2ull * W * kBulkChunk;
+  static bool attr = false;   // one attribute set per instantiation (host, first use)
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_rs_pull_bulk<W, kGradBf16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_rs_pull_bulk<W, kGradBf16><<<g, kThreads, smem, s>>>(tiles, ntiles, st, grad, ops);
+  return cudaGetLastError();
+}
+
 template <bool kGradBf16>
 cudaError_t launch_pull_w(const Tile* tiles, int ntiles, PeerPtrs st, float* grad, PullOps ops, int W, int g,
-                          cudaStream_t s, bool vec8) {
-  return vec8 ? launch_pull_wv<kGradBf16, 8>(tiles, ntiles, st, grad, ops, W, g, s)
-              : launch_pull_wv<kGradBf16, 4>(tiles, ntiles, st, grad, ops, W, g, s);
+                          cudaStream_t s, int variant) {
+  if (variant & 2) {   // TMA bulk pull
+    switch (W) {
+      case 1: return launch_pull_bulk_w<1, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
+      case 2: return launch_pull_bulk_w<2, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
+      case 3: return launch_pull_bulk_w<3, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
+      case 4: return launch_pull_bulk_w<4, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
+      case 5: return launch_pull_bulk_w<5, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
+      case 6: return launch_pull_bulk_w<6, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
+      case 7: return launch_pull_bulk_w<7, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
+      case 8: return launch_pull_bulk_w<8, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  return (variant & 1) ? launch_pull_wv<kGradBf16, 8>(tiles, ntiles, st, grad, ops, W, g, s)
+                       : launch_pull_wv<kGradBf16, 4>(tiles, ntiles, st, grad, ops, W, g, s);
 }
 
 }  // namespace
@@ -410,6 +615,11 @@ cudaError_t launch_unshard_push(const Tile* tiles, int ntiles, const float* shar
   if (ntiles == 0) return cudaSuccess;
   PeerPtrs rot{};   // destination order starts at the next rank: spreads NVLink traffic
   for (int i = 0; i < W; ++i) rot.p[i] = arena.p[(rank + 1 + i) % W];
+  if (cfg.variant & 4) {   // TMA bulk push
+    k_unshard_push_bulk<<<grid_for(ntiles, cfg, fsdpk::kCtasPush), kThreads, 0, st>>>(tiles, ntiles, shard, scales,
+                                                                                        rot, W);
+    return cudaGetLastError();
+  }
   k_unshard_push<<<grid_for(ntiles, cfg, fsdpk::kCtasPush), kThreads, 0, st>>>(tiles, ntiles, shard, scales, rot,
                                                                                W, rank);
   return cudaGetLastError();
@@ -426,9 +636,8 @@ cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool
   ops.acc = accumulate;
   ops.bf16r = bf16_reduce;
   const int g = grid_for(ntiles, cfg);
-  const bool vec8 = (cfg.variant & 1) != 0;
-  return grad_bf16 ? launch_pull_w<true>(tiles, ntiles, staging, grad, ops, W, g, st, vec8)
-                   : launch_pull_w<false>(tiles, ntiles, staging, grad, ops, W, g, st, vec8);
+  return grad_bf16 ? launch_pull_w<true>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant)
+                   : launch_pull_w<false>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant);
 }
 
 cudaError_t launch_gather_copy(const Tile* tiles, int ntiles, const fsdpk::PtrArray& srcs, void* dst,

@@ -632,9 +632,9 @@ static void mesh_common_init(fsdp_mesh* m) {
   if (const char* e = std::getenv("FSDP_B200_CTAS_PER_SM")) per_sm = std::max(1, std::min(16, std::atoi(e)));
   m->cfg.sms = sms;
   m->cfg.per_sm = per_sm;
-  // default: TMA bulk push (bit 2) and, for zero-copy reduce-scatters, TMA bulk pull (bit 1)
-  // — measured best at W=2/4 (profiles/r06); FSDP_B200_VARIANT overrides (0 = plain ld/st)
-  m->cfg.variant = 6;
+  // default: TMA bulk push (4), bulk RS copy-in (8) and, for zero-copy reduce-scatters, bulk
+  // pull (2) — measured best (profiles/r06, r07); FSDP_B200_VARIANT overrides (0 = plain ld/st)
+  m->cfg.variant = 14;
   if (const char* e = std::getenv("FSDP_B200_VARIANT")) m->cfg.variant = std::atoi(e);
   m->cfg.grid_cap = sms * (per_sm > 0 ? per_sm : 4);
   CUDA_CHECK(cudaMalloc(&m->d_err, sizeof(int)));

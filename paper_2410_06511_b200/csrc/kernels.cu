@@ -163,13 +163,11 @@ __device__ __forceinline__ void rs_body(const uint8_t* s, uint8_t* d, uint32_t n
 }
 
 template <bool kGradBf16, bool kOutBf16>
-__global__ void __launch_bounds__(kThreads) k_rs_copy_in(const Tile* __restrict__ tiles, int ntiles,
-                                                         PtrArray grads, uint8_t* __restrict__ rs_in,
-                                                         DivW div) {
+__device__ __forceinline__ void rs_tile(const Tile& tl, const PtrArray& grads, uint8_t* __restrict__ rs_in,
+                                        DivW div) {
   constexpr uint32_t gsz = kGradBf16 ? 2 : 4;
   constexpr uint32_t osz = kOutBf16 ? 2 : 4;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const Tile tl = tiles[t];
+  {
     uint8_t* d = rs_in + tl.dst * osz;   // 16-byte aligned (tiles start at 16-element offsets)
     const uint32_t n = tl.n;             // multiple of 16
     const uint32_t ns = tl.pad;          // valid source elements
@@ -195,6 +193,122 @@ __global__ void __launch_bounds__(kThreads) k_rs_copy_in(const Tile* __restrict_
     for (uint32_t b = zb * osz + 16 * threadIdx.x; b < n * osz; b += 16 * kThreads)
       st_v4(d + b, make_uint4(0, 0, 0, 0));
   }
+}
+
+template <bool kGradBf16, bool kOutBf16>
+__global__ void __launch_bounds__(kThreads) k_rs_copy_in(const Tile* __restrict__ tiles, int ntiles,
+                                                         PtrArray grads, uint8_t* __restrict__ rs_in,
+                                                         DivW div) {
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) rs_tile<kGradBf16, kOutBf16>(tiles[t], grads, rs_in, div);
+}
+
+// TMA bulk variant: per 2048-element chunk the TMA engine loads the grad chunk into shared
+// memory (mbarrier complete_tx, 2 stages), threads widen / divide / zero-pad into an output
+// stage, one thread bulk-stores it (cp.async.bulk shared->global, 2 stages).  Tiles whose
+// source is not 16-byte aligned take the register path.
+constexpr uint32_t kRsChunk = 2048;
+
+template <bool kGradBf16, bool kOutBf16>
+__global__ void __launch_bounds__(kThreads) k_rs_copy_in_bulk(const Tile* __restrict__ tiles, int ntiles,
+                                                              PtrArray grads, uint8_t* __restrict__ rs_in,
+                                                              DivW div) {
+  constexpr uint32_t gsz = kGradBf16 ? 2 : 4;
+  constexpr uint32_t osz = kOutBf16 ? 2 : 4;
+  __shared__ __align__(128) uint8_t sin[2][kRsChunk * gsz];
+  __shared__ __align__(128) uint8_t sout[2][kRsChunk * osz];
+  __shared__ uint64_t full[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t it = 0;           // chunks processed by this CTA (stage = it & 1)
+  uint32_t loads0 = 0, loads1 = 0;  // completed loads per stage barrier (parity = loads & 1)
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    const uint8_t* s = (const uint8_t*)grads.p[tl.param] + tl.src * gsz;
+    uint8_t* d = rs_in + tl.dst * osz;
+    const uint32_t n = tl.n, ns = tl.pad;
+    if ((((uintptr_t)s) & 15u) != 0 || ((ns * gsz) & 15u) != 0) {
+      rs_tile<kGradBf16, kOutBf16>(tl, grads, rs_in, div);
+      continue;
+    }
+    const uint32_t nch = (n + kRsChunk - 1) / kRsChunk;
+    auto valid = [&](uint32_t c) -> uint32_t {   // source elements of chunk c
+      const uint32_t b = c * kRsChunk;
+      const uint32_t ne = min(kRsChunk, n - b);
+      return ns > b ? min(ns - b, ne) : 0u;
+    };
+    auto issue = [&](uint32_t c, uint32_t i) {
+      const uint32_t nv = valid(c);
+      if (nv == 0) return;
+      mbar_arrive_expect_tx(&full[i & 1u], nv * gsz);
+      bulk_g2s(sin[i & 1u], s + (size_t)c * kRsChunk * gsz, nv * gsz, &full[i & 1u]);
+    };
+    if (threadIdx.x == 0) {
+      issue(0, it);
+      if (nch > 1) issue(1, it + 1);
+    }
+    for (uint32_t c = 0; c < nch; ++c) {
+      const uint32_t i = it + c, st = i & 1u;
+      const uint32_t ne = min(kRsChunk, n - c * kRsChunk);
+      const uint32_t nv = valid(c);
+      if (nv > 0) {
+        const uint32_t par = (st ? loads1 : loads0) & 1u;
+        if (st) ++loads1;
+        else ++loads0;
+        mbar_wait(&full[st], par);
+      }
+      if (threadIdx.x == 0) bulk_wait_read_le1();   // sout[st] (stored 2 chunks ago) was read
+      __syncthreads();
+      for (uint32_t e8 = threadIdx.x; e8 * 8 < ne; e8 += kThreads) {
+        float x[8];
+        const uint32_t e = e8 * 8;
+        if (e + 8 <= nv) {
+          if (kGradBf16) {
+            const uint4 a = *reinterpret_cast<const uint4*>(sin[st] + e * 2);
+            x[0] = bf16_lo(a.x); x[1] = bf16_hi(a.x); x[2] = bf16_lo(a.y); x[3] = bf16_hi(a.y);
+            x[4] = bf16_lo(a.z); x[5] = bf16_hi(a.z); x[6] = bf16_lo(a.w); x[7] = bf16_hi(a.w);
+          } else {
+            const float4 a = *reinterpret_cast<const float4*>(sin[st] + e * 4);
+            const float4 b = *reinterpret_cast<const float4*>(sin[st] + e * 4 + 16);
+            x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) x[j] = div(x[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t ej = e + j;
+            float v = 0.0f;   // padding rows / alignment gap
+            if (ej < nv) {
+              v = kGradBf16 ? __uint_as_float(((uint32_t)reinterpret_cast<const uint16_t*>(sin[st])[ej]) << 16)
+                            : reinterpret_cast<const float*>(sin[st])[ej];
+              v = div(v);
+            }
+            x[j] = v;
+          }
+        }
+        if (kOutBf16) {
+          *reinterpret_cast<uint4*>(sout[st] + e * 2) =
+              make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]), pack_bf16x2(x[4], x[5]), pack_bf16x2(x[6], x[7]));
+        } else {
+          *reinterpret_cast<float4*>(sout[st] + e * 4) = make_float4(x[0], x[1], x[2], x[3]);
+          *reinterpret_cast<float4*>(sout[st] + e * 4 + 16) = make_float4(x[4], x[5], x[6], x[7]);
+        }
+      }
+      fence_proxy_async_smem();
+      __syncthreads();   // sout[st] complete, sin[st] consumed
+      if (threadIdx.x == 0) {
+        bulk_s2g(d + (size_t)c * kRsChunk * osz, sout[st], ne * osz);
+        bulk_commit();
+        if (c + 2 < nch) issue(c + 2, i + 2);
+      }
+    }
+    it += nch;
+  }
+  if (threadIdx.x == 0) bulk_wait0();
 }
 
 // ------------------------------------------------------------------- K6 RS copy-out
@@ -353,8 +467,16 @@ cudaError_t launch_rs_copy_in(const Tile* tiles, int ntiles, const PtrArray& gra
   div.pow2 = (world_size & (world_size - 1)) == 0;
   div.inv = 1.0f / (float)world_size;
   div.mean = mean;
-  const int g = grid_for(ntiles, cfg, kCtasRsCopyIn);
   uint8_t* d = (uint8_t*)rs_in;
+  if (cfg.variant & 8) {   // TMA bulk K5
+    const int gb = grid_for(ntiles, cfg, kCtasCopy);
+    if (grad_bf16 && !out_bf16) k_rs_copy_in_bulk<true, false><<<gb, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
+    else if (grad_bf16 && out_bf16) k_rs_copy_in_bulk<true, true><<<gb, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
+    else if (!grad_bf16 && !out_bf16) k_rs_copy_in_bulk<false, false><<<gb, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
+    else k_rs_copy_in_bulk<false, true><<<gb, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
+    return cudaGetLastError();
+  }
+  const int g = grid_for(ntiles, cfg, kCtasRsCopyIn);
   if (grad_bf16 && !out_bf16) k_rs_copy_in<true, false><<<g, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
   else if (grad_bf16 && out_bf16) k_rs_copy_in<true, true><<<g, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
   else if (!grad_bf16 && !out_bf16) k_rs_copy_in<false, false><<<g, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);

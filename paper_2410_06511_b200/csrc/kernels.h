@@ -32,7 +32,9 @@ struct LaunchCfg {
   int grid_cap;     // max CTAs when the kernel has no tuned value (SMs * 4)
   int sms = 148;    // multiprocessor count
   int per_sm = 0;   // > 0: FSDP_B200_CTAS_PER_SM override for every kernel
-  int variant = 0;  // FSDP_B200_VARIANT bit mask (kernel experiments): bit 0 = 16-byte pull loads
+  // kernel-variant bit mask (FSDP_B200_VARIANT): 1 = 16-byte pull loads, 2 = TMA bulk pull,
+  // 4 = TMA bulk push, 8 = TMA bulk RS copy-in (K5)
+  int variant = 0;
   // persistent grid of a kernel whose measured best is `tuned` CTAs per SM
   int cap(int tuned) const { return sms * (per_sm > 0 ? per_sm : tuned); }
 };

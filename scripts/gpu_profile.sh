@@ -1,5 +1,5 @@
 # usage: bash scripts/gpu_profile.sh TAG — bench + ncu launch list + ncu --set full of the W=1 kernels
-TAG=${1:-r04}
+TAG=${1:-r07}
 mkdir -p gpurun_out
 B="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
 $B > gpurun_out/${TAG}_plain.log 2>&1 && \

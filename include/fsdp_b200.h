@@ -198,6 +198,11 @@ fsdp_status_t fsdp_mesh_get_algo(const fsdp_mesh_t* mesh, int32_t* algo);
  * error, FSDP_ERR_TIMEOUT after timeout_ms (<= 0: no timeout); after NCCL/TIMEOUT the
  * communicators are aborted and the mesh is unusable. */
 fsdp_status_t fsdp_mesh_synchronize(fsdp_mesh_t* mesh, int64_t timeout_ms);
+/* Marks the mesh unusable without any collective step (aborts its NCCL communicators);
+ * layers and the mesh can then be destroyed rank-locally.  Use after FSDP_ERR_TIMEOUT /
+ * FSDP_ERR_NCCL on any rank.  P2P handshakes give up after FSDP_B200_P2P_TIMEOUT_MS
+ * (default 60000) and report FSDP_ERR_TIMEOUT through fsdp_mesh_synchronize. */
+fsdp_status_t fsdp_mesh_abort(fsdp_mesh_t* mesh);
 
 /* Profiling: when on, every kernel / collective launch is bracketed by CUDA events on
  * its own stream; fsdp_profile_read synchronizes and returns the totals since the last

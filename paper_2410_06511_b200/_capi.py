@@ -62,6 +62,7 @@ SIGNATURES = {
     "fsdp_mesh_destroy": [_VP],
     "fsdp_mesh_info": [_VP, C.POINTER(_I32), C.POINTER(_I32), C.POINTER(_I32)],
     "fsdp_mesh_synchronize": [_VP, _I64],
+    "fsdp_mesh_abort": [_VP],
     "fsdp_mesh_set_algo": [_VP, _I32],
     "fsdp_mesh_get_algo": [_VP, C.POINTER(_I32)],
     "fsdp_profile_enable": [_VP, _I32],

@@ -218,6 +218,7 @@ struct fsdp_mesh {
   std::vector<SymSlot*> p2p_ag, p2p_rs;      // unsharded arenas, grad staging
   uint64_t rs_rr = 0;                        // round robin over staging slots
   int gbuf_seq = 0;                          // flag slots of layer grad buffers: kPoolSlots + seq
+  unsigned long long p2p_timeout_ns = 60ull * 1000 * 1000 * 1000;   // handshake spin bound
   int* d_barrier = nullptr;
 };
 
@@ -426,6 +427,15 @@ bool mesh_all_ok(fsdp_mesh* m, bool ok) {
   CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
   CUDA_CHECK(cudaMemcpy(&v, m->d_barrier, sizeof(int), cudaMemcpyDeviceToHost));
   return v == 1;
+}
+
+// Rank-local (aborted mesh): unmap the peers' copies and free the local one, no barrier.
+void sym_free_local(fsdp_mesh* m, SymBuf& b) {
+  for (int r = 0; r < m->W; ++r)
+    if (r != m->rank && r < (int)b.peers.size() && b.peers[r]) cudaIpcCloseMemHandle(b.peers[r]);
+  if (b.local) cudaFree(b.local);
+  cudaGetLastError();
+  b = SymBuf();
 }
 
 // Collective: unmap the peers' copies, wait until every rank did, then free the local one.
@@ -653,6 +663,8 @@ static void p2p_init(fsdp_mesh* m) {
   const char* env = std::getenv("FSDP_B200_ALGO");
   const bool want_nccl = env && std::string(env) == "nccl";
   m->algo = (m->p2p_ok && !want_nccl) ? FSDP_ALGO_P2P : FSDP_ALGO_NCCL;
+  if (const char* t = std::getenv("FSDP_B200_P2P_TIMEOUT_MS"))
+    m->p2p_timeout_ns = (unsigned long long)std::max(1L, std::atol(t)) * 1000000ull;
 }
 
 static fsdp_status_t mesh_init_impl(const uint8_t* id, int32_t W, int32_t rank, int32_t dev, bool local,
@@ -731,7 +743,19 @@ fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
     DeviceGuard g(m->device);
     for (cudaStream_t s : {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs})
       if (s) cudaStreamSynchronize(s);
-    if (!m->aborted) p2p_teardown(m);
+    if (!m->aborted) {
+      p2p_teardown(m);
+    } else {   // rank-local release, no collective step
+      for (auto* pool : {&m->p2p_ag, &m->p2p_rs}) {
+        for (SymSlot* s : *pool) {
+          sym_free_local(m, s->buf);
+          if (s->free_ev) cudaEventDestroy(s->free_ev);
+          delete s;
+        }
+        pool->clear();
+      }
+      sym_free_local(m, m->flags);
+    }
     for (auto* pool : {&m->ag_slots, &m->rs_slots})
       for (Slot* s : *pool) { s->a.release(); s->b.release(); if (s->free_ev) cudaEventDestroy(s->free_ev); delete s; }
     clear_presets(m);
@@ -759,6 +783,18 @@ fsdp_status_t fsdp_mesh_info(const fsdp_mesh_t* m, int32_t* W, int32_t* rank, in
     if (W) *W = m->W;
     if (rank) *rank = m->rank;
     if (dev) *dev = m->device;
+  });
+}
+
+fsdp_status_t fsdp_mesh_abort(fsdp_mesh_t* m) {
+  return guarded([&] {
+    if (!m) fail(FSDP_ERR_INVALID_ARGUMENT, "mesh is NULL");
+    m->aborted = true;
+    for (ncclComm_t* c : {&m->comm_ag, &m->comm_rs, &m->comm_rep, &m->comm_world})
+      if (*c) {
+        ncclCommAbort(*c);
+        *c = nullptr;
+      }
   });
 }
 
@@ -817,6 +853,11 @@ fsdp_status_t fsdp_mesh_synchronize(fsdp_mesh_t* m, int64_t timeout_ms) {
     CUDA_CHECK(cudaMemcpy(&err, m->d_err, sizeof(int), cudaMemcpyDeviceToHost));
     if (err) {
       CUDA_CHECK(cudaMemset(m->d_err, 0, sizeof(int)));
+      if ((err & 0xFF) == 2) {   // a P2P handshake gave up waiting for a peer
+        m->aborted = true;
+        fail(FSDP_ERR_TIMEOUT, "P2P handshake timed out waiting for shard rank " + std::to_string(err >> 8) +
+                                   " (a rank skipped or diverged from the collective call sequence); mesh aborted");
+      }
       fail(FSDP_ERR_NONFINITE, "non-finite fp8 amax seen by fsdp_precompute_fp8_scales (SPEC.md:38)");
     }
   });
@@ -948,7 +989,8 @@ fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* l) {
     l->t_push_bf16.release(); l->t_push_fp8.release(); l->t_pull.release(); l->t_stage_bf16.release();
     l->t_stage_fp32.release();
     if (l->gbuf) {
-      if (l->gbuf_sym) sym_free(m, l->gbuf->buf);   // collective
+      if (l->gbuf_sym && !m->aborted) sym_free(m, l->gbuf->buf);   // collective
+      else if (l->gbuf_sym) sym_free_local(m, l->gbuf->buf);
       else cudaFree(l->gbuf->buf.local);
       if (l->gbuf->free_ev) cudaEventDestroy(l->gbuf->free_ev);
       delete l->gbuf;
@@ -1112,7 +1154,7 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
       {
         ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_ag, 0);
         CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_AG_READY, ss->index), flag_local(m, FK_AG_READY, ss->index),
-                                             m->W, m->rank, epoch, m->s_ag));
+                                             m->W, m->rank, epoch, m->p2p_timeout_ns, m->d_err, m->s_ag));
         ph.done();
       }
       {
@@ -1125,7 +1167,7 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
       {
         ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_ag, 0);
         CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_AG_DONE, ss->index), flag_local(m, FK_AG_DONE, ss->index),
-                                             m->W, m->rank, epoch, m->s_ag));
+                                             m->W, m->rank, epoch, m->p2p_timeout_ns, m->d_err, m->s_ag));
         ph.done();
       }
       CUDA_CHECK(cudaEventRecord(l->ev_done, m->s_ag));
@@ -1327,7 +1369,7 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       {
         ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_rs, 0);
         CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_READY, ss->index), flag_local(m, FK_RS_READY, ss->index),
-                                             m->W, m->rank, epoch, m->s_rs));
+                                             m->W, m->rank, epoch, m->p2p_timeout_ns, m->d_err, m->s_rs));
         ph.done();
       }
       {
@@ -1341,7 +1383,7 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       {
         ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_rs, 0);
         CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_DONE, ss->index), flag_local(m, FK_RS_DONE, ss->index),
-                                             m->W, m->rank, epoch, m->s_rs));
+                                             m->W, m->rank, epoch, m->p2p_timeout_ns, m->d_err, m->s_rs));
         ph.done();
       }
       CUDA_CHECK(cudaEventRecord(ss->free_ev, m->s_rs));

@@ -31,8 +31,10 @@ struct FlagPtrs { unsigned long long* p[kMaxRanks]; };
 // Thread r < W: st.release.sys flags_remote.p[r][my_rank] = epoch (signal rank r), after a
 // system-scope fence; then every thread r < W spins (ld.acquire.sys) until
 // flags_local[r] >= epoch (rank r signalled me).  One CTA.
+// The spin gives up after timeout_ns and writes 2 | (peer << 8) to *err (FSDP_ERR_TIMEOUT).
 cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
-                               unsigned long long epoch, cudaStream_t st);
+                               unsigned long long epoch, unsigned long long timeout_ns, int* err,
+                               cudaStream_t st);
 
 // Push tiles: src = element offset into the fp32 shard, dst = byte offset into the arena,
 // n elements, kind TK_BF16 / TK_FP8 (scale = scales[param]).  Stores go to arena.p[d] for

@@ -20,14 +20,32 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 }
 
 // ------------------------------------------------------------------- handshake
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// The spin is bounded: after timeout_ns without the peer's flag (a rank that skipped the
+// collective, or died) the kernel records {kind=2 (timeout), peer} in *err and returns, so a
+// protocol error surfaces as FSDP_ERR_TIMEOUT from fsdp_mesh_synchronize instead of a hang.
 __global__ void k_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
-                              unsigned long long epoch) {
+                              unsigned long long epoch, unsigned long long timeout_ns, int* err) {
   const int r = threadIdx.x;
   __threadfence_system();   // order this GPU's earlier stores (previous kernels) before the flag
   __syncthreads();
-  if (r < W) st_release_sys(remote.p[r] + rank, epoch);
+#pragma unroll
+  for (int i = 0; i < kMaxRanks; ++i)   // constant indices: remote.p stays in param space
+    if (i == r && i < W) st_release_sys(remote.p[i] + rank, epoch);
   if (r < W) {
-    while (ld_acquire_sys(local + r) < epoch) __nanosleep(64);
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_sys(local + r) < epoch) {
+      __nanosleep(64);
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        atomicExch(err, 2 | (r << 8));
+        break;
+      }
+    }
   }
   __syncthreads();
   __threadfence_system();
@@ -605,8 +623,9 @@ cudaError_t launch_pull_w(const Tile* tiles, int ntiles, PeerPtrs st, float* gra
 }  // namespace
 
 cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
-                               unsigned long long epoch, cudaStream_t st) {
-  k_signal_wait<<<1, 32, 0, st>>>(remote, local, W, rank, epoch);
+                               unsigned long long epoch, unsigned long long timeout_ns, int* err,
+                               cudaStream_t st) {
+  k_signal_wait<<<1, 32, 0, st>>>(remote, local, W, rank, epoch, timeout_ns, err);
   return cudaGetLastError();
 }
 

@@ -159,6 +159,11 @@ class Mesh:
     def synchronize(self, timeout_ms: int = 0):
         call("fsdp_mesh_synchronize", self.handle, int(timeout_ms))
 
+    def abort(self):
+        """Rank-local: abort the communicators; layers/mesh can then be destroyed without
+        any collective step (after FSDP_ERR_TIMEOUT / FSDP_ERR_NCCL on any rank)."""
+        call("fsdp_mesh_abort", self.handle)
+
     def profile_enable(self, on: bool = True):
         call("fsdp_profile_enable", self.handle, int(bool(on)))
 

@@ -46,9 +46,41 @@ def main():
     mesh.destroy()
     for Ws in sorted({d for d in (1, 2, W // 2) if 1 <= d < W and W % d == 0}):
         run_hsdp_checks(W, rank, local, Ws)
+    run_fault_injection(W, rank, local)
     dist.barrier()
     dist.destroy_process_group()
     print(f"RANK {rank}/{W} OK (algos {algos}, hsdp)", flush=True)
+
+
+def run_fault_injection(W, rank, local):
+    """SPEC.md:190 idea ("rank never calls the collective -> report"): the last rank skips a
+    reduce-scatter; every other rank's P2P handshake gives up after the configured timeout
+    and fsdp_mesh_synchronize reports FSDP_ERR_TIMEOUT naming a peer, instead of hanging."""
+    os.environ["FSDP_B200_P2P_TIMEOUT_MS"] = "2000"
+    try:
+        mesh = F.Mesh.from_process_group(device=local)
+    finally:
+        del os.environ["FSDP_B200_P2P_TIMEOUT_MS"]
+    if mesh.algo != "p2p":
+        mesh.destroy()
+        return
+    u = synth.model_units("toy")[0]
+    shapes = [s for _, s, _ in u]
+    layer = F.fsdp_shard(mesh, None, [False] * len(shapes), shapes=shapes)
+    grads = [torch.zeros(s, dtype=torch.bfloat16, device="cuda") for s in shapes]
+    if rank != W - 1:
+        F.reduce_scatter_grads(layer, grads)
+        F.fsdp_wait_reduce_scatter(layer)
+        try:
+            mesh.synchronize(120000)
+            raise AssertionError("the missing rank was not detected")
+        except F.FsdpError as e:
+            assert e.status_name == "FSDP_ERR_TIMEOUT", e
+            assert "timed out" in str(e)
+    dist.barrier()
+    mesh.abort()
+    mesh.destroy()
+    print(f"rank {rank}/{W} fault injection (rank {W - 1} skips a reduce-scatter): OK", flush=True)
 
 
 def run_hsdp_checks(W, rank, local, Ws):

@@ -68,6 +68,11 @@ def run_fault_injection(W, rank, local):
     shapes = [s for _, s, _ in u]
     layer = F.fsdp_shard(mesh, None, [False] * len(shapes), shapes=shapes)
     grads = [torch.zeros(s, dtype=torch.bfloat16, device="cuda") for s in shapes]
+    for _ in range(2):   # both pooled staging slots get allocated (collectively) by good rounds
+        F.reduce_scatter_grads(layer, grads)
+        F.fsdp_wait_reduce_scatter(layer)
+    mesh.synchronize(120000)
+    dist.barrier()
     if rank != W - 1:
         F.reduce_scatter_grads(layer, grads)
         F.fsdp_wait_reduce_scatter(layer)

@@ -257,7 +257,9 @@ fsdp_status_t fsdp_fp8_scales(const fsdp_layer_t* layer, const float** scales_de
  * rank's slot), the all-gather, and copy-out (K4) into per-parameter full tensors.
  * param_dtype: FSDP_BFLOAT16 or FSDP_FLOAT8_E4M3FN (eligible params in
  * e4m3fn with per-tensor scale, others bf16).  fp8_scales_dev: P device floats, or NULL
- * to use the layer's precomputed scales.  State: SHARDED -> UNSHARDING. */
+ * to use the layer's precomputed scales.  State: SHARDED -> UNSHARDING; on a layer that is
+ * already unsharded (reshard_after_forward=False, the kept last block) it is a
+ * no-op for the same param_dtype and FSDP_ERR_STATE for another. */
 fsdp_status_t fsdp_unshard(fsdp_layer_t* layer, fsdp_dtype_t param_dtype,
                            const float* fp8_scales_dev, void* compute);
 /* Makes `compute` wait for the unshard.  State: UNSHARDING -> UNSHARDED. */

@@ -1135,8 +1135,13 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
   return guarded([&] {
     check_layer(l);
     fsdp_mesh* m = l->mesh;
-    if (l->state != SHARDED) fail(FSDP_ERR_STATE, "layer is already unsharded (reshard it first)");
     if (dt != FSDP_BFLOAT16 && dt != FSDP_FLOAT8_E4M3FN) fail(FSDP_ERR_DTYPE, "param_dtype must be BFLOAT16 or FLOAT8_E4M3FN");
+    if (l->state != SHARDED) {
+      // already unsharded (reshard_after_forward=False / the kept last block): a
+      // no-op like FSDP2's unshard(), as long as the dtype matches
+      if (dt != l->ushard_dtype) fail(FSDP_ERR_STATE, "layer is unsharded in another dtype (reshard it first)");
+      return;
+    }
     if (m->local && m->W > 1) fail(FSDP_ERR_UNAVAILABLE, "local mesh with world_size > 1 has no communicator");
     const bool fp8 = dt == FSDP_FLOAT8_E4M3FN;
     if (fp8 && !scales) scales = m->reg_scale + l->reg_base;

@@ -268,8 +268,9 @@ def test_state_errors_and_nonfinite():
             layer.unsharded_param(0)
         assert e.value.status_name == "FSDP_ERR_STATE"
         F.fsdp_unshard(layer)
+        F.fsdp_unshard(layer)               # already unsharded, same dtype: no-op (FSDP2 unshard())
         with pytest.raises(F.FsdpError) as e:
-            F.fsdp_unshard(layer)
+            F.fsdp_unshard(layer, torch.float8_e4m3fn)   # another dtype while unsharded
         assert e.value.status_name == "FSDP_ERR_STATE"
         with pytest.raises(F.FsdpError):
             layer.unsharded_param(0)        # before wait_unshard

@@ -42,6 +42,13 @@ def main():
     for algo in algos:
         mesh.set_algo(algo)
         run_checks(mesh, W, rank, local, algo)
+        # training steps vs the single-device run: bit-exact under P2P (same
+        # ascending-rank fp32 order as the reference mean), fp32 tolerance under NCCL
+        import toy_train
+        ref = toy_train.reference_steps(3, W)
+        got, metas = toy_train.fsdp_steps(F, mesh, rank, 3)
+        toy_train.compare(ref, got, metas, exact=(algo == "p2p"))
+        print(f"rank {rank}/{W} algo={algo}: 3 training steps match the single-device run", flush=True)
     mesh.synchronize(120000)
     mesh.destroy()
     for Ws in sorted({d for d in (1, 2, W // 2) if 1 <= d < W and W % d == 0}):

@@ -252,6 +252,32 @@ class Layer:
             out.append(_view(ptr.value, self.shapes[p], dtype, self.device))
         return out
 
+    def sharded_state_dict(self, names: Optional[Sequence[str]] = None) -> dict:
+        """Per-param local shards with their Shard(0) placement, without any communication
+        ("allowing sharded state dict to be represented by DTensor without any
+        communication"): {name: {"local": fp32 view (row_count, *shape[1:]), "global_shape",
+        "row_begin", "world_size", "rank"}}.  The views alias the optimizer-visible shard."""
+        names = names or [f"p{p}" for p in range(self.P)]
+        out = {}
+        for p, name in enumerate(names):
+            m = self.metas[p]
+            out[name] = {"local": self.sharded_param(p), "global_shape": self.shapes[p],
+                         "row_begin": m["row_begin"], "world_size": self.mesh.shard_size
+                         if hasattr(self.mesh, "shard_size") else self.mesh.world_size,
+                         "rank": getattr(self.mesh, "shard_rank", self.mesh.rank)}
+        return out
+
+    def load_sharded_state_dict(self, state: dict, names: Optional[Sequence[str]] = None):
+        """Copies local shards produced by sharded_state_dict (same world size and layout)
+        back into the layer's fp32 shard; rows are checked against this rank's placement."""
+        names = names or [f"p{p}" for p in range(self.P)]
+        for p, name in enumerate(names):
+            ent = state[name]
+            m = self.metas[p]
+            if tuple(ent["global_shape"]) != self.shapes[p] or int(ent["row_begin"]) != m["row_begin"]:
+                raise ValueError(f"{name}: placement does not match this rank's Shard(0) layout")
+            self.sharded_param(p).copy_(torch.as_tensor(ent["local"]).to(self.sharded_param(p).device))
+
     def fp8_scales(self):
         s = C.c_void_p()
         a = C.c_void_p()

@@ -1,0 +1,319 @@
+// Internal declarations shared by the C-ABI translation units (capi_*.cpp): error
+// handling, RAII helpers, buffer pools, symmetric (CUDA IPC) buffers, and the mesh /
+// layer objects behind the opaque handles of include/fsdp_b200.h.  Not installed.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "fsdp_b200.h"
+#include "kernels.h"
+#include "layout.h"
+#include "p2p.h"
+
+namespace fsdpc {
+
+using fsdpk::Tile;
+using fsdpl::Layout;
+
+
+extern thread_local std::string g_last_error;
+
+struct Error {
+  fsdp_status_t st;
+  std::string msg;
+};
+
+[[noreturn]] inline void fail(fsdp_status_t st, const std::string& msg) { throw Error{st, msg}; }
+
+#define CUDA_CHECK(x)                                                                        \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      fail(e_ == cudaErrorMemoryAllocation ? FSDP_ERR_OUT_OF_MEMORY : FSDP_ERR_CUDA,         \
+           std::string(#x) + ": " + cudaGetErrorString(e_));                                 \
+  } while (0)
+
+#define NCCL_CHECK(x)                                                                        \
+  do {                                                                                       \
+    ncclResult_t r_ = (x);                                                                   \
+    if (r_ != ncclSuccess) fail(FSDP_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+template <class F>
+fsdp_status_t guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return FSDP_OK;
+  } catch (const Error& e) {
+    g_last_error = e.msg;
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host out of memory";
+    return FSDP_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return FSDP_ERR_CUDA;
+  }
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) CUDA_CHECK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) CUDA_CHECK(cudaFree(p));
+    p = nullptr;
+    cap = 0;
+    // +64 B slack: the misaligned 16-byte loads of K4/K5 may touch the aligned block
+    // holding the last byte
+    CUDA_CHECK(cudaMalloc(&p, bytes + 64));
+    cap = bytes;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct DevTiles {
+  Tile* d = nullptr;
+  int n = 0;
+  std::vector<int> first;   // per-param first tile (param-major tables)
+  void upload(const std::vector<Tile>& h) {
+    release();
+    n = (int)h.size();
+    if (n) {
+      CUDA_CHECK(cudaMalloc(&d, sizeof(Tile) * h.size()));
+      CUDA_CHECK(cudaMemcpy(d, h.data(), sizeof(Tile) * h.size(), cudaMemcpyHostToDevice));
+    }
+  }
+  void release() {
+    if (d) cudaFree(d);
+    d = nullptr;
+    n = 0;
+  }
+};
+
+struct Slot {             // one pooled buffer set
+  DevBuf a, b;            // AG: a = [W][slot] buffer, b = unsharded arena
+                          // RS: a = [W][S] reduce-scatter input, b = staging output [S]
+  cudaEvent_t free_ev = nullptr;
+  bool in_use = false;
+  bool ever_used = false;
+  uint64_t last_use = 0;
+};
+
+struct ProfRec {
+  int kind;
+  cudaEvent_t a, b;
+  int64_t bytes;
+};
+
+// A symmetric buffer: same size on every rank, peers' copies mapped with CUDA IPC.
+struct SymBuf {
+  void* local = nullptr;
+  size_t bytes = 0;
+  std::vector<void*> peers;   // peers[r] = rank r's buffer in this process (peers[rank] = local)
+};
+
+// A pooled symmetric slot of the P2P path (unsharded arena, or grad staging).  Slots are
+// chosen deterministically (same choice on every rank) and each use bumps the epoch the
+// cross-GPU flags are compared against.
+struct SymSlot {
+  SymBuf buf;
+  cudaEvent_t free_ev = nullptr;
+  bool in_use = false;
+  bool ever_used = false;
+  uint64_t epoch = 0;
+  int index = 0;
+};
+
+constexpr int kFlagSlots = 512;  // flag slots per kind: pooled slots first, then layer grad buffers
+constexpr int kPoolSlots = 64;   // max pooled symmetric slots (arenas / staging) per pool
+constexpr int kHistMax = 64;     // max delayed-scaling amax history length
+enum FlagKind { FK_AG_READY = 0, FK_AG_DONE = 1, FK_RS_READY = 2, FK_RS_DONE = 3, FK_NUM = 4 };
+
+enum LayerState { SHARDED = 0, UNSHARDING = 1, UNSHARDED = 2 };
+
+
+}  // namespace fsdpc
+
+// the opaque handle types of the C ABI are global structs built from the internal types
+using namespace fsdpc;  // NOLINT (internal header, included only by capi_*.cpp)
+
+struct fsdp_layer;
+
+struct fsdp_mesh {
+  int W = 1, rank = 0, device = 0;   // shard group size / shard rank
+  int R = 1, rep = 0;                // HSDP replicate group size / replica index
+  bool local = true;
+  ncclComm_t comm_ag = nullptr, comm_rs = nullptr;
+  ncclComm_t comm_world = nullptr, comm_rep = nullptr;   // HSDP only
+  cudaStream_t s_cin = nullptr, s_ag = nullptr, s_cout = nullptr, s_rsc = nullptr, s_rs = nullptr;
+  fsdpk::LaunchCfg cfg{};
+  std::vector<Slot*> ag_slots, rs_slots;
+  uint64_t use_seq = 0;
+  // fp8 scale registry: one entry per param of every layer (contiguous per layer)
+  int reg_size = 0, reg_cap = 0;
+  uint32_t* reg_acc = nullptr;
+  float* reg_amax = nullptr;
+  float* reg_scale = nullptr;
+  uint8_t* reg_elig = nullptr;
+  float* reg_hist = nullptr;      // delayed scaling: [reg_cap][kHistMax] amax history
+  int32_t* reg_pos = nullptr;
+  uint8_t* reg_hinit = nullptr;
+  int hist_len = 0;               // fixed at the first delayed precompute
+  int* d_err = nullptr;
+  cudaEvent_t ev_pre_call = nullptr, ev_pre_done = nullptr;
+  std::vector<fsdp_layer*> layers;
+  // precompute cache: layer list -> (amax tiles, finalize index list)
+  struct PreSet {
+    std::vector<fsdp_layer*> layers;
+    DevTiles tiles;
+    int32_t* idx = nullptr;
+    int nidx = 0;
+    int64_t bytes = 0;
+  };
+  std::vector<PreSet*> presets;
+  // profiling
+  bool prof = false;
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  fsdp_profile_t prof_acc{};
+  bool aborted = false;
+  // P2P (fused peer-memory) path
+  int algo = FSDP_ALGO_NCCL;
+  bool p2p_ok = false;
+  SymBuf flags;                              // uint64 [FK_NUM][kFlagSlots][kMaxRanks]
+  std::vector<SymSlot*> p2p_ag, p2p_rs;      // unsharded arenas, grad staging
+  uint64_t rs_rr = 0;                        // round robin over staging slots
+  int gbuf_seq = 0;                          // flag slots of layer grad buffers: kPoolSlots + seq
+  unsigned long long p2p_timeout_ns = 60ull * 1000 * 1000 * 1000;   // handshake spin bound
+  int* d_barrier = nullptr;
+};
+
+struct fsdp_layer {
+  fsdp_mesh* mesh = nullptr;
+  int P = 0;
+  std::vector<fsdp_param_desc_t> descs;
+  Layout L;
+  float* shard = nullptr;
+  float* grad = nullptr;
+  int reg_base = 0;
+  int32_t* d_idx_local = nullptr;   // 0..P-1 (stage fp8 scale)
+  DevTiles t_cin_fp8, t_cout_bf16, t_cout_fp8, t_rsin;
+  int64_t bytes_cin_fp8 = 0, bytes_cout_bf16 = 0, bytes_cout_fp8 = 0;
+  int64_t grad_numel_total = 0;
+  // unshard state
+  int state = SHARDED;
+  Slot* slot = nullptr;
+  fsdp_dtype_t ushard_dtype = FSDP_BFLOAT16;
+  cudaEvent_t ev_call = nullptr, ev_cin = nullptr, ev_ag = nullptr, ev_done = nullptr;
+  // reduce-scatter state
+  bool rs_pending = false;
+  cudaEvent_t ev_rcall = nullptr, ev_k5 = nullptr, ev_rs_done = nullptr;
+  // P2P path
+  DevTiles t_push_bf16, t_push_fp8, t_pull, t_stage_bf16, t_stage_fp32;
+  std::vector<int64_t> stg_off_el;   // full-grad staging: param p at element offset (128-aligned)
+  int64_t stg_elems = 0;
+  int64_t push_bytes_bf16 = 0, push_bytes_fp8 = 0, pull_elems = 0;
+  int64_t local_push_bf16 = 0, local_push_fp8 = 0;
+  SymSlot* p2p_slot = nullptr;       // arena of the current P2P unshard
+  SymSlot* gbuf = nullptr;           // zero-copy full-grad buffer (fsdp_full_grad_buffer)
+  bool gbuf_sym = false;
+  fsdp_dtype_t gbuf_dtype = FSDP_BFLOAT16;
+  void* arena_base = nullptr;        // base of the unsharded tensors (either path)
+};
+
+
+namespace fsdpc {
+
+// ---- helpers (capi_util.cpp)
+cudaEvent_t new_event(bool timing = false);
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+void prof_collect(fsdp_mesh* m);
+Slot* acquire_slot(fsdp_mesh* m, std::vector<Slot*>& pool, size_t a_bytes, size_t b_bytes, int min_slots);
+void release_slot(Slot* s, cudaStream_t last_user);
+void check_mesh(const fsdp_mesh* m);
+void check_layer(const fsdp_layer* l);
+void check_param(const fsdp_layer* l, int p);
+bool comm_ready(const fsdp_mesh* m);
+void ensure_registry(fsdp_mesh* m, int need);
+void clear_presets(fsdp_mesh* m);
+int64_t dtype_size(fsdp_dtype_t d);
+void mesh_barrier(fsdp_mesh* m);
+bool mesh_all_ok(fsdp_mesh* m, bool ok);
+void sym_free_local(fsdp_mesh* m, SymBuf& b);
+void sym_free(fsdp_mesh* m, SymBuf& b);
+bool sym_alloc(fsdp_mesh* m, SymBuf& b, size_t bytes);
+fsdpp::FlagPtrs flag_remote(fsdp_mesh* m, int kind, int slot);
+unsigned long long* flag_local(fsdp_mesh* m, int kind, int slot);
+SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t bytes, int prefer = -1);
+fsdpp::PeerPtrs peer_ptrs(const fsdp_mesh* m, const SymBuf& b);
+void p2p_teardown(fsdp_mesh* m);
+void launch_copy_out_all(fsdp_layer* l, bool fp8, const void* ag, void* const* outs, cudaStream_t st);
+void launch_rs_copy_in_all(fsdp_layer* l, const void* const* grads, bool grad_bf16, void* rs_in, bool out_bf16,
+                           bool mean, cudaStream_t st);
+int64_t cin_bytes(const fsdp_layer* l, bool fp8);
+int64_t slot_bytes(const fsdp_layer* l, bool fp8);
+void do_copy_in(fsdp_layer* l, bool fp8, const float* scales, void* dst, cudaStream_t st);
+void validate_grads(const fsdp_layer* l, const void* const* grads, fsdp_dtype_t gd, fsdp_dtype_t rd);
+
+
+// ---- profiling helpers
+struct ProfScope {
+  fsdp_mesh* m;
+  int kind;
+  cudaStream_t st;
+  int64_t bytes;
+  cudaEvent_t a = nullptr;
+  ProfScope(fsdp_mesh* m_, int k, cudaStream_t s, int64_t b) : m(m_), kind(k), st(s), bytes(b) {
+    if (!m->prof) return;
+    a = take();
+    CUDA_CHECK(cudaEventRecord(a, st));
+  }
+  cudaEvent_t take() {
+    if (!m->ev_pool.empty()) {
+      cudaEvent_t e = m->ev_pool.back();
+      m->ev_pool.pop_back();
+      return e;
+    }
+    return new_event(true);
+  }
+  void done() {
+    if (!m->prof || !a) return;
+    cudaEvent_t b = take();
+    CUDA_CHECK(cudaEventRecord(b, st));
+    m->prof_recs.push_back(ProfRec{kind, a, b, bytes});
+    a = nullptr;
+  }
+};
+
+
+
+}  // namespace fsdpc

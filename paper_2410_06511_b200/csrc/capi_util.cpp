@@ -1,0 +1,305 @@
+// Internal helpers of the C ABI: pools, registry, symmetric memory, launch wrappers.
+#include "capi_internal.h"
+
+namespace fsdpc {
+
+thread_local std::string g_last_error;
+
+
+cudaEvent_t new_event(bool timing) {
+  cudaEvent_t e;
+  CUDA_CHECK(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+  return e;
+}
+
+
+// ---- profiling helpers
+
+void prof_collect(fsdp_mesh* m) {
+  for (auto& r : m->prof_recs) {
+    CUDA_CHECK(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+    m->prof_acc.launches[r.kind] += 1;
+    m->prof_acc.total_ms[r.kind] += ms;
+    m->prof_acc.bytes[r.kind] += r.bytes;
+    m->ev_pool.push_back(r.a);
+    m->ev_pool.push_back(r.b);
+  }
+  m->prof_recs.clear();
+}
+
+// ---- pools
+Slot* acquire_slot(fsdp_mesh* m, std::vector<Slot*>& pool, size_t a_bytes, size_t b_bytes, int min_slots) {
+  Slot* best = nullptr;
+  int n_free = 0;
+  for (Slot* s : pool) {
+    if (s->in_use) continue;
+    ++n_free;
+    if (!best) { best = s; continue; }
+    const bool s_done = !s->ever_used || cudaEventQuery(s->free_ev) == cudaSuccess;
+    const bool b_done = !best->ever_used || cudaEventQuery(best->free_ev) == cudaSuccess;
+    if (s_done != b_done) { if (s_done) best = s; continue; }
+    if (s->last_use < best->last_use) best = s;
+  }
+  cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not sticky; clear it anyway
+  const bool best_busy = best && best->ever_used && cudaEventQuery(best->free_ev) != cudaSuccess;
+  cudaGetLastError();
+  if (!best || ((int)pool.size() < min_slots && best_busy)) {
+    Slot* s = new Slot();
+    s->free_ev = new_event();
+    pool.push_back(s);
+    best = s;
+  }
+  if (best->a.cap < a_bytes || best->b.cap < b_bytes) {
+    if (best->ever_used) CUDA_CHECK(cudaEventSynchronize(best->free_ev));   // growth: setup-time only
+    best->a.ensure(a_bytes);
+    best->b.ensure(b_bytes);
+  }
+  best->in_use = true;
+  best->last_use = ++m->use_seq;
+  return best;
+}
+
+void release_slot(Slot* s, cudaStream_t last_user) {
+  CUDA_CHECK(cudaEventRecord(s->free_ev, last_user));
+  s->ever_used = true;
+  s->in_use = false;
+}
+
+void check_mesh(const fsdp_mesh* m) {
+  if (!m) fail(FSDP_ERR_INVALID_ARGUMENT, "mesh is NULL");
+  if (m->aborted) fail(FSDP_ERR_STATE, "mesh was aborted after a NCCL error/timeout");
+}
+void check_layer(const fsdp_layer* l) {
+  if (!l) fail(FSDP_ERR_INVALID_ARGUMENT, "layer is NULL");
+  check_mesh(l->mesh);
+}
+void check_param(const fsdp_layer* l, int p) {
+  if (p < 0 || p >= l->P) fail(FSDP_ERR_INVALID_ARGUMENT, "param index out of range");
+}
+
+bool comm_ready(const fsdp_mesh* m) { return !m->local && m->W > 1; }
+
+void ensure_registry(fsdp_mesh* m, int need) {
+  if (need <= m->reg_cap) return;
+  int cap = std::max(need, std::max(64, 2 * m->reg_cap));
+  uint32_t* acc;
+  float *amax, *scale;
+  uint8_t* elig;
+  CUDA_CHECK(cudaMalloc(&acc, sizeof(uint32_t) * cap));
+  CUDA_CHECK(cudaMalloc(&amax, sizeof(float) * cap));
+  CUDA_CHECK(cudaMalloc(&scale, sizeof(float) * cap));
+  CUDA_CHECK(cudaMalloc(&elig, cap));
+  CUDA_CHECK(cudaMemset(acc, 0, sizeof(uint32_t) * cap));
+  CUDA_CHECK(cudaMemset(amax, 0, sizeof(float) * cap));
+  CUDA_CHECK(cudaMemset(scale, 0, sizeof(float) * cap));
+  CUDA_CHECK(cudaMemset(elig, 0, cap));
+  if (m->reg_size) {
+    CUDA_CHECK(cudaDeviceSynchronize());
+    CUDA_CHECK(cudaMemcpy(acc, m->reg_acc, sizeof(uint32_t) * m->reg_size, cudaMemcpyDeviceToDevice));
+    CUDA_CHECK(cudaMemcpy(amax, m->reg_amax, sizeof(float) * m->reg_size, cudaMemcpyDeviceToDevice));
+    CUDA_CHECK(cudaMemcpy(scale, m->reg_scale, sizeof(float) * m->reg_size, cudaMemcpyDeviceToDevice));
+    CUDA_CHECK(cudaMemcpy(elig, m->reg_elig, m->reg_size, cudaMemcpyDeviceToDevice));
+  }
+  // delayed-scaling state: amax history [cap][kHistMax], ring position, initialised flag
+  float* hist;
+  int32_t* pos;
+  uint8_t* hinit;
+  CUDA_CHECK(cudaMalloc(&hist, sizeof(float) * (size_t)cap * kHistMax));
+  CUDA_CHECK(cudaMalloc(&pos, sizeof(int32_t) * cap));
+  CUDA_CHECK(cudaMalloc(&hinit, cap));
+  CUDA_CHECK(cudaMemset(hist, 0, sizeof(float) * (size_t)cap * kHistMax));
+  CUDA_CHECK(cudaMemset(pos, 0, sizeof(int32_t) * cap));
+  CUDA_CHECK(cudaMemset(hinit, 0, cap));
+  if (m->reg_size) {
+    CUDA_CHECK(cudaMemcpy(hist, m->reg_hist, sizeof(float) * (size_t)m->reg_size * kHistMax, cudaMemcpyDeviceToDevice));
+    CUDA_CHECK(cudaMemcpy(pos, m->reg_pos, sizeof(int32_t) * m->reg_size, cudaMemcpyDeviceToDevice));
+    CUDA_CHECK(cudaMemcpy(hinit, m->reg_hinit, m->reg_size, cudaMemcpyDeviceToDevice));
+  }
+  cudaFree(m->reg_acc); cudaFree(m->reg_amax); cudaFree(m->reg_scale); cudaFree(m->reg_elig);
+  cudaFree(m->reg_hist); cudaFree(m->reg_pos); cudaFree(m->reg_hinit);
+  m->reg_acc = acc; m->reg_amax = amax; m->reg_scale = scale; m->reg_elig = elig;
+  m->reg_hist = hist; m->reg_pos = pos; m->reg_hinit = hinit;
+  m->reg_cap = cap;
+  for (auto* ps : m->presets) { ps->tiles.release(); cudaFree(ps->idx); delete ps; }
+  m->presets.clear();
+}
+
+void clear_presets(fsdp_mesh* m) {
+  for (auto* ps : m->presets) { ps->tiles.release(); cudaFree(ps->idx); delete ps; }
+  m->presets.clear();
+}
+
+int64_t dtype_size(fsdp_dtype_t d) { return d == FSDP_FLOAT32 ? 4 : (d == FSDP_BFLOAT16 ? 2 : 1); }
+
+// ---- symmetric memory over CUDA IPC (collective helpers; every rank calls them in the
+// same order, which the deterministic FSDP call sequence guarantees)
+void mesh_barrier(fsdp_mesh* m) {
+  NCCL_CHECK(ncclAllReduce(m->d_barrier, m->d_barrier, 1, ncclInt32, ncclSum, m->comm_ag, m->s_ag));
+  CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
+}
+
+// all ranks agree that `ok` holds everywhere
+bool mesh_all_ok(fsdp_mesh* m, bool ok) {
+  int v = ok ? 1 : 0;
+  CUDA_CHECK(cudaMemcpy(m->d_barrier, &v, sizeof(int), cudaMemcpyHostToDevice));
+  NCCL_CHECK(ncclAllReduce(m->d_barrier, m->d_barrier, 1, ncclInt32, ncclMin, m->comm_ag, m->s_ag));
+  CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
+  CUDA_CHECK(cudaMemcpy(&v, m->d_barrier, sizeof(int), cudaMemcpyDeviceToHost));
+  return v == 1;
+}
+
+// Rank-local (aborted mesh): unmap the peers' copies and free the local one, no barrier.
+void sym_free_local(fsdp_mesh* m, SymBuf& b) {
+  for (int r = 0; r < m->W; ++r)
+    if (r != m->rank && r < (int)b.peers.size() && b.peers[r]) cudaIpcCloseMemHandle(b.peers[r]);
+  if (b.local) cudaFree(b.local);
+  cudaGetLastError();
+  b = SymBuf();
+}
+
+// Collective: unmap the peers' copies, wait until every rank did, then free the local one.
+void sym_free(fsdp_mesh* m, SymBuf& b) {
+  for (int r = 0; r < m->W; ++r)
+    if (r != m->rank && r < (int)b.peers.size() && b.peers[r]) cudaIpcCloseMemHandle(b.peers[r]);
+  cudaGetLastError();
+  mesh_barrier(m);
+  if (b.local) cudaFree(b.local);
+  b = SymBuf();
+}
+
+// Returns false (on every rank) if any rank failed to allocate or map.
+bool sym_alloc(fsdp_mesh* m, SymBuf& b, size_t bytes) {
+  bool ok = cudaMalloc(&b.local, bytes + 256) == cudaSuccess;
+  cudaIpcMemHandle_t h{};
+  if (ok) ok = cudaMemset(b.local, 0, bytes + 256) == cudaSuccess;
+  if (ok) ok = cudaIpcGetMemHandle(&h, b.local) == cudaSuccess;
+  cudaGetLastError();
+  uint8_t* d = nullptr;
+  CUDA_CHECK(cudaMalloc(&d, sizeof(h) * m->W));
+  CUDA_CHECK(cudaMemcpy(d + sizeof(h) * m->rank, &h, sizeof(h), cudaMemcpyHostToDevice));
+  NCCL_CHECK(ncclAllGather(d + sizeof(h) * m->rank, d, sizeof(h), ncclUint8, m->comm_ag, m->s_ag));
+  CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
+  std::vector<cudaIpcMemHandle_t> hs(m->W);
+  CUDA_CHECK(cudaMemcpy(hs.data(), d, sizeof(h) * m->W, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  b.peers.assign(m->W, nullptr);
+  b.bytes = bytes;
+  if (ok) {
+    b.peers[m->rank] = b.local;
+    for (int r = 0; r < m->W && ok; ++r) {
+      if (r == m->rank) continue;
+      void* p = nullptr;
+      ok = cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      cudaGetLastError();
+      b.peers[r] = ok ? p : nullptr;
+    }
+  }
+  if (!mesh_all_ok(m, ok)) {
+    sym_free(m, b);
+    return false;
+  }
+  return true;
+}
+
+fsdpp::FlagPtrs flag_remote(fsdp_mesh* m, int kind, int slot) {
+  fsdpp::FlagPtrs f{};
+  const size_t off = ((size_t)kind * kFlagSlots + slot) * fsdpp::kMaxRanks;
+  for (int r = 0; r < m->W; ++r) f.p[r] = (unsigned long long*)m->flags.peers[r] + off;
+  return f;
+}
+unsigned long long* flag_local(fsdp_mesh* m, int kind, int slot) {
+  return (unsigned long long*)m->flags.local + ((size_t)kind * kFlagSlots + slot) * fsdpp::kMaxRanks;
+}
+
+// Deterministic choice: the lowest-index free slot (same on every rank, since in_use
+// depends only on the call sequence); grows / creates slots collectively.
+SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t bytes, int prefer) {
+  SymSlot* s = nullptr;
+  while (prefer >= (int)pool.size() && (int)pool.size() < kPoolSlots) {
+    SymSlot* n = new SymSlot();
+    n->free_ev = new_event();
+    n->index = (int)pool.size();
+    pool.push_back(n);
+  }
+  if (prefer >= 0 && prefer < (int)pool.size() && !pool[prefer]->in_use) s = pool[prefer];
+  for (size_t i = 0; !s && i < pool.size(); ++i)
+    if (!pool[i]->in_use) s = pool[i];
+  if (!s) {
+    if ((int)pool.size() >= kPoolSlots) fail(FSDP_ERR_STATE, "too many unsharded layers / pending reduce-scatters at once");
+    s = new SymSlot();
+    s->free_ev = new_event();
+    s->index = (int)pool.size();
+    pool.push_back(s);
+  }
+  if (s->buf.bytes < bytes) {   // collective (re)allocation; setup-time only
+    if (s->ever_used) CUDA_CHECK(cudaEventSynchronize(s->free_ev));
+    CUDA_CHECK(cudaDeviceSynchronize());
+    mesh_barrier(m);
+    if (s->buf.local || !s->buf.peers.empty()) sym_free(m, s->buf);
+    if (!sym_alloc(m, s->buf, bytes)) fail(FSDP_ERR_OUT_OF_MEMORY, "symmetric buffer allocation/mapping failed");
+  }
+  s->in_use = true;
+  return s;
+}
+
+fsdpp::PeerPtrs peer_ptrs(const fsdp_mesh* m, const SymBuf& b) {
+  fsdpp::PeerPtrs p{};
+  for (int r = 0; r < m->W; ++r) p.p[r] = (uint8_t*)b.peers[r];
+  return p;
+}
+
+void p2p_teardown(fsdp_mesh* m) {
+  if (!m->p2p_ok) return;
+  CUDA_CHECK(cudaDeviceSynchronize());
+  mesh_barrier(m);   // every rank's kernels are done with every peer buffer
+  for (auto* pool : {&m->p2p_ag, &m->p2p_rs}) {
+    for (SymSlot* s : *pool) {
+      if (s->buf.local || !s->buf.peers.empty()) sym_free(m, s->buf);
+      if (s->free_ev) cudaEventDestroy(s->free_ev);
+      delete s;
+    }
+    pool->clear();
+  }
+  sym_free(m, m->flags);
+  m->p2p_ok = false;
+}
+
+// ---- K4 / K5 launches (fsdp_shard enforces P <= kMaxPtrs, one pointer array per launch)
+void launch_copy_out_all(fsdp_layer* l, bool fp8, const void* ag, void* const* outs, cudaStream_t st) {
+  const DevTiles& T = fp8 ? l->t_cout_fp8 : l->t_cout_bf16;
+  fsdpk::PtrArray pa{};
+  for (int p = 0; p < l->P; ++p) pa.p[p] = outs[p];
+  CUDA_CHECK(fsdpk::launch_copy_out(T.d, T.n, ag, pa, l->mesh->cfg, st));
+}
+
+void launch_rs_copy_in_all(fsdp_layer* l, const void* const* grads, bool grad_bf16, void* rs_in, bool out_bf16,
+                           bool mean, cudaStream_t st) {
+  fsdpk::PtrArray pa{};
+  for (int p = 0; p < l->P; ++p) pa.p[p] = grads[p];
+  CUDA_CHECK(fsdpk::launch_rs_copy_in(l->t_rsin.d, l->t_rsin.n, pa, grad_bf16, rs_in, out_bf16, mean,
+                                      l->mesh->W * l->mesh->R,
+                                      l->mesh->cfg, st));
+}
+
+int64_t cin_bytes(const fsdp_layer* l, bool fp8) { return fp8 ? l->bytes_cin_fp8 : 6 * l->L.S; }
+int64_t slot_bytes(const fsdp_layer* l, bool fp8) { return fp8 ? l->L.S_bytes_fp8 : 2 * l->L.S; }
+
+void do_copy_in(fsdp_layer* l, bool fp8, const float* scales, void* dst, cudaStream_t st) {
+  fsdp_mesh* m = l->mesh;
+  ProfScope ps(m, FSDP_PROF_COPY_IN, st, cin_bytes(l, fp8));
+  if (fp8) CUDA_CHECK(fsdpk::launch_copy_in_fp8(l->t_cin_fp8.d, l->t_cin_fp8.n, l->shard, dst, scales, m->cfg, st));
+  else CUDA_CHECK(fsdpk::launch_copy_in_bf16(l->shard, dst, l->L.S, m->cfg, st));
+  ps.done();
+}
+
+void validate_grads(const fsdp_layer* l, const void* const* grads, fsdp_dtype_t gd, fsdp_dtype_t rd) {
+  if (!grads) fail(FSDP_ERR_INVALID_ARGUMENT, "full_grads is NULL");
+  for (int p = 0; p < l->P; ++p)
+    if (!grads[p] && l->L.numel[p] > 0) fail(FSDP_ERR_INVALID_ARGUMENT, "full_grads[p] is NULL");
+  if (gd != FSDP_BFLOAT16 && gd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "grad_dtype must be BFLOAT16 or FLOAT32");
+  if (rd != FSDP_BFLOAT16 && rd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "reduce_dtype must be FLOAT32 or BFLOAT16");
+}
+
+}  // namespace fsdpc

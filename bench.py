@@ -62,6 +62,11 @@ def parse():
     ap.add_argument("--grads", default="auto", choices=["auto", "torch", "library"],
                     help="where the full grads live: torch tensors (the RS stages them), or the layer's "
                          "own symmetric grad buffers (zero-copy; auto = library under P2P)")
+    ap.add_argument("--compute-tokens", type=int, default=0,
+                    help="optional compute proxy (SURVEY.md 8(d) row 4; bf16 unit step only): after each unit's "
+                         "wait_unshard, bf16 GEMMs x[T, in] @ W_p^T over its gathered 2-D weights, 3 passes "
+                         "(6*N*T flops, forward + backward), so prefetch/RS overlap with compute is measured; "
+                         "also times the compute alone -> exposed communication")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     return ap.parse_args()
 
@@ -178,6 +183,24 @@ def run_ours(args):
     comp = torch.cuda.Stream(device=dev)
     W = mesh.shard_size if N > 1 else 1     # Shard(0) degree (HSDP: shard group size)
 
+    T = args.compute_tokens
+    if T and (wl["fp8"] or args.step != "unit"):
+        raise SystemExit("--compute-tokens: bf16 workloads with --step unit only")
+    xin = {}
+    if T:
+        for l in layers:
+            for s in l.shapes:
+                if len(s) == 2 and s[1] not in xin:
+                    xin[s[1]] = torch.randn(T, s[1], generator=gen, device=dev).to(torch.bfloat16)
+
+    def compute(weights):
+        """3 forward-shaped GEMM passes over the unit's 2-D weights (6*N*T flops)."""
+        with torch.cuda.stream(comp):
+            for _ in range(3):
+                for w in weights:
+                    if w.dim() == 2:
+                        torch.matmul(xin[w.shape[1]], w.t())
+
     def step_unit():
         n = len(layers)
         if not args.serial:
@@ -188,6 +211,8 @@ def run_ours(args):
             F.fsdp_wait_unshard(layers[i], stream=comp)
             if not args.serial and i + 1 < n:
                 F.fsdp_unshard(layers[i + 1], pdtype, stream=comp)   # prefetch
+            if T:
+                compute(layers[i].unsharded_params())
             F.fsdp_reshard(layers[i], stream=comp)
             F.reduce_scatter_grads(layers[i], grads[i], stream=comp)
             if args.serial:
@@ -260,25 +285,27 @@ def run_ours(args):
         clocks.start()
     mesh.profile_enable(True)
     mesh.profile_read(reset=True)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]   # step boundaries
     barrier()
     torch.cuda.synchronize()
-    e0.record(comp)
-    for _ in range(args.steps):
+    evs[0].record(comp)
+    for k in range(args.steps):
         step()
-    e1.record(comp)
+        evs[k + 1].record(comp)
     comp.synchronize()
     torch.cuda.synchronize()
     barrier()
     prof = mesh.profile_read(reset=True)
     mesh.profile_enable(False)
     clk = clocks.stop() if clocks else None
-    ms = e0.elapsed_time(e1) / args.steps
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    per_step = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    t = torch.tensor([evs[0].elapsed_time(evs[-1]) / args.steps] + per_step, device=dev, dtype=torch.float64)
     if N > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = float(t[0].item())
+    step_pct = {"median": round(float(t[1:].median().item()), 4),
+                "p10": round(float(torch.quantile(t[1:], 0.1).item()), 4),
+                "p90": round(float(torch.quantile(t[1:], 0.9).item()), 4), "of": "per-step max over ranks"}
     value = N * bytes_rank / (ms_max * 1e-3) / 1e9
     algbw_rank = bytes_rank / (ms_max * 1e-3) / 1e9
     busbw_rank = algbw_rank * (W - 1) / W
@@ -303,6 +330,29 @@ def run_ours(args):
     mesh.profile_enable(False)
     args.serial = serial_saved
     barrier()
+    proxy = None
+    if T:   # the same GEMMs alone, each unit's weights unsharded beforehand (outside the events)
+        ms_c = 0.0
+        for rep in range(2):
+            tot = 0.0
+            for l in layers:
+                F.fsdp_unshard(l, pdtype, stream=comp)
+                F.fsdp_wait_unshard(l, stream=comp)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(comp)
+                compute(l.unsharded_params())
+                b.record(comp)
+                F.fsdp_reshard(l, stream=comp)
+                b.synchronize()
+                tot += a.elapsed_time(b)
+            ms_c = tot          # second repetition: warm GEMM heuristics
+        tc = torch.tensor([ms_c], device=dev, dtype=torch.float64)
+        if N > 1:
+            dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+        flops = 6 * T * sum(int(np.prod(s)) for l in layers for s in l.shapes if len(s) == 2)
+        proxy = {"tokens": T, "flops_per_step": flops, "ms_compute_only": round(float(tc.item()), 4),
+                 "ms_with_fsdp": round(ms_max, 4), "exposed_comm_ms": round(ms_max - float(tc.item()), 4),
+                 "compute_TFLOPs": round(flops / (float(tc.item()) * 1e-3) / 1e12, 1)}
 
     # ---- roofline of the dominant kernel (largest total device time among ours).
     # HBM-bound kernels are measured against the measured HBM copy peak; the fused P2P
@@ -358,7 +408,8 @@ def run_ours(args):
             cpu = cpu_baseline(args, W)
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": N, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "ms_per_step_pct": step_pct,
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp8_e4m3+bf16/f32" if wl["fp8"] else "bf16/f32",
             "data": "synthetic (seeded normal params and bf16 grads, Llama 3.1 parameter shapes)",
             "config": {"workload": f"{args.workload} layout: {len(layers)} FSDP units "
@@ -381,6 +432,9 @@ def run_ours(args):
                          "step_hbm_GBps": round(step_hbm, 1), "step_hbm_frac": round(step_hbm / measured_peaks()[0], 4)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,
         }
+        if proxy:
+            line["compute_proxy"] = proxy
+            line["config"]["step"] += f" + compute proxy ({T} tokens/rank; value includes compute time)"
     for l in layers:
         l.destroy()
     mesh.destroy()

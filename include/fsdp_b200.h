@@ -210,6 +210,25 @@ fsdp_status_t fsdp_mesh_abort(fsdp_mesh_t* mesh);
 fsdp_status_t fsdp_profile_enable(fsdp_mesh_t* mesh, int32_t on);
 fsdp_status_t fsdp_profile_read(fsdp_mesh_t* mesh, fsdp_profile_t* out, int32_t reset);
 
+/* Device-memory allocator of the mesh's bulk buffers (SURVEY.md §8(b) "Ownership": device
+ * memory comes from a caller-supplied allocator, which the Python binding wires to the
+ * torch caching allocator — "PyTorch for device memory" without the library calling
+ * torch).  alloc_fn(ctx, bytes, device, &ptr) returns 0 and a device pointer of at least
+ * `bytes` bytes on `device`, 256-byte aligned (else FSDP_ERR_INVALID_ARGUMENT), or non-zero
+ * for out of memory (-> FSDP_ERR_OUT_OF_MEMORY); free_fn(ctx, ptr, device) releases it.
+ * The library synchronizes the device before calling free_fn, so the block may be reused
+ * on any stream at once.  Covered: every layer's fp32 shard and sharded-grad buffers, the
+ * NCCL path's all-gather / reduce-scatter pool buffers and the non-symmetric full-grad
+ * buffers (fsdp_full_grad_buffer under NCCL) allocated after the call; each buffer is
+ * freed through the allocator that made it.  Not covered (stay cudaMalloc / CUDA-IPC
+ * exported, library-owned): the P2P path's symmetric buffers (they must be IPC-mappable
+ * allocations of their own) and bookkeeping tables (tiles, fp8 registry; < 1 MB per
+ * unit).  Both NULL restores cudaMalloc / cudaFree.  Host-synchronous. */
+typedef int32_t (*fsdp_alloc_fn)(void* ctx, size_t bytes, int32_t device, void** out_ptr);
+typedef void (*fsdp_free_fn)(void* ctx, void* ptr, int32_t device);
+fsdp_status_t fsdp_mesh_set_allocator(fsdp_mesh_t* mesh, fsdp_alloc_fn alloc_fn, fsdp_free_fn free_fn,
+                                      void* ctx);
+
 /* ---------------------------------------------------------------- shard (a1) */
 /* fsdp_shard(params, mesh): synchronous, collective over the mesh (all ranks call it
  * with the same descs, checked by an all-gather of the layout hash -> FSDP_ERR_SHAPE).

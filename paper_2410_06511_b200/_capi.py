@@ -49,6 +49,9 @@ _VP = C.c_void_p
 _I32 = C.c_int32
 _I64 = C.c_int64
 _PP = C.POINTER(C.c_void_p)
+# fsdp_alloc_fn / fsdp_free_fn (fsdp_mesh_set_allocator)
+ALLOC_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_size_t, C.c_int32, C.POINTER(C.c_void_p))
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_int32)
 
 # name -> argtypes (restype is fsdp_status_t unless listed in _OTHER)
 SIGNATURES = {
@@ -67,6 +70,7 @@ SIGNATURES = {
     "fsdp_mesh_get_algo": [_VP, C.POINTER(_I32)],
     "fsdp_profile_enable": [_VP, _I32],
     "fsdp_profile_read": [_VP, C.POINTER(Profile), _I32],
+    "fsdp_mesh_set_allocator": [_VP, ALLOC_FN, FREE_FN, _VP],
     "fsdp_shard": [_VP, _I32, C.POINTER(ParamDesc), _PP, C.POINTER(_VP)],
     "fsdp_layer_destroy": [_VP],
     "fsdp_layer_info": [_VP, C.POINTER(_I32), C.POINTER(_I64), C.POINTER(_I64)],

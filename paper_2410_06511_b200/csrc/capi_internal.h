@@ -80,21 +80,53 @@ struct DeviceGuard {
   }
 };
 
+// Allocator of the bulk device buffers (fsdp_mesh_set_allocator); no callbacks = cudaMalloc.
+// Buffers keep a copy of the allocator that made them and are freed through it.
+struct Allocator {
+  fsdp_alloc_fn alloc_fn = nullptr;
+  fsdp_free_fn free_fn = nullptr;
+  void* ctx = nullptr;
+  int device = 0;
+  void* allocate(size_t bytes) const {
+    void* p = nullptr;
+    if (!alloc_fn) {
+      CUDA_CHECK(cudaMalloc(&p, bytes));
+      return p;
+    }
+    if (alloc_fn(ctx, bytes, device, &p) != 0 || !p) fail(FSDP_ERR_OUT_OF_MEMORY, "allocator callback failed");
+    if (reinterpret_cast<uintptr_t>(p) & 255) {
+      free_fn(ctx, p, device);
+      fail(FSDP_ERR_INVALID_ARGUMENT, "allocator callback returned a pointer that is not 256-byte aligned");
+    }
+    return p;
+  }
+  void release(void* p) const {   // never throws (destroy paths)
+    if (!p) return;
+    if (!free_fn) {
+      cudaFree(p);
+      return;
+    }
+    cudaDeviceSynchronize();      // a callback free is not stream-ordered against our kernels
+    cudaGetLastError();
+    free_fn(ctx, p, device);
+  }
+};
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
-  void ensure(size_t bytes) {
+  Allocator al;
+  void ensure(size_t bytes, const Allocator& with) {
     if (bytes <= cap) return;
-    if (p) CUDA_CHECK(cudaFree(p));
-    p = nullptr;
-    cap = 0;
+    release();
     // +64 B slack: the misaligned 16-byte loads of K4/K5 may touch the aligned block
     // holding the last byte
-    CUDA_CHECK(cudaMalloc(&p, bytes + 64));
+    al = with;
+    p = al.allocate(bytes + 64);
     cap = bytes;
   }
   void release() {
-    if (p) cudaFree(p);
+    al.release(p);
     p = nullptr;
     cap = 0;
   }
@@ -215,6 +247,7 @@ struct fsdp_mesh {
   int gbuf_seq = 0;                          // flag slots of layer grad buffers: kPoolSlots + seq
   unsigned long long p2p_timeout_ns = 60ull * 1000 * 1000 * 1000;   // handshake spin bound
   int* d_barrier = nullptr;
+  Allocator allocator;                       // bulk buffers (fsdp_mesh_set_allocator)
 };
 
 struct fsdp_layer {
@@ -248,6 +281,7 @@ struct fsdp_layer {
   bool gbuf_sym = false;
   fsdp_dtype_t gbuf_dtype = FSDP_BFLOAT16;
   void* arena_base = nullptr;        // base of the unsharded tensors (either path)
+  Allocator al;                      // made shard / grad / non-symmetric gbuf (mesh's at shard time)
 };
 
 

@@ -40,8 +40,9 @@ fsdp_status_t fsdp_shard(fsdp_mesh_t* m, int32_t n, const fsdp_param_desc_t* des
     try {
       const Layout& Ly = l->L;
       const size_t sbytes = sizeof(float) * (size_t)std::max<int64_t>(Ly.S, 16);
-      CUDA_CHECK(cudaMalloc(&l->shard, sbytes));
-      CUDA_CHECK(cudaMalloc(&l->grad, sbytes));
+      l->al = m->allocator;
+      l->shard = static_cast<float*>(l->al.allocate(sbytes));
+      l->grad = static_cast<float*>(l->al.allocate(sbytes));
       CUDA_CHECK(cudaMemset(l->shard, 0, sbytes));
       CUDA_CHECK(cudaMemset(l->grad, 0, sbytes));
       if (full_params) {
@@ -108,8 +109,8 @@ fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* l) {
     if (l->state != SHARDED) fail(FSDP_ERR_STATE, "reshard the layer before destroying it");
     DeviceGuard g(m->device);
     for (cudaStream_t s : {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs}) cudaStreamSynchronize(s);
-    cudaFree(l->shard);
-    cudaFree(l->grad);
+    l->al.release(l->shard);
+    l->al.release(l->grad);
     cudaFree(l->d_idx_local);
     l->t_cin_fp8.release(); l->t_cout_bf16.release(); l->t_cout_fp8.release(); l->t_rsin.release();
     l->t_push_bf16.release(); l->t_push_fp8.release(); l->t_pull.release(); l->t_stage_bf16.release();
@@ -117,7 +118,7 @@ fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* l) {
     if (l->gbuf) {
       if (l->gbuf_sym && !m->aborted) sym_free(m, l->gbuf->buf);   // collective
       else if (l->gbuf_sym) sym_free_local(m, l->gbuf->buf);
-      else cudaFree(l->gbuf->buf.local);
+      else l->al.release(l->gbuf->buf.local);
       if (l->gbuf->free_ev) cudaEventDestroy(l->gbuf->free_ev);
       delete l->gbuf;
       l->gbuf = nullptr;
@@ -641,7 +642,13 @@ fsdp_status_t fsdp_full_grad_buffer(fsdp_layer_t* l, fsdp_dtype_t gd, int32_t p,
         }
         l->gbuf_sym = true;
       } else {
-        CUDA_CHECK(cudaMalloc(&s->buf.local, bytes + 256));
+        try {
+          s->buf.local = l->al.allocate(bytes + 256);
+        } catch (...) {
+          cudaEventDestroy(s->free_ev);
+          delete s;
+          throw;
+        }
         CUDA_CHECK(cudaMemset(s->buf.local, 0, bytes + 256));
         s->buf.bytes = bytes;
         l->gbuf_sym = false;

@@ -297,6 +297,15 @@ fsdp_status_t fsdp_mesh_synchronize(fsdp_mesh_t* m, int64_t timeout_ms) {
   });
 }
 
+fsdp_status_t fsdp_mesh_set_allocator(fsdp_mesh_t* m, fsdp_alloc_fn alloc_fn, fsdp_free_fn free_fn, void* ctx) {
+  return guarded([&] {
+    check_mesh(m);
+    if ((alloc_fn == nullptr) != (free_fn == nullptr))
+      fail(FSDP_ERR_INVALID_ARGUMENT, "alloc_fn and free_fn must both be set or both be NULL");
+    m->allocator = Allocator{alloc_fn, free_fn, alloc_fn ? ctx : nullptr, m->device};
+  });
+}
+
 fsdp_status_t fsdp_profile_enable(fsdp_mesh_t* m, int32_t on) {
   return guarded([&] {
     check_mesh(m);

@@ -53,8 +53,8 @@ Slot* acquire_slot(fsdp_mesh* m, std::vector<Slot*>& pool, size_t a_bytes, size_
   }
   if (best->a.cap < a_bytes || best->b.cap < b_bytes) {
     if (best->ever_used) CUDA_CHECK(cudaEventSynchronize(best->free_ev));   // growth: setup-time only
-    best->a.ensure(a_bytes);
-    best->b.ensure(b_bytes);
+    best->a.ensure(a_bytes, m->allocator);
+    best->b.ensure(b_bytes, m->allocator);
   }
   best->in_use = true;
   best->last_use = ++m->use_seq;

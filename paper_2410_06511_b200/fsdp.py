@@ -101,14 +101,35 @@ def get_unique_id() -> bytes:
     return bytes(buf)
 
 
+def _torch_allocator():
+    """fsdp_alloc_fn / fsdp_free_fn backed by the torch caching allocator (SURVEY.md §8(b)
+    "Ownership"): the library's bulk buffers show up in torch.cuda.memory_allocated() and
+    share torch's cache.  The library synchronizes the device before every free."""
+    def alloc(ctx, nbytes, dev, out):
+        try:
+            out[0] = torch.cuda.caching_allocator_alloc(int(nbytes), int(dev))
+            return 0
+        except Exception:          # OOM (or anything else): FSDP_ERR_OUT_OF_MEMORY in the caller
+            return 1
+
+    def free(ctx, ptr, dev):
+        if ptr:
+            torch.cuda.caching_allocator_delete(int(ptr))
+    return capi.ALLOC_FN(alloc), capi.FREE_FN(free)
+
+
 # ----------------------------------------------------------------------- mesh
 class Mesh:
     """1-D data-parallel mesh (fsdp_mesh_t).  world_size defaults to all ranks."""
 
     def __init__(self, world_size: int, rank: int, device: int, unique_id: Optional[bytes] = None,
-                 local: bool = False, shard_size: Optional[int] = None):
+                 local: bool = False, shard_size: Optional[int] = None, allocator: str = "torch"):
         """world_size ranks; shard_size < world_size makes an HSDP mesh of world_size //
-        shard_size replica groups x shard_size ranks."""
+        shard_size replica groups x shard_size ranks.  allocator:
+        "torch" (bulk buffers from the torch caching allocator, fsdp_mesh_set_allocator) or
+        "cuda" (the library's own cudaMalloc)."""
+        if allocator not in ("torch", "cuda"):
+            raise ValueError("allocator must be 'torch' or 'cuda'")
         self.world_size, self.rank, self.device = int(world_size), int(rank), int(device)
         self.local = local
         h = C.c_void_p()
@@ -124,6 +145,11 @@ class Mesh:
                 call("fsdp_mesh_init", idb, self.world_size, self.rank, self.device, C.byref(h))
         self.handle = h
         self.layers: List["Layer"] = []
+        self.allocator = allocator
+        self._alloc_cbs = None           # kept alive for the mesh's lifetime (frees at destroy)
+        if allocator == "torch":
+            self._alloc_cbs = _torch_allocator()
+            call("fsdp_mesh_set_allocator", h, self._alloc_cbs[0], self._alloc_cbs[1], None)
         R = C.c_int32()
         rep = C.c_int32()
         call("fsdp_mesh_info_hsdp", h, C.byref(R), C.byref(rep))
@@ -133,7 +159,7 @@ class Mesh:
 
     @classmethod
     def from_process_group(cls, group=None, device: Optional[int] = None,
-                           shard_size: Optional[int] = None) -> "Mesh":
+                           shard_size: Optional[int] = None, allocator: str = "torch") -> "Mesh":
         """Collective: rank 0 creates the NCCL unique id, torch.distributed broadcasts it
         (the binding's only torch.distributed use), every rank initialises the mesh.
         shard_size (data_parallel_shard_degree) defaults to all ranks."""
@@ -144,7 +170,7 @@ class Mesh:
         r = dist.get_rank(group)
         obj = [get_unique_id() if r == 0 else None]
         dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
-        return cls(W, r, device, unique_id=obj[0], shard_size=shard_size)
+        return cls(W, r, device, unique_id=obj[0], shard_size=shard_size, allocator=allocator)
 
     @property
     def algo(self) -> str:

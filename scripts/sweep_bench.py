@@ -22,6 +22,27 @@ import synth  # noqa: E402
 import paper_2410_06511_b200 as F  # noqa: E402
 
 
+def fit_alpha_B(lines, W):
+    """Least-squares fit of the alpha-beta cost model t = alpha + x / B per variant and
+    collective (SPEC.md:673's latency + bytes/bandwidth model), x = bus bytes
+    (W-1)/W * algorithm bytes; alpha in us, B in GB/s."""
+    import numpy as np
+    out = []
+    for var in sorted({l["variant"] for l in lines}):
+        rows = [l for l in lines if l["variant"] == var]
+        for op, key, mult in (("unshard", "unshard_us", 1), ("reduce_scatter", "rs_us", 2)):
+            x = np.array([l["ag_bytes"] * mult * (W - 1) / W for l in rows], dtype=np.float64)
+            t = np.array([l[key] for l in rows], dtype=np.float64)
+            if len(x) < 2 or W == 1:
+                continue
+            A = np.stack([np.ones_like(x), x], axis=1) / t[:, None]     # relative residuals:
+            (alpha, inv_b), *_ = np.linalg.lstsq(A, np.ones_like(t), rcond=None)  # small sizes count
+            out.append({"fit": "alpha_B", "variant": var, "op": op, "W": W, "points": len(x),
+                        "alpha_us": round(float(alpha), 2),
+                        "B_GBps": round(float(1e-3 / inv_b), 1) if inv_b > 0 else None})
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
@@ -112,10 +133,14 @@ def main():
         if rank == 0:
             for l in lines[-3:]:
                 print(json.dumps(l), flush=True)
-    if rank == 0 and args.out:
-        with open(args.out, "w") as f:
-            for l in lines:
-                f.write(json.dumps(l) + "\n")
+    if rank == 0:
+        fits = fit_alpha_B(lines, W)
+        for l in fits:
+            print(json.dumps(l), flush=True)
+        if args.out:
+            with open(args.out, "w") as f:
+                for l in lines + fits:
+                    f.write(json.dumps(l) + "\n")
     mesh.destroy()
     dist.destroy_process_group()
 

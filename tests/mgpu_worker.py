@@ -31,6 +31,26 @@ def u16(t):
     return t.view(torch.int16).cpu().numpy().view(np.uint16)
 
 
+def pow2(W):
+    return W & (W - 1) == 0
+
+
+def check_rs(got, ref, p, W, algo, dyadic, ordered=True, tag=()):
+    """fp32 reduce-scatter result vs the oracle.  Dyadic grads k*2^-10 divided by a power of
+    two W are exact in fp32 and so is every partial sum: bit-exact for ANY order.  For other W
+    (x/3 rounds) or normal data, the P2P pull's ascending-rank order is bit-exact to the
+    oracle's ordered sum (`ordered`), and anything else (NCCL, HSDP's two stages) is held to the
+    R10 bound."""
+    if dyadic and pow2(W):
+        np.testing.assert_array_equal(got, ref["exact"][p])
+    elif algo == "p2p" and ordered:
+        np.testing.assert_array_equal(got, ref["order"][p])
+    else:
+        ok, ratio, nrel = rs_error_ok(got.reshape(-1), ref["exact"][p].reshape(-1),
+                                      ref["mag"][p].reshape(-1), W)
+        assert ok, tag + (p, ratio, nrel)
+
+
 def main():
     rank = int(os.environ["RANK"])
     W = int(os.environ["WORLD_SIZE"])
@@ -131,13 +151,12 @@ def run_hsdp_checks(W, rank, local, Ws):
                         got = layer.sharded_grad(p).cpu().numpy()
                         m = layer.metas[p]
                         prev = before[m["elem_offset"]:m["elem_offset"] + got.size].cpu().numpy().reshape(got.shape)
-                        if kind == "dyadic":
+                        if kind == "dyadic" and pow2(W):
                             want = (prev + ref["exact"][p]).astype(np.float32) if acc else ref["exact"][p]
                             np.testing.assert_array_equal(got, want)
                         elif not acc:
-                            ok, ratio, nrel = rs_error_ok(got.reshape(-1), ref["exact"][p].reshape(-1),
-                                                          ref["mag"][p].reshape(-1), W)
-                            assert ok, (algo, Ws, ui, p, ratio, nrel)
+                            check_rs(got, ref, p, W, algo, kind == "dyadic", ordered=False,
+                                     tag=(algo, Ws, ui))
             layer.destroy()
         print(f"rank {rank}/{W} hsdp {R}x{Ws} algo={algo}: OK", flush=True)
     mesh.synchronize(120000)
@@ -186,25 +205,18 @@ def run_checks(mesh, W, rank, local, algo):
             ref = w.reduce_scatter_grads(G, BF16, True)[rank]
             for p in range(len(shapes)):
                 got = layer.sharded_grad(p).cpu().numpy()
-                if kind == "dyadic":
-                    np.testing.assert_array_equal(got, ref["exact"][p])
-                elif algo == "p2p":
-                    # the pull kernel sums fp32(g_q)/W in ascending rank order: bit-exact
-                    # to the oracle's ordered sum (SPEC.md:159 reduction order)
-                    np.testing.assert_array_equal(got, ref["order"][p])
-                else:
-                    ok, ratio, nrel = rs_error_ok(got.reshape(-1), ref["exact"][p].reshape(-1),
-                                                  ref["mag"][p].reshape(-1), W)
-                    assert ok, (ui, p, ratio, nrel)
-            # accumulate: the second RS adds in fp32 onto the first
+                # the pull kernel sums fp32(g_q)/W in ascending rank order: bit-exact to the
+                # oracle's ordered sum (SPEC.md:159 reduction order)
+                check_rs(got, ref, p, W, algo, kind == "dyadic", tag=(ui,))
+            # accumulate: the second RS adds in fp32 onto the first (g = old + reduced)
             before = layer.sharded_grad_flat().clone()
             F.reduce_scatter_grads(layer, gt, accumulate=True)
             F.fsdp_wait_reduce_scatter(layer)
-            once = w.reduce_scatter_grads(G, BF16, True)[rank]["exact"]
+            once = ref["exact"] if kind == "dyadic" and pow2(W) else ref["order"]
             for p in range(len(shapes)):
                 got = layer.sharded_grad(p).cpu().numpy()
                 prev = before[layer.metas[p]["elem_offset"]:layer.metas[p]["elem_offset"] + got.size].cpu().numpy()
-                if kind == "dyadic":
+                if (kind == "dyadic" and pow2(W)) or algo == "p2p":
                     np.testing.assert_array_equal(got.reshape(-1), (prev + once[p].reshape(-1)).astype(np.float32))
         # bf16 reduce (reading R11): elementwise (W-1)*2^-8*mag + tiny, normwise 1e-2
         G = [[synth.grad_bf16_bits(ui, p, q, s) for p, s in enumerate(shapes)] for q in range(W)]
@@ -229,7 +241,7 @@ def run_checks(mesh, W, rank, local, algo):
         F.fsdp_wait_reduce_scatter(layer)
         ref = w.reduce_scatter_grads(G, BF16, True)[rank]
         for p in range(len(shapes)):
-            np.testing.assert_array_equal(layer.sharded_grad(p).cpu().numpy(), ref["exact"][p])
+            check_rs(layer.sharded_grad(p).cpu().numpy(), ref, p, W, algo, True, tag=(ui, "zero-copy"))
         layer.destroy()
         checks += 1
 
@@ -272,11 +284,17 @@ def run_checks(mesh, W, rank, local, algo):
         _, fulls = worlds[i].unshard(worlds[i].shard(params[i]), BF16)
         for t, want in zip(got[i], fulls):
             np.testing.assert_array_equal(u16(t), want)
-        want_g = np.float32(sum((i + 1 + q) / W for q in range(W)))
+        acc = np.float32(0)        # ascending-rank fp32 sum of fp32(g_q)/W (exact for W = 2^k)
+        for q in range(W):
+            acc = np.float32(acc + np.float32(np.float32(i + 1 + q) / np.float32(W)))
         for p in range(l.P):
             g = l.sharded_grad(p)
-            if g.numel():
-                assert torch.all(g == float(want_g)), (i, p)
+            if not g.numel():
+                continue
+            if pow2(W) or algo == "p2p":
+                assert torch.all(g == float(acc)), (i, p)
+            else:
+                assert torch.allclose(g, torch.full_like(g, float(acc)), rtol=W * 2.0 ** -23, atol=0), (i, p)
     for l in layers:
         l.destroy()
     mesh.synchronize(120000)

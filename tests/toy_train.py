@@ -49,6 +49,9 @@ def loss_of(x, blocks):
 def reference_steps(n_steps, W, lr=0.05, n_blocks=2):
     """Single-device: returns the fp32 master params after each step."""
     master = [[torch.from_numpy(p).cuda() for p in blk] for blk in init_params(n_blocks)]
+    # IEEE division by W (P:466 "a single division kernel"): a 0-dim CUDA divisor, because
+    # torch divides by a CPU scalar as x * (1/W), which differs from x / W when W != 2^k
+    div = torch.tensor(float(W), device="cuda")
     history = []
     for step in range(n_steps):
         grads = [[torch.zeros_like(p) for p in blk] for blk in master]
@@ -57,7 +60,7 @@ def reference_steps(n_steps, W, lr=0.05, n_blocks=2):
             loss_of(batch(step, r), params).backward()
             for gb, pb in zip(grads, params):
                 for g, p in zip(gb, pb):
-                    g += p.grad.float() / W            # fp32 mean of the per-rank bf16 grads
+                    g += p.grad.float() / div          # fp32 mean of the per-rank bf16 grads
         for mb, gb in zip(master, grads):
             for m, g in zip(mb, gb):
                 m -= lr * g

@@ -260,6 +260,7 @@ struct fsdp_layer {
   int reg_base = 0;
   int32_t* d_idx_local = nullptr;   // 0..P-1 (stage fp8 scale)
   DevTiles t_cin_fp8, t_cout_bf16, t_cout_fp8, t_rsin;
+  DevTiles t_amax_stage;             // fsdp_stage_local_amax (lazily built)
   int64_t bytes_cin_fp8 = 0, bytes_cout_bf16 = 0, bytes_cout_fp8 = 0;
   int64_t grad_numel_total = 0;
   // unshard state

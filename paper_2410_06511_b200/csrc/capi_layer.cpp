@@ -114,7 +114,7 @@ fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* l) {
     cudaFree(l->d_idx_local);
     l->t_cin_fp8.release(); l->t_cout_bf16.release(); l->t_cout_fp8.release(); l->t_rsin.release();
     l->t_push_bf16.release(); l->t_push_fp8.release(); l->t_pull.release(); l->t_stage_bf16.release();
-    l->t_stage_fp32.release();
+    l->t_stage_fp32.release(); l->t_amax_stage.release();
     if (l->gbuf) {
       if (l->gbuf_sym && !m->aborted) sym_free(m, l->gbuf->buf);   // collective
       else if (l->gbuf_sym) sym_free_local(m, l->gbuf->buf);

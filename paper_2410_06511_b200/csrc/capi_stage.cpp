@@ -44,15 +44,18 @@ fsdp_status_t fsdp_stage_local_amax(const fsdp_layer_t* lc, float* amax_out, voi
     if (!amax_out) fail(FSDP_ERR_INVALID_ARGUMENT, "amax_out is NULL");
     DeviceGuard g(l->mesh->device);
     cudaStream_t st = as_stream(stream);
-    std::vector<Tile> tiles;
-    fsdpl::append_tiles_amax(l->L, l->shard, 0, &tiles);
-    DevTiles T;
-    T.upload(tiles);   // synchronous upload (test entry point, not on the hot path)
+    if (!l->t_amax_stage.d) {   // built once per layer (registry index = local param index)
+      std::vector<Tile> tiles;
+      fsdpl::append_tiles_amax(l->L, l->shard, 0, &tiles);
+      if (tiles.empty()) {
+        CUDA_CHECK(cudaMemsetAsync(amax_out, 0, sizeof(float) * l->P, st));
+        return;
+      }
+      l->t_amax_stage.upload(tiles);
+    }
     CUDA_CHECK(cudaMemsetAsync(amax_out, 0, sizeof(float) * l->P, st));
-    cudaError_t e = fsdpk::launch_amax(T.d, T.n, reinterpret_cast<uint32_t*>(amax_out), l->mesh->cfg, st);
-    CUDA_CHECK(cudaStreamSynchronize(st));
-    T.release();
-    CUDA_CHECK(e);
+    CUDA_CHECK(fsdpk::launch_amax(l->t_amax_stage.d, l->t_amax_stage.n, reinterpret_cast<uint32_t*>(amax_out),
+                                  l->mesh->cfg, st));
   });
 }
 

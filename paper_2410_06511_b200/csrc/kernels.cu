@@ -314,29 +314,40 @@ __global__ void __launch_bounds__(kThreads) k_rs_copy_in_bulk(const Tile* __rest
 // ------------------------------------------------------------------- K6 RS copy-out
 template <bool kInBf16, bool kAcc>
 __global__ void __launch_bounds__(kThreads) k_rs_copy_out(const uint8_t* __restrict__ in,
-                                                          float* __restrict__ grad, int64_t n8) {
+                                                          float* __restrict__ grad, int64_t n4) {
+  // 4 elements per thread per item, so every warp load / store instruction covers one
+  // contiguous 256 B (bf16 in) / 512 B span with whole 32 B sectors; kU grid-stride items
+  // per thread with all loads issued before any store (HBM latency-bandwidth product)
+  constexpr int kU = 4;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
-  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n8; i += stride) {
-    float x[8];
-    if (kInBf16) {
-      const uint4 a = ld_stream(in + 16 * i);
-      x[0] = bf16_lo(a.x); x[1] = bf16_hi(a.x); x[2] = bf16_lo(a.y); x[3] = bf16_hi(a.y);
-      x[4] = bf16_lo(a.z); x[5] = bf16_hi(a.z); x[6] = bf16_lo(a.w); x[7] = bf16_hi(a.w);
-    } else {
-      const uint4 a = ld_stream(in + 32 * i), b = ld_stream(in + 32 * i + 16);
-      x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y); x[2] = __uint_as_float(a.z);
-      x[3] = __uint_as_float(a.w); x[4] = __uint_as_float(b.x); x[5] = __uint_as_float(b.y);
-      x[6] = __uint_as_float(b.z); x[7] = __uint_as_float(b.w);
+  float4* g4 = reinterpret_cast<float4*>(grad);
+  for (int64_t base = (int64_t)blockIdx.x * kThreads + threadIdx.x; base < n4; base += kU * stride) {
+    uint4 a[kU];
+    uint2 h[kU];
+    float4 g[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = base + u * stride;
+      if (i < n4) {
+        if (kInBf16) h[u] = ld_stream8(in + 8 * i);
+        else a[u] = ld_stream(in + 16 * i);
+        if (kAcc) g[u] = g4[i];
+      }
     }
-    float4* g = reinterpret_cast<float4*>(grad + 8 * i);
-    if (kAcc) {
-      const float4 g0 = g[0], g1 = g[1];
-      x[0] = __fadd_rn(g0.x, x[0]); x[1] = __fadd_rn(g0.y, x[1]); x[2] = __fadd_rn(g0.z, x[2]);
-      x[3] = __fadd_rn(g0.w, x[3]); x[4] = __fadd_rn(g1.x, x[4]); x[5] = __fadd_rn(g1.y, x[5]);
-      x[6] = __fadd_rn(g1.z, x[6]); x[7] = __fadd_rn(g1.w, x[7]);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = base + u * stride;
+      if (i >= n4) break;
+      float4 x;
+      if (kInBf16) x = make_float4(bf16_lo(h[u].x), bf16_hi(h[u].x), bf16_lo(h[u].y), bf16_hi(h[u].y));
+      else x = make_float4(__uint_as_float(a[u].x), __uint_as_float(a[u].y), __uint_as_float(a[u].z),
+                           __uint_as_float(a[u].w));
+      if (kAcc) {
+        x.x = __fadd_rn(g[u].x, x.x); x.y = __fadd_rn(g[u].y, x.y);
+        x.z = __fadd_rn(g[u].z, x.z); x.w = __fadd_rn(g[u].w, x.w);
+      }
+      g4[i] = x;
     }
-    g[0] = make_float4(x[0], x[1], x[2], x[3]);
-    g[1] = make_float4(x[4], x[5], x[6], x[7]);
   }
 }
 
@@ -486,14 +497,14 @@ cudaError_t launch_rs_copy_in(const Tile* tiles, int ntiles, const PtrArray& gra
 
 cudaError_t launch_rs_copy_out(const void* rs_out, bool in_bf16, float* grad, bool accumulate, int64_t S,
                                LaunchCfg cfg, cudaStream_t st) {
-  const int64_t n8 = S / 8;
-  if (n8 == 0) return cudaSuccess;
-  const int g = grid_for((n8 + kThreads - 1) / kThreads, cfg);
+  const int64_t n4 = S / 4;   // S is a multiple of 16 (R2)
+  if (n4 == 0) return cudaSuccess;
+  const int g = grid_for((n4 + kThreads - 1) / kThreads, cfg);
   const uint8_t* in = (const uint8_t*)rs_out;
-  if (in_bf16 && accumulate) k_rs_copy_out<true, true><<<g, kThreads, 0, st>>>(in, grad, n8);
-  else if (in_bf16) k_rs_copy_out<true, false><<<g, kThreads, 0, st>>>(in, grad, n8);
-  else if (accumulate) k_rs_copy_out<false, true><<<g, kThreads, 0, st>>>(in, grad, n8);
-  else k_rs_copy_out<false, false><<<g, kThreads, 0, st>>>(in, grad, n8);
+  if (in_bf16 && accumulate) k_rs_copy_out<true, true><<<g, kThreads, 0, st>>>(in, grad, n4);
+  else if (in_bf16) k_rs_copy_out<true, false><<<g, kThreads, 0, st>>>(in, grad, n4);
+  else if (accumulate) k_rs_copy_out<false, true><<<g, kThreads, 0, st>>>(in, grad, n4);
+  else k_rs_copy_out<false, false><<<g, kThreads, 0, st>>>(in, grad, n4);
   return cudaGetLastError();
 }
 

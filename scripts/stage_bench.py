@@ -193,10 +193,11 @@ def main():
         F.stage_grads_to_staging(layer, grads, staging, stream=st)
         emit(W, "grads_to_staging", "ours", 4 * N,
              lambda: F.stage_grads_to_staging(layer, grads, staging, stream=st))
-        stagings = [staging] * W
+        # W distinct stagings (the same buffer W times would serve W-1 of the reads from L2)
+        stagings = [staging] + [staging.clone() for _ in range(W - 1)]
         emit(W, "pull_fp32", "ours", 2 * W * sum(valid) + 4 * S,
              lambda: F.stage_rs_pull(layer, stagings, torch.bfloat16, stream=st),
-             note="reads this rank's rows from W stagings (all local here), fp32 sum, /W")
+             note="reads this rank's rows from W distinct stagings (all local here), fp32 sum, /W")
         del staging, stagings, grads
         st.synchronize()
         layer.destroy()

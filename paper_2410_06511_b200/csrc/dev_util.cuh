@@ -199,4 +199,21 @@ __device__ __forceinline__ void load4(const uint8_t* p, uint32_t k, float (&x)[4
   }
 }
 
+// ---- host: persistent-grid launches
+// CTAs of `fn` (kThreads threads, `dyn_smem` dynamic bytes, plus its registers and static
+// shared memory) the whole GPU holds at once; cached per kernel (kernels.cu).
+int resident_ctas(const void* fn, size_t dyn_smem);
+
+// Launches a persistent tile-loop kernel with min(g, resident CTAs) CTAs: a CTA that does
+// not fit in the first wave would start only after a first-wave CTA finished ALL of its
+// tiles, so an oversized grid turns into a tail of serial work.
+template <class... KArgs, class... Args>
+cudaError_t launch_persistent(void (*kern)(KArgs...), int g, size_t dyn_smem, cudaStream_t st, Args&&... args) {
+  const int r = resident_ctas(reinterpret_cast<const void*>(kern), dyn_smem);
+  if (r > 0 && g > r) g = r;
+  if (g < 1) g = 1;
+  kern<<<g, kThreads, dyn_smem, st>>>(static_cast<Args&&>(args)...);
+  return cudaGetLastError();
+}
+
 }  // namespace fsdpdev

@@ -16,6 +16,10 @@
 
 #include <cuda_bf16.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "dev_util.cuh"
 
 namespace fsdpk {
@@ -450,23 +454,21 @@ inline int grid_for(int64_t work_items, LaunchCfg cfg, int tuned = kCtasCopy) {
 cudaError_t launch_copy_in_bf16(const float* shard, void* slot, int64_t S, LaunchCfg cfg, cudaStream_t st) {
   const int64_t n4 = S / 4;
   if (n4 == 0) return cudaSuccess;
-  k_copy_in_bf16<<<grid_for((n4 + kThreads - 1) / kThreads, cfg), kThreads, 0, st>>>(
-      reinterpret_cast<const float4*>(shard), reinterpret_cast<uint2*>(slot), n4);
-  return cudaGetLastError();
+  return launch_persistent(k_copy_in_bf16, grid_for((n4 + kThreads - 1) / kThreads, cfg), 0, st,
+                           reinterpret_cast<const float4*>(shard), reinterpret_cast<uint2*>(slot), n4);
 }
 
 cudaError_t launch_copy_in_fp8(const Tile* tiles, int ntiles, const float* shard, void* slot,
                                const float* scales, LaunchCfg cfg, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
-  k_copy_in_fp8<<<grid_for(ntiles, cfg), kThreads, 0, st>>>(tiles, ntiles, shard, (uint8_t*)slot, scales);
-  return cudaGetLastError();
+  return launch_persistent(k_copy_in_fp8, grid_for(ntiles, cfg), 0, st, tiles, ntiles, shard, (uint8_t*)slot,
+                           scales);
 }
 
 cudaError_t launch_copy_out(const Tile* tiles, int ntiles, const void* ag, const PtrArray& outs,
                             LaunchCfg cfg, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
-  k_copy_out<<<grid_for(ntiles, cfg), kThreads, 0, st>>>(tiles, ntiles, (const uint8_t*)ag, outs);
-  return cudaGetLastError();
+  return launch_persistent(k_copy_out, grid_for(ntiles, cfg), 0, st, tiles, ntiles, (const uint8_t*)ag, outs);
 }
 
 cudaError_t launch_rs_copy_in(const Tile* tiles, int ntiles, const PtrArray& grads, bool grad_bf16,
@@ -481,18 +483,14 @@ cudaError_t launch_rs_copy_in(const Tile* tiles, int ntiles, const PtrArray& gra
   uint8_t* d = (uint8_t*)rs_in;
   if (cfg.variant & 8) {   // TMA bulk K5
     const int gb = grid_for(ntiles, cfg, kCtasCopy);
-    if (grad_bf16 && !out_bf16) k_rs_copy_in_bulk<true, false><<<gb, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
-    else if (grad_bf16 && out_bf16) k_rs_copy_in_bulk<true, true><<<gb, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
-    else if (!grad_bf16 && !out_bf16) k_rs_copy_in_bulk<false, false><<<gb, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
-    else k_rs_copy_in_bulk<false, true><<<gb, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
-    return cudaGetLastError();
+    auto k = grad_bf16 ? (out_bf16 ? k_rs_copy_in_bulk<true, true> : k_rs_copy_in_bulk<true, false>)
+                       : (out_bf16 ? k_rs_copy_in_bulk<false, true> : k_rs_copy_in_bulk<false, false>);
+    return launch_persistent(k, gb, 0, st, tiles, ntiles, grads, d, div);
   }
   const int g = grid_for(ntiles, cfg, kCtasRsCopyIn);
-  if (grad_bf16 && !out_bf16) k_rs_copy_in<true, false><<<g, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
-  else if (grad_bf16 && out_bf16) k_rs_copy_in<true, true><<<g, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
-  else if (!grad_bf16 && !out_bf16) k_rs_copy_in<false, false><<<g, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
-  else k_rs_copy_in<false, true><<<g, kThreads, 0, st>>>(tiles, ntiles, grads, d, div);
-  return cudaGetLastError();
+  auto k = grad_bf16 ? (out_bf16 ? k_rs_copy_in<true, true> : k_rs_copy_in<true, false>)
+                     : (out_bf16 ? k_rs_copy_in<false, true> : k_rs_copy_in<false, false>);
+  return launch_persistent(k, g, 0, st, tiles, ntiles, grads, d, div);
 }
 
 cudaError_t launch_rs_copy_out(const void* rs_out, bool in_bf16, float* grad, bool accumulate, int64_t S,
@@ -501,17 +499,14 @@ cudaError_t launch_rs_copy_out(const void* rs_out, bool in_bf16, float* grad, bo
   if (n4 == 0) return cudaSuccess;
   const int g = grid_for((n4 + kThreads - 1) / kThreads, cfg);
   const uint8_t* in = (const uint8_t*)rs_out;
-  if (in_bf16 && accumulate) k_rs_copy_out<true, true><<<g, kThreads, 0, st>>>(in, grad, n4);
-  else if (in_bf16) k_rs_copy_out<true, false><<<g, kThreads, 0, st>>>(in, grad, n4);
-  else if (accumulate) k_rs_copy_out<false, true><<<g, kThreads, 0, st>>>(in, grad, n4);
-  else k_rs_copy_out<false, false><<<g, kThreads, 0, st>>>(in, grad, n4);
-  return cudaGetLastError();
+  auto k = in_bf16 ? (accumulate ? k_rs_copy_out<true, true> : k_rs_copy_out<true, false>)
+                   : (accumulate ? k_rs_copy_out<false, true> : k_rs_copy_out<false, false>);
+  return launch_persistent(k, g, 0, st, in, grad, n4);
 }
 
 cudaError_t launch_amax(const Tile* tiles, int ntiles, uint32_t* acc_bits, LaunchCfg cfg, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
-  k_amax<<<grid_for(ntiles, cfg), kThreads, 0, st>>>(tiles, ntiles, acc_bits);
-  return cudaGetLastError();
+  return launch_persistent(k_amax, grid_for(ntiles, cfg), 0, st, tiles, ntiles, acc_bits);
 }
 
 cudaError_t launch_fp8_scale(const int32_t* idx, int n, uint32_t* acc_bits, float* amax_out, float* scale_out,
@@ -534,3 +529,24 @@ cudaError_t launch_fp8_scale_delayed(const int32_t* idx, int n, uint32_t* acc_bi
   return cudaGetLastError();
 }
 }  // namespace fsdpk
+
+namespace fsdpdev {
+int resident_ctas(const void* fn, size_t dyn_smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, size_t>, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(fn, dyn_smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0, dev = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, dyn_smem) != cudaSuccess ||
+      cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;   // unknown: the caller keeps its grid
+  }
+  const int r = per_sm * sms;
+  cache[key] = r;
+  return r;
+}
+}  // namespace fsdpdev

@@ -572,17 +572,16 @@ template <bool kGradBf16, int V>
 cudaError_t launch_pull_wv(const Tile* tiles, int ntiles, PeerPtrs st, float* grad, PullOps ops, int W, int g,
                            cudaStream_t s) {
   switch (W) {
-    case 1: k_rs_pull<1, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 2: k_rs_pull<2, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 3: k_rs_pull<3, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 4: k_rs_pull<4, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 5: k_rs_pull<5, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 6: k_rs_pull<6, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 7: k_rs_pull<7, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
-    case 8: k_rs_pull<8, kGradBf16, V><<<g, kThreads, 0, s>>>(tiles, ntiles, st, grad, ops); break;
+    case 1: return launch_persistent(k_rs_pull<1, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 2: return launch_persistent(k_rs_pull<2, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 3: return launch_persistent(k_rs_pull<3, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 4: return launch_persistent(k_rs_pull<4, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 5: return launch_persistent(k_rs_pull<5, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 6: return launch_persistent(k_rs_pull<6, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 7: return launch_persistent(k_rs_pull<7, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 8: return launch_persistent(k_rs_pull<8, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 template <int W, bool kGradBf16>
@@ -596,8 +595,8 @@ cudaError_t launch_pull_bulk_w(const Tile* tiles, int ntiles, PeerPtrs st, float
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_rs_pull_bulk<W, kGradBf16><<<g, kThreads, smem, s>>>(tiles, ntiles, st, grad, ops);
-  return cudaGetLastError();
+  // one wave (launch_persistent): at W = 8 the 64 KB stages allow 3 CTAs per SM, not 4
+  return launch_persistent(k_rs_pull_bulk<W, kGradBf16>, g, smem, s, tiles, ntiles, st, grad, ops);
 }
 
 template <bool kGradBf16>
@@ -634,14 +633,10 @@ cudaError_t launch_unshard_push(const Tile* tiles, int ntiles, const float* shar
   if (ntiles == 0) return cudaSuccess;
   PeerPtrs rot{};   // destination order starts at the next rank: spreads NVLink traffic
   for (int i = 0; i < W; ++i) rot.p[i] = arena.p[(rank + 1 + i) % W];
-  if (cfg.variant & 4) {   // TMA bulk push
-    k_unshard_push_bulk<<<grid_for(ntiles, cfg, fsdpk::kCtasPush), kThreads, 0, st>>>(tiles, ntiles, shard, scales,
-                                                                                        rot, W);
-    return cudaGetLastError();
-  }
-  k_unshard_push<<<grid_for(ntiles, cfg, fsdpk::kCtasPush), kThreads, 0, st>>>(tiles, ntiles, shard, scales, rot,
-                                                                               W, rank);
-  return cudaGetLastError();
+  const int g = grid_for(ntiles, cfg, fsdpk::kCtasPush);
+  if (cfg.variant & 4)   // TMA bulk push
+    return launch_persistent(k_unshard_push_bulk, g, 0, st, tiles, ntiles, shard, scales, rot, W);
+  return launch_persistent(k_unshard_push, g, 0, st, tiles, ntiles, shard, scales, rot, W, rank);
 }
 
 cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool grad_bf16, int divisor, float* grad, bool mean,
@@ -662,8 +657,7 @@ cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool
 cudaError_t launch_gather_copy(const Tile* tiles, int ntiles, const fsdpk::PtrArray& srcs, void* dst,
                                fsdpk::LaunchCfg cfg, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
-  k_gather_copy<<<grid_for(ntiles, cfg), kThreads, 0, st>>>(tiles, ntiles, srcs, (uint8_t*)dst);
-  return cudaGetLastError();
+  return launch_persistent(k_gather_copy, grid_for(ntiles, cfg), 0, st, tiles, ntiles, srcs, (uint8_t*)dst);
 }
 
 }  // namespace fsdpp

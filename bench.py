@@ -367,8 +367,20 @@ def run_ours(args):
     per_launch_bytes = d["bytes"] / max(d["launches"], 1)
     avg_ms = d["ms"] / max(d["launches"], 1)
     achieved = per_launch_bytes / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
+    mech = None
     if dom in nvl_k:
         bound, peak, peak_src = "nvlink", 770.0, "measured peer copy per direction (B200_PROFILING.md; 900 nominal)"
+        # what SM-issued traffic (stores for the push, loads for the pull) reaches in the same
+        # bidirectional / all-to-all pattern on this pool (profiles/nvlink_ceiling.json)
+        try:
+            ceil = json.load(open(os.path.join(ROOT, "profiles", "nvlink_ceiling.json")))
+            tab = ceil["bidir_2gpu"] if W == 2 else ceil["a2a_4gpu"]
+            key = "sm_store" if dom == "unshard_push" else "sm_load"
+            mech = {"mechanism": key, "GBps": tab[key], "frac": round(achieved / tab[key], 4),
+                    "pattern": "bidirectional, 2 GPUs" if W == 2 else "all-to-all, 4 GPUs",
+                    "source": "profiles/nvlink_ceiling.json (scripts/nvlink_probe.cu)"}
+        except (OSError, KeyError, ValueError):
+            mech = None
     else:
         bound = "hbm"
     def ktable(pr, nsteps, step_ms):
@@ -428,6 +440,7 @@ def run_ours(args):
             "roofline": {"bound": bound, "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
                          "bytes_per_launch": int(per_launch_bytes), "traffic": traffic,
+                         "sm_mechanism_ceiling": mech,
                          "pass": f"serial issue, {roof_steps} steps after the timed region (CUDA events on the launching streams)",
                          "step_hbm_GBps": round(step_hbm, 1), "step_hbm_frac": round(step_hbm / measured_peaks()[0], 4)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,

@@ -35,6 +35,10 @@ struct LaunchCfg {
   // kernel-variant bit mask (FSDP_B200_VARIANT): 1 = 16-byte pull loads, 2 = TMA bulk pull,
   // 4 = TMA bulk push, 8 = TMA bulk RS copy-in (K5)
   int variant = 0;
+  // TMA bulk pull: bytes per peer per chunk (power of two, 1-16 KB) and pipeline stages (2-4)
+  // (FSDP_B200_PULL_CHUNK / FSDP_B200_PULL_STAGES)
+  int pull_chunk = 4096;
+  int pull_stages = 2;
   // persistent grid of a kernel whose measured best is `tuned` CTAs per SM
   int cap(int tuned) const { return sms * (per_sm > 0 ? per_sm : tuned); }
 };

@@ -200,6 +200,7 @@ __device__ __forceinline__ uint4 pload16(const uint8_t* p, uint32_t k) {
 struct PullOps {
   float w, inv;
   bool pow2, mean, acc, bf16r;
+  uint32_t chunk, stages;   // bulk pull: bytes per peer per chunk, pipeline stages
   __device__ __forceinline__ float div(float x) const {
     if (!mean) return x;
     return pow2 ? __fmul_rn(x, inv) : __fdiv_rn(x, w);
@@ -366,32 +367,58 @@ __global__ void __launch_bounds__(kThreads) k_rs_pull(const Tile* __restrict__ t
 }
 
 // ------------------------------------------------------------------- TMA bulk variants
-// Pull: the TMA engine brings each rank's chunk (4 KB) of the tile into shared memory
-// (cp.async.bulk global->shared, mbarrier complete_tx, 2 stages), threads reduce from smem.
+// Pull: the TMA engine brings each rank's chunk (LaunchCfg::pull_chunk, 4 KB default) of the
+// tile into shared memory (cp.async.bulk global->shared, mbarrier complete_tx, pull_stages
+// stages), threads reduce from smem.
 // Push: threads cast a 4 KB output chunk into smem once, one thread bulk-stores it into
 // every rank's arena (cp.async.bulk shared->global, W stores per chunk, 2 stages).
 constexpr uint32_t kBulkChunk = 4096;
+constexpr uint32_t kPullMaxStages = 4;
+constexpr size_t kPullMaxSmem = 200 * 1024;   // stages * W * chunk, leaves room for 1 CTA/SM
 
 template <int W, bool kGradBf16>
 __global__ void __launch_bounds__(kThreads) k_rs_pull_bulk(const Tile* __restrict__ tiles, int ntiles, PeerPtrs st,
                                                            float* __restrict__ grad, PullOps ops) {
-  extern __shared__ __align__(128) uint8_t smem[];   // [2][W][kBulkChunk]
-  __shared__ uint64_t full[2];
+  extern __shared__ __align__(128) uint8_t smem[];   // [stages][W][chunk]
+  __shared__ uint64_t full[kPullMaxStages];
   constexpr uint32_t gs = kGradBf16 ? 2 : 4;
-  constexpr uint32_t CE = kBulkChunk / gs;             // elements per chunk
+  const uint32_t chunk = ops.chunk, NS = ops.stages;
+  const uint32_t CE = chunk / gs;                      // elements per chunk
   if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    for (uint32_t s = 0; s < NS; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  uint32_t it = 0;   // chunks consumed by this CTA so far (stage = it & 1, parity = (it >> 1) & 1)
+  // One chunk stream across all of this CTA's tiles: thread 0 keeps the TMA issue cursor NS
+  // chunks ahead of consumption, also across tile boundaries (a per-tile prologue would expose
+  // one NVLink round trip per tile).  Misaligned tiles take the register path and are skipped
+  // by the issue cursor.  consumed / issued count bulk chunks: stage = i % NS, parity (i/NS)&1.
+  auto bulk_ok = [&](const Tile& tl) { return ((tl.src * gs) & 15u) == 0 && ((tl.n * gs) & 15u) == 0; };
+  uint32_t consumed = 0;
+  uint32_t issued = 0, it_c = 0;   // thread 0 only
+  int it_t = blockIdx.x;           // thread 0 only: tile of the next chunk to issue
+  auto advance_issue = [&]() {
+    while (issued < consumed + NS && it_t < ntiles) {
+      const Tile tl = tiles[it_t];
+      if (!bulk_ok(tl)) { it_t += gridDim.x; it_c = 0; continue; }
+      const uint32_t nch = (tl.n + CE - 1) / CE;
+      const uint32_t s = issued % NS;
+      const uint32_t bytes = min(CE, tl.n - it_c * CE) * gs;
+      const uint64_t off = tl.src * gs + (uint64_t)it_c * chunk;
+      mbar_arrive_expect_tx(&full[s], W * bytes);
+#pragma unroll
+      for (int q = 0; q < W; ++q) bulk_g2s(smem + ((size_t)s * W + q) * chunk, st.p[q] + off, bytes, &full[s]);
+      ++issued;
+      if (++it_c == nch) { it_t += gridDim.x; it_c = 0; }
+    }
+  };
+  if (threadIdx.x == 0) advance_issue();
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
     const uint64_t sb = tl.src * gs;
     float* g = grad + tl.dst;
     const uint32_t n = tl.n;
-    if ((sb & 15u) != 0 || ((n * gs) & 15u) != 0) {   // bulk needs 16-byte granularity
+    if (!bulk_ok(tl)) {   // bulk needs 16-byte granularity
       const uint32_t k = (uint32_t)(sb & (kGradBf16 ? 7u : 15u));
       const uint32_t nv = n / 4;
       if (k == 0) pull_body<W, kGradBf16, true>(st, sb, g, nv, 0, ops);
@@ -410,28 +437,16 @@ __global__ void __launch_bounds__(kThreads) k_rs_pull_bulk(const Tile* __restric
       continue;
     }
     const uint32_t nch = (n + CE - 1) / CE;
-    auto issue = [&](uint32_t c, uint32_t i) {
-      const uint32_t s = i & 1u;
-      const uint32_t bytes = min(CE, n - c * CE) * gs;
-      mbar_arrive_expect_tx(&full[s], W * bytes);
-#pragma unroll
-      for (int q = 0; q < W; ++q)
-        bulk_g2s(smem + ((size_t)s * W + q) * kBulkChunk, st.p[q] + sb + (uint64_t)c * kBulkChunk, bytes, &full[s]);
-    };
-    if (threadIdx.x == 0) {
-      issue(0, it);
-      if (nch > 1) issue(1, it + 1);
-    }
     for (uint32_t c = 0; c < nch; ++c) {
-      const uint32_t i = it + c, s = i & 1u;
-      mbar_wait(&full[s], (i >> 1) & 1u);
+      const uint32_t i = consumed, s = i % NS;
+      mbar_wait(&full[s], (i / NS) & 1u);
       const uint32_t ne = min(CE, n - c * CE);
       float* gc = g + (size_t)c * CE;
       for (uint32_t e4 = threadIdx.x; e4 * 4 < ne; e4 += kThreads) {
         float a[4];
 #pragma unroll
         for (int q = 0; q < W; ++q) {
-          const uint8_t* sp = smem + ((size_t)s * W + q) * kBulkChunk + (size_t)e4 * 4 * gs;
+          const uint8_t* sp = smem + ((size_t)s * W + q) * chunk + (size_t)e4 * 4 * gs;
           float x[4];
           if (kGradBf16) {
             const uint2 u = *reinterpret_cast<const uint2*>(sp);
@@ -456,9 +471,9 @@ __global__ void __launch_bounds__(kThreads) k_rs_pull_bulk(const Tile* __restric
         *gp = make_float4(a[0], a[1], a[2], a[3]);
       }
       __syncthreads();   // everyone is done with stage s before the TMA refills it
-      if (threadIdx.x == 0 && c + 2 < nch) issue(c + 2, i + 2);
+      ++consumed;
+      if (threadIdx.x == 0) advance_issue();
     }
-    it += nch;
   }
 }
 
@@ -587,11 +602,15 @@ cudaError_t launch_pull_wv(const Tile* tiles, int ntiles, PeerPtrs st, float* gr
 template <int W, bool kGradBf16>
 cudaError_t launch_pull_bulk_w(const Tile* tiles, int ntiles, PeerPtrs st, float* grad, PullOps ops, int g,
                                cudaStream_t s) {
-  const size_t smem = 2ull * W * kBulkChunk;
+  while ((size_t)ops.stages * W * ops.chunk > kPullMaxSmem) {   // shrink stages, then chunk
+    if (ops.stages > 2) --ops.stages;
+    else ops.chunk /= 2;
+  }
+  const size_t smem = (size_t)ops.stages * W * ops.chunk;
   static bool attr = false;   // one attribute set per instantiation (host, first use)
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_rs_pull_bulk<W, kGradBf16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+                                         (int)kPullMaxSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -649,6 +668,8 @@ cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool
   ops.mean = mean;
   ops.acc = accumulate;
   ops.bf16r = bf16_reduce;
+  ops.chunk = (uint32_t)cfg.pull_chunk;
+  ops.stages = (uint32_t)std::min<int>(std::max(cfg.pull_stages, 2), (int)kPullMaxStages);
   const int g = grid_for(ntiles, cfg);
   return grad_bf16 ? launch_pull_w<true>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant)
                    : launch_pull_w<false>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant);

@@ -67,6 +67,10 @@ def parse():
                          "wait_unshard, bf16 GEMMs x[T, in] @ W_p^T over its gathered 2-D weights, 3 passes "
                          "(6*N*T flops, forward + backward), so prefetch/RS overlap with compute is measured; "
                          "also times the compute alone -> exposed communication")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture the step into a CUDA graph after the warm-up and time its replays (for "
+                         "launch-bound units, e.g. --workload toy); kernel statistics then come from one eager "
+                         "profiled step")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     return ap.parse_args()
 
@@ -280,6 +284,29 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
 
+    timed_step, graph_prof = step, None
+    if args.graph:
+        # one eager profiled step: the per-step kernel counts / bytes (no timing events exist
+        # inside a graph), then capture the step and time graph.replay() instead
+        mesh.profile_enable(True)
+        mesh.profile_read(reset=True)
+        step()
+        comp.synchronize()
+        graph_prof = mesh.profile_read(reset=True)
+        mesh.profile_enable(False)
+        barrier()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=comp):
+            step()
+
+        def timed_step():
+            with torch.cuda.stream(comp):   # replay() launches on the current stream
+                g.replay()
+        for _ in range(args.warmup):
+            timed_step()
+        torch.cuda.synchronize()
+        barrier()
+
     clocks = ClockSampler(list(range(N))) if rank == 0 else None
     if clocks:
         clocks.start()
@@ -290,7 +317,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     evs[0].record(comp)
     for k in range(args.steps):
-        step()
+        timed_step()
         evs[k + 1].record(comp)
     comp.synchronize()
     torch.cuda.synchronize()
@@ -310,6 +337,9 @@ def run_ours(args):
     algbw_rank = bytes_rank / (ms_max * 1e-3) / 1e9
     busbw_rank = algbw_rank * (W - 1) / W
     prof_step = prof
+    if graph_prof is not None:   # replays: one eager step's counts x steps, device time unknown per kernel
+        prof_step = {k: {"launches": v["launches"] * args.steps, "ms": 0.0, "bytes": v["bytes"] * args.steps}
+                     for k, v in graph_prof.items()}
 
     # ---- roofline pass: the same step with every unit issued serially (no prefetch), so
     # no two of our kernels overlap and each kernel's event-timed duration is its own
@@ -430,6 +460,7 @@ def run_ours(args):
                                    f"{'serial' if args.serial else 'prefetch next unit'}",
                        "world_size": N, "shard_size": W, "units": len(layers), "collectives": algo,
                        "step": args.step + (" zero2" if args.zero2 else ""),
+                       "cuda_graph": bool(args.graph),
                        "grads": "layer symmetric grad buffers (zero-copy RS)" if lib_grads else "torch tensors (RS stages them)",
                        "l2": "inputs larger than L2 (every unit's shard/grads/buffers are 100s of MB; 126 MB L2)",
                        "bytes_per_step_per_rank": bytes_rank},

@@ -27,6 +27,15 @@
  *    work previously enqueued on `compute`, and later work on `compute` may consume
  *    the results after the matching fsdp_wait_* call.
  *  - A mesh and its layers are used from one host thread.
+ *  - CUDA graphs: every stream-ordered call (precompute, unshard / wait / reshard,
+ *    reduce-scatter / wait) may be captured while `compute` is capturing (e.g.
+ *    torch.cuda.graph) and the graph replayed on the same stream, provided the same call
+ *    sequence ran eagerly once before the capture (the capture uses the buffers that run
+ *    allocated; pools never grow inside a capture -> FSDP_ERR_STATE) and the capture
+ *    starts after a device synchronize.  P2P handshakes advance device-side epoch
+ *    counters, so every replay re-synchronizes the ranks; every rank must replay the same
+ *    graphs in the same order as its peers, like any collective.  Profiling events are not
+ *    recorded inside a capture.
  *  - Layout: param order is the caller's order; rank r owns rows
  *    [min(r*c, d0), min((r+1)*c, d0)) with c = ceil(d0/W) (trailing ranks may be
  *    empty); the padded shard of param p has n_p = c*rest elements (rest = product of

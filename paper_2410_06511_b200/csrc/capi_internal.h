@@ -151,6 +151,26 @@ struct DevTiles {
   }
 };
 
+// CUDA graph capture state of a stream.  Every stream-ordered call is capturable
+// (include/fsdp_b200.h "CUDA graphs"): while the caller's stream is capturing, pools pick
+// buffers without querying events and never grow, profiling is off, and a pooled buffer's
+// release event is waited on only if it was recorded in the same capture.
+struct Capture {
+  bool on = false;
+  unsigned long long id = 0;
+};
+inline Capture capture_of(cudaStream_t s) {
+  Capture c;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  if (cudaStreamGetCaptureInfo(s, &st, &id) == cudaSuccess && st == cudaStreamCaptureStatusActive) {
+    c.on = true;
+    c.id = id;
+  }
+  cudaGetLastError();
+  return c;
+}
+
 struct Slot {             // one pooled buffer set
   DevBuf a, b;            // AG: a = [W][slot] buffer, b = unsharded arena
                           // RS: a = [W][S] reduce-scatter input, b = staging output [S]
@@ -158,7 +178,25 @@ struct Slot {             // one pooled buffer set
   bool in_use = false;
   bool ever_used = false;
   uint64_t last_use = 0;
+  cudaEvent_t cap_ev = nullptr;        // releases recorded inside a capture (free_ev: eager only)
+  unsigned long long ev_capture = 0;   // capture of the last release (0: eager)
 };
+
+// `st` waits until a pooled buffer's previous user released it.  Eager releases record
+// free_ev; releases inside a capture record cap_ev (an event recorded during a capture
+// cannot be waited on outside it).  Inside a capture, a release recorded outside it is
+// already complete (capture begins after a device synchronize, as torch.cuda.graph does),
+// so only releases from the same capture become graph dependencies.  Eager calls after a
+// replay are ordered after the whole graph by the compute-stream event every call waits on.
+template <class SlotT>
+inline void wait_released(cudaStream_t st, const SlotT* s, const Capture& cap) {
+  if (!s->ever_used) return;
+  if (cap.on) {
+    if (s->ev_capture == cap.id && s->cap_ev) CUDA_CHECK(cudaStreamWaitEvent(st, s->cap_ev, 0));
+    return;
+  }
+  CUDA_CHECK(cudaStreamWaitEvent(st, s->free_ev, 0));
+}
 
 struct ProfRec {
   int kind;
@@ -181,8 +219,9 @@ struct SymSlot {
   cudaEvent_t free_ev = nullptr;
   bool in_use = false;
   bool ever_used = false;
-  uint64_t epoch = 0;
-  int index = 0;
+  cudaEvent_t cap_ev = nullptr;        // releases recorded inside a capture (see wait_released)
+  unsigned long long ev_capture = 0;   // capture of the last release (0: eager)
+  int index = 0;                       // flag slot; handshake epochs live on the device
 };
 
 constexpr int kFlagSlots = 512;  // flag slots per kind: pooled slots first, then layer grad buffers
@@ -247,6 +286,9 @@ struct fsdp_mesh {
   int gbuf_seq = 0;                          // flag slots of layer grad buffers: kPoolSlots + seq
   unsigned long long p2p_timeout_ns = 60ull * 1000 * 1000 * 1000;   // handshake spin bound
   int* d_barrier = nullptr;
+  // handshake epochs [FK_NUM][kFlagSlots], advanced by the handshake kernels themselves so
+  // that a captured CUDA graph signals fresh epochs on every replay
+  unsigned long long* d_epochs = nullptr;
   Allocator allocator;                       // bulk buffers (fsdp_mesh_set_allocator)
 };
 
@@ -292,8 +334,9 @@ namespace fsdpc {
 cudaEvent_t new_event(bool timing = false);
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 void prof_collect(fsdp_mesh* m);
-Slot* acquire_slot(fsdp_mesh* m, std::vector<Slot*>& pool, size_t a_bytes, size_t b_bytes, int min_slots);
-void release_slot(Slot* s, cudaStream_t last_user);
+Slot* acquire_slot(fsdp_mesh* m, std::vector<Slot*>& pool, size_t a_bytes, size_t b_bytes, int min_slots,
+                   const Capture& cap);
+void release_slot(Slot* s, cudaStream_t last_user, const Capture& cap);
 void check_mesh(const fsdp_mesh* m);
 void check_layer(const fsdp_layer* l);
 void check_param(const fsdp_layer* l, int p);
@@ -308,7 +351,9 @@ void sym_free(fsdp_mesh* m, SymBuf& b);
 bool sym_alloc(fsdp_mesh* m, SymBuf& b, size_t bytes);
 fsdpp::FlagPtrs flag_remote(fsdp_mesh* m, int kind, int slot);
 unsigned long long* flag_local(fsdp_mesh* m, int kind, int slot);
-SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t bytes, int prefer = -1);
+unsigned long long* epoch_ctr(fsdp_mesh* m, int kind, int slot);
+SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t bytes, int prefer, const Capture& cap);
+void release_sym_slot(SymSlot* s, cudaStream_t last_user, const Capture& cap);
 fsdpp::PeerPtrs peer_ptrs(const fsdp_mesh* m, const SymBuf& b);
 void p2p_teardown(fsdp_mesh* m);
 void launch_copy_out_all(fsdp_layer* l, bool fp8, const void* ag, void* const* outs, cudaStream_t st);
@@ -328,7 +373,7 @@ struct ProfScope {
   int64_t bytes;
   cudaEvent_t a = nullptr;
   ProfScope(fsdp_mesh* m_, int k, cudaStream_t s, int64_t b) : m(m_), kind(k), st(s), bytes(b) {
-    if (!m->prof) return;
+    if (!m->prof || capture_of(st).on) return;   // no timing events inside a CUDA graph
     a = take();
     CUDA_CHECK(cudaEventRecord(a, st));
   }

@@ -120,6 +120,7 @@ fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* l) {
       else if (l->gbuf_sym) sym_free_local(m, l->gbuf->buf);
       else l->al.release(l->gbuf->buf.local);
       if (l->gbuf->free_ev) cudaEventDestroy(l->gbuf->free_ev);
+      if (l->gbuf->cap_ev) cudaEventDestroy(l->gbuf->cap_ev);
       delete l->gbuf;
       l->gbuf = nullptr;
     }
@@ -182,6 +183,8 @@ static fsdp_status_t precompute_impl(fsdp_mesh_t* m, fsdp_layer_t* const* layers
     std::vector<fsdp_layer*> key(layers, layers + n);
     fsdp_mesh::PreSet* ps = nullptr;
     for (auto* c : m->presets) if (c->layers == key) { ps = c; break; }
+    if (!ps && capture_of(as_stream(stream)).on)
+      fail(FSDP_ERR_STATE, "first precompute of this layer list inside a CUDA graph capture: run it once eagerly first");
     if (!ps) {
       ps = new fsdp_mesh::PreSet();
       ps->layers = key;
@@ -275,18 +278,19 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
     DeviceGuard g(m->device);
     const int64_t sb = slot_bytes(l, fp8);
     const int64_t arena = fp8 ? l->L.arena_fp8 : l->L.arena_bf16;
+    const Capture cap = capture_of(as_stream(compute));
     if (m->algo == FSDP_ALGO_P2P) {
       // fused path: ready handshake -> push (cast + store into every rank's arena) -> done
-      SymSlot* ss = acquire_sym_slot(m, m->p2p_ag, (size_t)arena);
-      const uint64_t epoch = ++ss->epoch;
+      SymSlot* ss = acquire_sym_slot(m, m->p2p_ag, (size_t)arena, -1, cap);
       cudaStream_t cs = as_stream(compute);
       CUDA_CHECK(cudaEventRecord(l->ev_call, cs));
       CUDA_CHECK(cudaStreamWaitEvent(m->s_ag, l->ev_call, 0));
-      if (ss->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_ag, ss->free_ev, 0));
+      wait_released(m->s_ag, ss, cap);
       {
         ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_ag, 0);
         CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_AG_READY, ss->index), flag_local(m, FK_AG_READY, ss->index),
-                                             m->W, m->rank, epoch, m->p2p_timeout_ns, m->d_err, m->s_ag));
+                                             m->W, m->rank, epoch_ctr(m, FK_AG_READY, ss->index), m->p2p_timeout_ns,
+                                             m->d_err, m->s_ag));
         ph.done();
       }
       {
@@ -299,7 +303,8 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
       {
         ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_ag, 0);
         CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_AG_DONE, ss->index), flag_local(m, FK_AG_DONE, ss->index),
-                                             m->W, m->rank, epoch, m->p2p_timeout_ns, m->d_err, m->s_ag));
+                                             m->W, m->rank, epoch_ctr(m, FK_AG_DONE, ss->index), m->p2p_timeout_ns,
+                                             m->d_err, m->s_ag));
         ph.done();
       }
       CUDA_CHECK(cudaEventRecord(l->ev_done, m->s_ag));
@@ -313,11 +318,11 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
     if (m->W == 1) {
       // W = 1: the all-gather is the identity, so the unshard is ONE kernel that casts the
       // shard straight into the unsharded tensors (the push kernel with the local arena only)
-      Slot* slot = acquire_slot(m, m->ag_slots, 0, (size_t)arena, 1);
+      Slot* slot = acquire_slot(m, m->ag_slots, 0, (size_t)arena, 1, cap);
       cudaStream_t cs = as_stream(compute);
       CUDA_CHECK(cudaEventRecord(l->ev_call, cs));
       CUDA_CHECK(cudaStreamWaitEvent(m->s_cin, l->ev_call, 0));
-      if (slot->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_cin, slot->free_ev, 0));
+      wait_released(m->s_cin, slot, cap);
       fsdpp::PeerPtrs pp{};
       pp.p[0] = (uint8_t*)slot->b.p;
       const DevTiles& T = fp8 ? l->t_push_fp8 : l->t_push_bf16;
@@ -336,13 +341,13 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
       l->state = UNSHARDING;
       return;
     }
-    Slot* slot = acquire_slot(m, m->ag_slots, (size_t)(m->W * sb), (size_t)arena, 1);
+    Slot* slot = acquire_slot(m, m->ag_slots, (size_t)(m->W * sb), (size_t)arena, 1, cap);
     cudaStream_t cs = as_stream(compute);
     // copy-in after the caller's prior work (optimizer step on the shard) and after the
     // previous user of this buffer released it
     CUDA_CHECK(cudaEventRecord(l->ev_call, cs));
     CUDA_CHECK(cudaStreamWaitEvent(m->s_cin, l->ev_call, 0));
-    if (slot->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_cin, slot->free_ev, 0));
+    wait_released(m->s_cin, slot, cap);
     uint8_t* ag = (uint8_t*)slot->a.p;
     do_copy_in(l, fp8, scales, ag + (size_t)m->rank * sb, m->s_cin);
     CUDA_CHECK(cudaEventRecord(l->ev_cin, m->s_cin));
@@ -409,18 +414,17 @@ fsdp_status_t fsdp_reshard(fsdp_layer_t* l, void* compute) {
     if (l->state == SHARDED) return;
     DeviceGuard g(l->mesh->device);
     cudaStream_t cs = as_stream(compute);
+    const Capture cap = capture_of(cs);
     if (l->state == UNSHARDING) CUDA_CHECK(cudaStreamWaitEvent(cs, l->ev_done, 0));
     // the buffer is free once everything enqueued on `compute` so far (the consumers of
     // the unsharded params) has run; the next user's copy-in waits on this event
     if (l->p2p_slot) {
       // peers write into this arena only after this rank's next ready handshake on it,
       // which the next unshard issues after waiting on free_ev
-      CUDA_CHECK(cudaEventRecord(l->p2p_slot->free_ev, cs));
-      l->p2p_slot->ever_used = true;
-      l->p2p_slot->in_use = false;
+      release_sym_slot(l->p2p_slot, cs, cap);
       l->p2p_slot = nullptr;
     } else {
-      release_slot(l->slot, cs);
+      release_slot(l->slot, cs, cap);
     }
     l->slot = nullptr;
     l->arena_base = nullptr;
@@ -447,6 +451,7 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
     // replicas, then added to the grad (the all-reduce must not see the old grad)
     const bool via_temp = hsdp && accumulate;
     cudaStream_t cs = as_stream(compute);
+    const Capture cap = capture_of(cs);
     auto replica_all_reduce = [&](float* buf) {
       ProfScope pa(m, FSDP_PROF_ALL_REDUCE, m->s_rs, (int64_t)2 * (m->R - 1) * S * 4 / m->R);
       NCCL_CHECK(ncclAllReduce(buf, buf, (size_t)S, ncclFloat32, ncclSum, m->comm_rep, m->s_rs));
@@ -471,16 +476,15 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
         ss = l->gbuf;
       } else {
         const int prefer = (int)(m->rs_rr++ % 2);   // deterministic round robin: copy of i+1 overlaps pull of i
-        ss = acquire_sym_slot(m, m->p2p_rs, (size_t)(l->stg_elems * gsz), prefer);
+        ss = acquire_sym_slot(m, m->p2p_rs, (size_t)(l->stg_elems * gsz), prefer, cap);
       }
-      Slot* tmp = via_temp ? acquire_slot(m, m->rs_slots, 0, (size_t)(S * 4), 1) : nullptr;
-      const uint64_t epoch = ++ss->epoch;
+      Slot* tmp = via_temp ? acquire_slot(m, m->rs_slots, 0, (size_t)(S * 4), 1, cap) : nullptr;
       CUDA_CHECK(cudaEventRecord(l->ev_rcall, cs));
       if (zc) {
         CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, l->ev_rcall, 0));
       } else {
         CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, l->ev_rcall, 0));
-        if (ss->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, ss->free_ev, 0));
+        wait_released(m->s_rsc, ss, cap);
         {
           const DevTiles& T = gd == FSDP_BFLOAT16 ? l->t_stage_bf16 : l->t_stage_fp32;
           fsdpk::PtrArray pa{};
@@ -494,14 +498,15 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       }
       float* target = l->grad;
       if (via_temp) {
-        if (tmp->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, tmp->free_ev, 0));
+        wait_released(m->s_rs, tmp, cap);
         target = (float*)tmp->b.p;
         CUDA_CHECK(cudaMemsetAsync(target, 0, sizeof(float) * S, m->s_rs));   // padding stays 0
       }
       {
         ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_rs, 0);
         CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_READY, ss->index), flag_local(m, FK_RS_READY, ss->index),
-                                             m->W, m->rank, epoch, m->p2p_timeout_ns, m->d_err, m->s_rs));
+                                             m->W, m->rank, epoch_ctr(m, FK_RS_READY, ss->index), m->p2p_timeout_ns,
+                                             m->d_err, m->s_rs));
         ph.done();
       }
       {
@@ -515,17 +520,16 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       {
         ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_rs, 0);
         CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_DONE, ss->index), flag_local(m, FK_RS_DONE, ss->index),
-                                             m->W, m->rank, epoch, m->p2p_timeout_ns, m->d_err, m->s_rs));
+                                             m->W, m->rank, epoch_ctr(m, FK_RS_DONE, ss->index), m->p2p_timeout_ns,
+                                             m->d_err, m->s_rs));
         ph.done();
       }
-      CUDA_CHECK(cudaEventRecord(ss->free_ev, m->s_rs));
-      ss->ever_used = true;
-      ss->in_use = false;
+      release_sym_slot(ss, m->s_rs, cap);
       if (hsdp) {
         replica_all_reduce(target);
         if (via_temp) {
           add_temp_into_grad(target);
-          release_slot(tmp, m->s_rs);
+          release_slot(tmp, m->s_rs, cap);
         }
       }
       CUDA_CHECK(cudaEventRecord(l->ev_rs_done, m->s_rs));
@@ -538,10 +542,10 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
     const bool need_in = comm_ready(m) || !direct;
     const size_t stage_b = (comm_ready(m) && !direct) ? (size_t)(S * osz) : 0;
     Slot* slot = acquire_slot(m, m->rs_slots, need_in ? (size_t)(m->W * S * osz) : 0,
-                              via_temp ? std::max(stage_b, (size_t)(S * 4)) : stage_b, 2);
+                              via_temp ? std::max(stage_b, (size_t)(S * 4)) : stage_b, 2, cap);
     CUDA_CHECK(cudaEventRecord(l->ev_rcall, cs));
     CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, l->ev_rcall, 0));
-    if (slot->ever_used) CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, slot->free_ev, 0));
+    wait_released(m->s_rsc, slot, cap);
     void* rs_in = need_in ? slot->a.p : (void*)l->grad;
     {
       ProfScope pk(m, FSDP_PROF_RS_COPY_IN, m->s_rsc,
@@ -580,7 +584,7 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       if (hsdp) replica_all_reduce(l->grad);
     }
     CUDA_CHECK(cudaEventRecord(l->ev_rs_done, m->s_rs));
-    release_slot(slot, m->s_rs);
+    release_slot(slot, m->s_rs, cap);
     l->rs_pending = true;
   });
 }

@@ -99,6 +99,8 @@ static void p2p_init(fsdp_mesh* m) {
   if (m->local || m->W < 2 || m->W > 8) return;
   const size_t fbytes = sizeof(unsigned long long) * FK_NUM * kFlagSlots * fsdpp::kMaxRanks;
   m->p2p_ok = sym_alloc(m, m->flags, fbytes);
+  CUDA_CHECK(cudaMalloc(&m->d_epochs, sizeof(unsigned long long) * FK_NUM * kFlagSlots));
+  CUDA_CHECK(cudaMemset(m->d_epochs, 0, sizeof(unsigned long long) * FK_NUM * kFlagSlots));
   const char* env = std::getenv("FSDP_B200_ALGO");
   const bool want_nccl = env && std::string(env) == "nccl";
   m->algo = (m->p2p_ok && !want_nccl) ? FSDP_ALGO_P2P : FSDP_ALGO_NCCL;
@@ -189,6 +191,7 @@ fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
         for (SymSlot* s : *pool) {
           sym_free_local(m, s->buf);
           if (s->free_ev) cudaEventDestroy(s->free_ev);
+          if (s->cap_ev) cudaEventDestroy(s->cap_ev);
           delete s;
         }
         pool->clear();
@@ -196,7 +199,12 @@ fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
       sym_free_local(m, m->flags);
     }
     for (auto* pool : {&m->ag_slots, &m->rs_slots})
-      for (Slot* s : *pool) { s->a.release(); s->b.release(); if (s->free_ev) cudaEventDestroy(s->free_ev); delete s; }
+      for (Slot* s : *pool) {
+        s->a.release(); s->b.release();
+        if (s->free_ev) cudaEventDestroy(s->free_ev);
+        if (s->cap_ev) cudaEventDestroy(s->cap_ev);
+        delete s;
+      }
     clear_presets(m);
     for (auto& r : m->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : m->ev_pool) cudaEventDestroy(e);
@@ -204,6 +212,7 @@ fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
     cudaFree(m->reg_hist); cudaFree(m->reg_pos); cudaFree(m->reg_hinit);
     cudaFree(m->d_err);
     cudaFree(m->d_barrier);
+    cudaFree(m->d_epochs);
     if (m->ev_pre_call) cudaEventDestroy(m->ev_pre_call);
     if (m->ev_pre_done) cudaEventDestroy(m->ev_pre_done);
     if (m->comm_rs) { if (m->aborted) ncclCommAbort(m->comm_rs); else ncclCommDestroy(m->comm_rs); }

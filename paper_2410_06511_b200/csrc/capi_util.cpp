@@ -30,7 +30,20 @@ void prof_collect(fsdp_mesh* m) {
 }
 
 // ---- pools
-Slot* acquire_slot(fsdp_mesh* m, std::vector<Slot*>& pool, size_t a_bytes, size_t b_bytes, int min_slots) {
+Slot* acquire_slot(fsdp_mesh* m, std::vector<Slot*>& pool, size_t a_bytes, size_t b_bytes, int min_slots,
+                   const Capture& cap) {
+  if (cap.on) {   // capturing: least recently used free slot that is big enough; no queries, no growth
+    Slot* best = nullptr;
+    for (Slot* s : pool)
+      if (!s->in_use && s->a.cap >= a_bytes && s->b.cap >= b_bytes && (!best || s->last_use < best->last_use))
+        best = s;
+    if (!best)
+      fail(FSDP_ERR_STATE, "no warm buffer for this call inside a CUDA graph capture: run the same step once "
+                           "eagerly before capturing it");
+    best->in_use = true;
+    best->last_use = ++m->use_seq;
+    return best;
+  }
   Slot* best = nullptr;
   int n_free = 0;
   for (Slot* s : pool) {
@@ -61,11 +74,22 @@ Slot* acquire_slot(fsdp_mesh* m, std::vector<Slot*>& pool, size_t a_bytes, size_
   return best;
 }
 
-void release_slot(Slot* s, cudaStream_t last_user) {
-  CUDA_CHECK(cudaEventRecord(s->free_ev, last_user));
+template <class SlotT>
+static void release_any(SlotT* s, cudaStream_t last_user, const Capture& cap) {
+  if (cap.on) {
+    if (!s->cap_ev) s->cap_ev = new_event();
+    CUDA_CHECK(cudaEventRecord(s->cap_ev, last_user));
+    s->ev_capture = cap.id;
+  } else {
+    CUDA_CHECK(cudaEventRecord(s->free_ev, last_user));
+    s->ev_capture = 0;
+  }
   s->ever_used = true;
   s->in_use = false;
 }
+
+void release_slot(Slot* s, cudaStream_t last_user, const Capture& cap) { release_any(s, last_user, cap); }
+void release_sym_slot(SymSlot* s, cudaStream_t last_user, const Capture& cap) { release_any(s, last_user, cap); }
 
 void check_mesh(const fsdp_mesh* m) {
   if (!m) fail(FSDP_ERR_INVALID_ARGUMENT, "mesh is NULL");
@@ -212,10 +236,26 @@ fsdpp::FlagPtrs flag_remote(fsdp_mesh* m, int kind, int slot) {
 unsigned long long* flag_local(fsdp_mesh* m, int kind, int slot) {
   return (unsigned long long*)m->flags.local + ((size_t)kind * kFlagSlots + slot) * fsdpp::kMaxRanks;
 }
+unsigned long long* epoch_ctr(fsdp_mesh* m, int kind, int slot) {
+  return m->d_epochs + (size_t)kind * kFlagSlots + slot;
+}
 
 // Deterministic choice: the lowest-index free slot (same on every rank, since in_use
-// depends only on the call sequence); grows / creates slots collectively.
-SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t bytes, int prefer) {
+// depends only on the call sequence); grows / creates slots collectively — except while
+// capturing a CUDA graph, where the pool must already be warm.
+SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t bytes, int prefer, const Capture& cap) {
+  if (cap.on) {
+    SymSlot* s = nullptr;
+    if (prefer >= 0 && prefer < (int)pool.size() && !pool[prefer]->in_use && pool[prefer]->buf.bytes >= bytes)
+      s = pool[prefer];
+    for (size_t i = 0; !s && i < pool.size(); ++i)
+      if (!pool[i]->in_use && pool[i]->buf.bytes >= bytes) s = pool[i];
+    if (!s)
+      fail(FSDP_ERR_STATE, "no warm symmetric buffer for this call inside a CUDA graph capture: run the same "
+                           "step once eagerly before capturing it");
+    s->in_use = true;
+    return s;
+  }
   SymSlot* s = nullptr;
   while (prefer >= (int)pool.size() && (int)pool.size() < kPoolSlots) {
     SymSlot* n = new SymSlot();
@@ -258,6 +298,7 @@ void p2p_teardown(fsdp_mesh* m) {
     for (SymSlot* s : *pool) {
       if (s->buf.local || !s->buf.peers.empty()) sym_free(m, s->buf);
       if (s->free_ev) cudaEventDestroy(s->free_ev);
+      if (s->cap_ev) cudaEventDestroy(s->cap_ev);
       delete s;
     }
     pool->clear();

@@ -28,12 +28,14 @@ constexpr int kMaxRanks = 16;
 struct PeerPtrs { uint8_t* p[kMaxRanks]; };
 struct FlagPtrs { unsigned long long* p[kMaxRanks]; };
 
+// epoch = ++*epoch_ctr (device counter of this flag slot: every rank runs the same sequence
+// of handshakes per slot, so the epochs agree, and a replayed CUDA graph advances them).
 // Thread r < W: st.release.sys flags_remote.p[r][my_rank] = epoch (signal rank r), after a
 // system-scope fence; then every thread r < W spins (ld.acquire.sys) until
 // flags_local[r] >= epoch (rank r signalled me).  One CTA.
 // The spin gives up after timeout_ns and writes 2 | (peer << 8) to *err (FSDP_ERR_TIMEOUT).
 cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
-                               unsigned long long epoch, unsigned long long timeout_ns, int* err,
+                               unsigned long long* epoch_ctr, unsigned long long timeout_ns, int* err,
                                cudaStream_t st);
 
 // Push tiles: src = element offset into the fp32 shard, dst = byte offset into the arena,

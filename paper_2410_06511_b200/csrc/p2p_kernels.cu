@@ -30,10 +30,16 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // collective, or died) the kernel records {kind=2 (timeout), peer} in *err and returns, so a
 // protocol error surfaces as FSDP_ERR_TIMEOUT from fsdp_mesh_synchronize instead of a hang.
 __global__ void k_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
-                              unsigned long long epoch, unsigned long long timeout_ns, int* err) {
+                              unsigned long long* epoch_ctr, unsigned long long timeout_ns, int* err) {
+  __shared__ unsigned long long e_sh;
   const int r = threadIdx.x;
+  if (r == 0) {
+    e_sh = *epoch_ctr + 1;
+    *epoch_ctr = e_sh;
+  }
   __threadfence_system();   // order this GPU's earlier stores (previous kernels) before the flag
   __syncthreads();
+  const unsigned long long epoch = e_sh;
 #pragma unroll
   for (int i = 0; i < kMaxRanks; ++i)   // constant indices: remote.p stays in param space
     if (i == r && i < W) st_release_sys(remote.p[i] + rank, epoch);
@@ -641,9 +647,9 @@ cudaError_t launch_pull_w(const Tile* tiles, int ntiles, PeerPtrs st, float* gra
 }  // namespace
 
 cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
-                               unsigned long long epoch, unsigned long long timeout_ns, int* err,
+                               unsigned long long* epoch_ctr, unsigned long long timeout_ns, int* err,
                                cudaStream_t st) {
-  k_signal_wait<<<1, 32, 0, st>>>(remote, local, W, rank, epoch, timeout_ns, err);
+  k_signal_wait<<<1, 32, 0, st>>>(remote, local, W, rank, epoch_ctr, timeout_ns, err);
   return cudaGetLastError();
 }
 

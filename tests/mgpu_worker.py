@@ -62,6 +62,7 @@ def main():
     for algo in algos:
         mesh.set_algo(algo)
         run_checks(mesh, W, rank, local, algo)
+        run_graph_checks(mesh, W, rank, algo)
         # training steps vs the single-device run: bit-exact under P2P (same
         # ascending-rank fp32 order as the reference mean), fp32 tolerance under NCCL
         import toy_train
@@ -77,6 +78,72 @@ def main():
     dist.barrier()
     dist.destroy_process_group()
     print(f"RANK {rank}/{W} OK (algos {algos}, hsdp)", flush=True)
+
+
+def run_graph_checks(mesh, W, rank, algo):
+    """A whole toy step (fp8 precompute + unshard with prefetch + reduce-scatter per unit)
+    captured into a CUDA graph and replayed: P2P handshakes take their epochs from device
+    counters, so replays re-synchronize the ranks; NCCL collectives are captured as graph
+    nodes.  Replays equal the eager step, and after in-place input changes equal the oracle."""
+    import graph_step
+    layers, grads, params = graph_step.setup(F, mesh, rank)
+    s = torch.cuda.Stream()
+    outs = graph_step.outs_for(layers, True)
+    with torch.cuda.stream(s):
+        graph_step.step(F, mesh, layers, grads, s, outs, True)
+    s.synchronize()
+    eager_g = [l.sharded_grad_flat().clone() for l in layers]
+    eager_o = [[o.clone() for o in row] for row in outs]
+    dist.barrier()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        graph_step.step(F, mesh, layers, grads, s, outs, True)
+    for l in layers:
+        l.sharded_grad_flat().zero_()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for l, e in zip(layers, eager_g):
+        if algo == "p2p":
+            assert torch.equal(l.sharded_grad_flat(), e)
+        else:
+            torch.testing.assert_close(l.sharded_grad_flat(), e, rtol=1e-6, atol=1e-12)
+    for row, erow in zip(outs, eager_o):
+        for o, e in zip(row, erow):
+            assert torch.equal(o, e)
+    params = graph_step.refill(layers, grads, params, rank, 700)
+    dist.barrier()
+    g.replay()
+    torch.cuda.synchronize()
+    for ui, l in enumerate(layers):
+        shapes, elig, P2 = params[ui]
+        w = World(shapes, W, elig)
+        sh = w.shard(P2)
+        _, scale = w.precompute_fp8_scales(sh)
+        _, fulls = w.unshard(sh, FP8, scale)
+        for o, want in zip(outs[ui], fulls):
+            got = o.cpu().numpy() if o.dtype == torch.uint8 else u16(o)
+            np.testing.assert_array_equal(got, want)
+        G = [[synth.grad_bf16_bits(ui + 700, p, q, s_) for p, s_ in enumerate(shapes)] for q in range(W)]
+        ref = w.reduce_scatter_grads(G, BF16, True)[rank]
+        for p in range(l.P):
+            check_rs(l.sharded_grad(p).cpu().numpy(), ref, p, W, algo, False, tag=("graph", ui))
+    # eager steps after replays (buffers released inside the capture) still work
+    after_g = [l.sharded_grad_flat().clone() for l in layers]
+    with torch.cuda.stream(s):
+        graph_step.step(F, mesh, layers, grads, s, outs, True)
+    s.synchronize()
+    for l, e in zip(layers, after_g):
+        if algo == "p2p":
+            assert torch.equal(l.sharded_grad_flat(), e)
+        else:
+            torch.testing.assert_close(l.sharded_grad_flat(), e, rtol=1e-6, atol=1e-12)
+    del g
+    torch.cuda.synchronize()
+    for l in layers:
+        l.destroy()
+    mesh.synchronize(120000)
+    print(f"rank {rank}/{W} algo={algo}: CUDA graph replays == eager == oracle OK", flush=True)
 
 
 def run_fault_injection(W, rank, local):

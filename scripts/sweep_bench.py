@@ -49,6 +49,9 @@ def main():
     ap.add_argument("--min-log2", type=int, default=16)
     ap.add_argument("--max-log2", type=int, default=30)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--graph", action="store_true",
+                    help="time CUDA-graph replays of each library op (captured once after the warm-up): the "
+                         "device-side latency alpha without host launch overhead; the NCCL ceiling stays eager")
     args = ap.parse_args()
     W = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
@@ -61,10 +64,20 @@ def main():
     lines = []
     algos = ["p2p", "nccl"] if mesh.algo == "p2p" else ["nccl"]
 
-    def timed(fn):
+    def timed(fn, graph=False):
         for _ in range(3):
             fn()
         comp.synchronize()
+        if graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=comp):
+                fn()
+
+            def fn():   # noqa: F811 (replays on the capture stream)
+                with torch.cuda.stream(comp):
+                    g.replay()
+            fn()
+            comp.synchronize()
         dist.barrier(device_ids=[local])
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(comp)
@@ -98,12 +111,13 @@ def main():
                 F.reduce_scatter_grads(layer, grads, stream=comp)
                 F.fsdp_wait_reduce_scatter(layer, stream=comp)
 
-            ms_u = timed(unshard)
-            ms_r = timed(rs)
+            ms_u = timed(unshard, args.graph)
+            ms_r = timed(rs, args.graph)
             ag_bytes = W * 2 * layer.S
             rs_bytes = W * 4 * layer.S
             busbw = (ag_bytes + rs_bytes) * (W - 1) / W / ((ms_u + ms_r) * 1e-3) / 1e9
-            lines.append({"log2_bytes": lg, "variant": f"fsdp_{algo}", "W": W, "params": len(shapes),
+            lines.append({"log2_bytes": lg, "variant": f"fsdp_{algo}" + ("_graph" if args.graph else ""), "W": W,
+                          "params": len(shapes),
                           "ag_bytes": ag_bytes, "unshard_us": round(ms_u * 1e3, 2), "rs_us": round(ms_r * 1e3, 2),
                           "unshard_busbw_GBps": round(ag_bytes * (W - 1) / W / (ms_u * 1e-3) / 1e9, 1),
                           "rs_busbw_GBps": round(rs_bytes * (W - 1) / W / (ms_r * 1e-3) / 1e9, 1),

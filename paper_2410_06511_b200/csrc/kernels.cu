@@ -18,6 +18,7 @@
 
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <utility>
 
 #include "dev_util.cuh"
@@ -533,14 +534,17 @@ cudaError_t launch_fp8_scale_delayed(const int32_t* idx, int n, uint32_t* acc_bi
 namespace fsdpdev {
 int resident_ctas(const void* fn, size_t dyn_smem) {
   static std::mutex mu;
-  static std::map<std::pair<const void*, size_t>, int> cache;
+  static std::map<std::tuple<const void*, size_t, int>, int> cache;
   std::lock_guard<std::mutex> lock(mu);
-  const auto key = std::make_pair(fn, dyn_smem);
+  int per_sm = 0, dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const auto key = std::make_tuple(fn, dyn_smem, dev);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  int per_sm = 0, dev = 0, sms = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, dyn_smem) != cudaSuccess ||
-      cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
     cudaGetLastError();
     return 0;   // unknown: the caller keeps its grid

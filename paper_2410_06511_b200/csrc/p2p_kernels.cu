@@ -613,12 +613,14 @@ cudaError_t launch_pull_bulk_w(const Tile* tiles, int ntiles, PeerPtrs st, float
     else ops.chunk /= 2;
   }
   const size_t smem = (size_t)ops.stages * W * ops.chunk;
-  static bool attr = false;   // one attribute set per instantiation (host, first use)
-  if (!attr) {
+  static bool attr[64] = {};   // function attributes are per device: set once per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(k_rs_pull_bulk<W, kGradBf16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kPullMaxSmem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   // one wave (launch_persistent): at W = 8 the 64 KB stages allow 3 CTAs per SM, not 4
   return launch_persistent(k_rs_pull_bulk<W, kGradBf16>, g, smem, s, tiles, ntiles, st, grad, ops);

@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--zero2", action="store_true",
                     help="with --step train: reshard_after_forward=False for every block (ZeRO-2, P:636)")
     ap.add_argument("--shard-size", type=int, default=0, help="HSDP: data_parallel_shard_degree (default all ranks)")
+    ap.add_argument("--p2p-rs", default="auto", choices=["auto", "store", "pull"],
+                    help="P2P reduce-scatter mechanism: peers store rows into owners' receive buffers, or owners "
+                         "pull rows from peers' staging (auto = library default)")
     ap.add_argument("--grads", default="auto", choices=["auto", "torch", "library"],
                     help="where the full grads live: torch tensors (the RS stages them), or the layer's "
                          "own symmetric grad buffers (zero-copy; auto = library under P2P)")
@@ -156,7 +159,11 @@ def run_ours(args):
         mesh = F.Mesh(1, 0, local, unique_id=F.get_unique_id())
     if args.algo != "auto" and N > 1:
         mesh.set_algo(args.algo)
+    if args.p2p_rs != "auto" and N > 1:
+        mesh.set_p2p_rs(args.p2p_rs)
     algo = mesh.algo if N > 1 else "local (W=1: identity collectives)"
+    if N > 1 and mesh.algo == "p2p":
+        algo += f" (reduce-scatter: {mesh.p2p_rs})"
     wl = WORKLOADS[args.workload]
     units = unit_lists(wl["model"])
     if wl["cycle"]:   # 70B: cycle `cycle` distinct block instances (memory), SURVEY.md §8(d) row 4
@@ -166,7 +173,8 @@ def run_ours(args):
     # ---- setup: shard (synthetic seeded params written straight into the shards)
     layers, grads = [], []
     gen = torch.Generator(device=dev).manual_seed(241006511 + rank)
-    lib_grads = args.grads == "library" or (args.grads == "auto" and N > 1 and mesh.algo == "p2p")
+    lib_grads = args.grads == "library" or (args.grads == "auto" and N > 1 and mesh.algo == "p2p"
+                                             and mesh.p2p_rs != "store")   # store mode reads any grads
     for ui, (shapes, elig) in enumerate(units):
         l = F.fsdp_shard(mesh, None, elig, shapes=shapes)
         flat = l.sharded_flat()
@@ -389,8 +397,8 @@ def run_ours(args):
     # kernels are NVLink-bound: their bytes are the per-rank NVLink bytes, measured against
     # the measured per-direction peer bandwidth (B200_PROFILING.md: 770 GB/s; 900 nominal).
     peak, peak_src = measured_peaks()
-    hbm_k = ["copy_in", "copy_out", "rs_copy_in", "rs_copy_out", "amax", "scale", "stage_grads"]
-    nvl_k = ["unshard_push", "rs_pull"]
+    hbm_k = ["copy_in", "copy_out", "rs_copy_in", "rs_copy_out", "amax", "scale", "stage_grads", "rs_reduce"]
+    nvl_k = ["unshard_push", "rs_pull", "rs_scatter"]
     ours = hbm_k + nvl_k + ["handshake"]
     dom = max(hbm_k + nvl_k, key=lambda k: prof[k]["ms"])
     d = prof[dom]
@@ -405,7 +413,7 @@ def run_ours(args):
         try:
             ceil = json.load(open(os.path.join(ROOT, "profiles", "nvlink_ceiling.json")))
             tab = ceil["bidir_2gpu"] if W == 2 else ceil["a2a_4gpu"]
-            key = "sm_store" if dom == "unshard_push" else "sm_load"
+            key = "sm_store" if dom in ("unshard_push", "rs_scatter") else "sm_load"
             mech = {"mechanism": key, "GBps": tab[key], "frac": round(achieved / tab[key], 4),
                     "pattern": "bidirectional, 2 GPUs" if W == 2 else "all-to-all, 4 GPUs",
                     "source": "profiles/nvlink_ceiling.json (scripts/nvlink_probe.cu)"}

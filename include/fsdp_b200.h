@@ -117,7 +117,9 @@ typedef enum {
   FSDP_PROF_RS_PULL = 10,      /* P2P: fused chunk + /W + reduce + copy-out    */
   FSDP_PROF_STAGE_GRADS = 11,  /* P2P: caller grads -> symmetric staging       */
   FSDP_PROF_HANDSHAKE = 12,    /* P2P: cross-GPU ready/done flag kernels       */
-  FSDP_PROF_NUM = 13
+  FSDP_PROF_RS_SCATTER = 13,   /* P2P store RS: own grad rows -> peers' receive buffers (NVLink) */
+  FSDP_PROF_RS_REDUCE = 14,    /* P2P store RS: local ascending-rank reduce of the receive buffer */
+  FSDP_PROF_NUM = 15
 } fsdp_prof_kind_t;
 
 /* How the collectives of a mesh run.
@@ -200,6 +202,24 @@ fsdp_status_t fsdp_mesh_info(const fsdp_mesh_t* mesh, int32_t* world_size, int32
  * FSDP_ERR_UNAVAILABLE if P2P is requested but not possible. */
 fsdp_status_t fsdp_mesh_set_algo(fsdp_mesh_t* mesh, int32_t algo);
 fsdp_status_t fsdp_mesh_get_algo(const fsdp_mesh_t* mesh, int32_t* algo);
+
+/* How FSDP_ALGO_P2P reduce-scatters (fsdp_p2p_rs_t; same result bits either way: this
+ * rank's rows, sum over ranks q = 0..W-1 ascending of fp32(g_q) / W in fp32):
+ *  FSDP_P2P_RS_PULL:  every rank stages its full grads into its symmetric staging buffer (or
+ *                     writes them into fsdp_full_grad_buffer) and pulls its rows from all
+ *                     ranks' staging over NVLink (loads);
+ *  FSDP_P2P_RS_STORE: every rank stores each peer's rows of its own grads (read locally, so no
+ *                     staging copy for any caller buffer) into that peer's symmetric receive
+ *                     buffer over NVLink (stores), then reduces its received rows locally on a
+ *                     second stream, overlapping the next unit's transfer.
+ *  FSDP_P2P_RS_AUTO:  PULL when W == 2 and the layer has zero-copy grad buffers
+ *                     (fsdp_full_grad_buffer, created collectively, so every rank decides
+ *                     alike), else STORE — the faster one on 2 and 4 B200s.
+ * Collective (same call on every rank, nothing pending).  Default: FSDP_P2P_RS_AUTO
+ * (environment FSDP_B200_P2P_RS=pull|store|auto overrides). */
+typedef enum { FSDP_P2P_RS_PULL = 0, FSDP_P2P_RS_STORE = 1, FSDP_P2P_RS_AUTO = 2 } fsdp_p2p_rs_t;
+fsdp_status_t fsdp_mesh_set_p2p_rs(fsdp_mesh_t* mesh, int32_t mode);
+fsdp_status_t fsdp_mesh_get_p2p_rs(const fsdp_mesh_t* mesh, int32_t* mode);
 
 /* Waits (host) until every internal stream of the mesh is idle, polling NCCL for
  * asynchronous errors.  Returns FSDP_ERR_NONFINITE if a precompute saw a non-finite
@@ -381,6 +401,18 @@ fsdp_status_t fsdp_stage_grads_to_staging(const fsdp_layer_t* layer, const void*
 fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* layer, const void* const* stagings_dev,
                                  fsdp_dtype_t grad_dtype, fsdp_dtype_t reduce_dtype, int32_t mean,
                                  int32_t accumulate, void* stream);
+/* Store-based reduce-scatter (FSDP_P2P_RS_STORE), sender: for every rank r, this rank's
+ * full-grad rows of r's Shard(0) chunk of each param are copied into r's receive buffer
+ * recv_dev[r] at slot `rank`: recv_r[(rank * S + off_p) + j] (grad_dtype elements; a receive
+ * buffer is W * S elements, every slot laid out like the flat shard).  recv_dev: W pointers
+ * the current device can store to (peer-mapped in the real path). */
+fsdp_status_t fsdp_stage_rs_scatter(const fsdp_layer_t* layer, const void* const* full_grads_dev,
+                                    fsdp_dtype_t grad_dtype, void* const* recv_dev, void* stream);
+/* Store-based reduce-scatter, receiver: for this rank's rows, grad (+)= sum over q = 0..W-1
+ * ascending of fp32(recv[q * S + off_p + j]) / W (mean): the same arithmetic as the pull. */
+fsdp_status_t fsdp_stage_rs_recv_reduce(fsdp_layer_t* layer, const void* recv_dev, fsdp_dtype_t grad_dtype,
+                                        fsdp_dtype_t reduce_dtype, int32_t mean, int32_t accumulate,
+                                        void* stream);
 
 #ifdef __cplusplus
 }

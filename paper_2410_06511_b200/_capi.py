@@ -21,8 +21,10 @@ STATUS = {0: "FSDP_OK", 1: "FSDP_ERR_INVALID_ARGUMENT", 2: "FSDP_ERR_SHAPE", 3: 
           8: "FSDP_ERR_TIMEOUT", 9: "FSDP_ERR_NONFINITE", 10: "FSDP_ERR_UNAVAILABLE"}
 
 PROF_KINDS = ["copy_in", "all_gather", "copy_out", "rs_copy_in", "reduce_scatter", "rs_copy_out",
-              "amax", "scale", "all_reduce", "unshard_push", "rs_pull", "stage_grads", "handshake"]
+              "amax", "scale", "all_reduce", "unshard_push", "rs_pull", "stage_grads", "handshake",
+              "rs_scatter", "rs_reduce"]
 ALGO_NCCL, ALGO_P2P = 0, 1
+P2P_RS_PULL, P2P_RS_STORE, P2P_RS_AUTO = 0, 1, 2
 
 
 class ParamDesc(C.Structure):
@@ -35,7 +37,7 @@ class ParamMeta(C.Structure):
 
 
 class Profile(C.Structure):
-    _fields_ = [("launches", C.c_int64 * 13), ("total_ms", C.c_double * 13), ("bytes", C.c_int64 * 13)]
+    _fields_ = [("launches", C.c_int64 * 15), ("total_ms", C.c_double * 15), ("bytes", C.c_int64 * 15)]
 
 
 class FsdpError(RuntimeError):
@@ -68,6 +70,8 @@ SIGNATURES = {
     "fsdp_mesh_abort": [_VP],
     "fsdp_mesh_set_algo": [_VP, _I32],
     "fsdp_mesh_get_algo": [_VP, C.POINTER(_I32)],
+    "fsdp_mesh_set_p2p_rs": [_VP, _I32],
+    "fsdp_mesh_get_p2p_rs": [_VP, C.POINTER(_I32)],
     "fsdp_profile_enable": [_VP, _I32],
     "fsdp_profile_read": [_VP, C.POINTER(Profile), _I32],
     "fsdp_mesh_set_allocator": [_VP, ALLOC_FN, FREE_FN, _VP],
@@ -102,6 +106,8 @@ SIGNATURES = {
     "fsdp_grad_staging_layout": [_VP, C.POINTER(_I64), C.POINTER(_I64)],
     "fsdp_stage_grads_to_staging": [_VP, _PP, _I32, _VP, _VP],
     "fsdp_stage_rs_pull": [_VP, _PP, _I32, _I32, _I32, _I32, _VP],
+    "fsdp_stage_rs_scatter": [_VP, _PP, _I32, _PP, _VP],
+    "fsdp_stage_rs_recv_reduce": [_VP, _VP, _I32, _I32, _I32, _I32, _VP],
 }
 _OTHER = {
     "fsdp_abi_version": ([], C.c_int32),

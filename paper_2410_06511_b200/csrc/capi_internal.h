@@ -279,6 +279,7 @@ struct fsdp_mesh {
   bool aborted = false;
   // P2P (fused peer-memory) path
   int algo = FSDP_ALGO_NCCL;
+  int p2p_rs_mode = FSDP_P2P_RS_AUTO;        // how the P2P reduce-scatter moves data
   bool p2p_ok = false;
   SymBuf flags;                              // uint64 [FK_NUM][kFlagSlots][kMaxRanks]
   std::vector<SymSlot*> p2p_ag, p2p_rs;      // unsharded arenas, grad staging
@@ -315,9 +316,11 @@ struct fsdp_layer {
   cudaEvent_t ev_rcall = nullptr, ev_k5 = nullptr, ev_rs_done = nullptr;
   // P2P path
   DevTiles t_push_bf16, t_push_fp8, t_pull, t_stage_bf16, t_stage_fp32;
+  DevTiles t_scatter_bf16, t_scatter_fp32, t_recv;   // store-based reduce-scatter
   std::vector<int64_t> stg_off_el;   // full-grad staging: param p at element offset (128-aligned)
   int64_t stg_elems = 0;
   int64_t push_bytes_bf16 = 0, push_bytes_fp8 = 0, pull_elems = 0;
+  int64_t scatter_elems = 0;         // store RS: elements this rank stores into other ranks
   int64_t local_push_bf16 = 0, local_push_fp8 = 0;
   SymSlot* p2p_slot = nullptr;       // arena of the current P2P unshard
   SymSlot* gbuf = nullptr;           // zero-copy full-grad buffer (fsdp_full_grad_buffer)

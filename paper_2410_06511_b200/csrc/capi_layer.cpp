@@ -64,6 +64,9 @@ fsdp_status_t fsdp_shard(fsdp_mesh_t* m, int32_t n, const fsdp_param_desc_t* des
       l->t_pull.upload(fsdpl::tiles_pull(Ly, l->stg_off_el));
       l->t_stage_bf16.upload(fsdpl::tiles_stage(Ly, l->stg_off_el, 2));
       l->t_stage_fp32.upload(fsdpl::tiles_stage(Ly, l->stg_off_el, 4));
+      l->t_scatter_bf16.upload(fsdpl::tiles_scatter(Ly, 2));
+      l->t_scatter_fp32.upload(fsdpl::tiles_scatter(Ly, 4));
+      l->t_recv.upload(fsdpl::tiles_recv_reduce(Ly));
       for (int p = 0; p < n; ++p) {
         const int64_t cnt = Ly.metas[p].row_count * Ly.metas[p].rest;
         const int64_t es8 = Ly.fp8[p] ? 1 : 2;
@@ -72,6 +75,7 @@ fsdp_status_t fsdp_shard(fsdp_mesh_t* m, int32_t n, const fsdp_param_desc_t* des
         l->local_push_bf16 += cnt * (4 + 2);                        // W=1: HBM read + write
         l->local_push_fp8 += cnt * (4 + es8);
         l->pull_elems += cnt;
+        l->scatter_elems += Ly.numel[p] - cnt;                       // the other ranks' rows
       }
       for (int p = 0; p < n; ++p) {
         const int64_t es = Ly.fp8[p] ? 1 : 2;
@@ -115,6 +119,7 @@ fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* l) {
     l->t_cin_fp8.release(); l->t_cout_bf16.release(); l->t_cout_fp8.release(); l->t_rsin.release();
     l->t_push_bf16.release(); l->t_push_fp8.release(); l->t_pull.release(); l->t_stage_bf16.release();
     l->t_stage_fp32.release(); l->t_amax_stage.release();
+    l->t_scatter_bf16.release(); l->t_scatter_fp32.release(); l->t_recv.release();
     if (l->gbuf) {
       if (l->gbuf_sym && !m->aborted) sym_free(m, l->gbuf->buf);   // collective
       else if (l->gbuf_sym) sym_free_local(m, l->gbuf->buf);
@@ -452,16 +457,84 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
     const bool via_temp = hsdp && accumulate;
     cudaStream_t cs = as_stream(compute);
     const Capture cap = capture_of(cs);
-    auto replica_all_reduce = [&](float* buf) {
-      ProfScope pa(m, FSDP_PROF_ALL_REDUCE, m->s_rs, (int64_t)2 * (m->R - 1) * S * 4 / m->R);
-      NCCL_CHECK(ncclAllReduce(buf, buf, (size_t)S, ncclFloat32, ncclSum, m->comm_rep, m->s_rs));
+    auto replica_all_reduce = [&](float* buf, cudaStream_t st) {
+      ProfScope pa(m, FSDP_PROF_ALL_REDUCE, st, (int64_t)2 * (m->R - 1) * S * 4 / m->R);
+      NCCL_CHECK(ncclAllReduce(buf, buf, (size_t)S, ncclFloat32, ncclSum, m->comm_rep, st));
       pa.done();
     };
-    auto add_temp_into_grad = [&](const float* T) {
-      ProfScope po(m, FSDP_PROF_RS_COPY_OUT, m->s_rs, S * 12);
-      CUDA_CHECK(fsdpk::launch_rs_copy_out(T, false, l->grad, true, S, m->cfg, m->s_rs));
+    auto add_temp_into_grad = [&](const float* T, cudaStream_t st) {
+      ProfScope po(m, FSDP_PROF_RS_COPY_OUT, st, S * 12);
+      CUDA_CHECK(fsdpk::launch_rs_copy_out(T, false, l->grad, true, S, m->cfg, st));
       po.done();
     };
+    // P2P mechanism: identical on every rank (the mode is set collectively; the layer's
+    // zero-copy buffer exists on all ranks or none)
+    const bool p2p_store = m->p2p_rs_mode == FSDP_P2P_RS_STORE ||
+                           (m->p2p_rs_mode == FSDP_P2P_RS_AUTO && !(m->W == 2 && l->gbuf && l->gbuf_sym));
+    if (m->algo == FSDP_ALGO_P2P && p2p_store) {
+      // store-based path: ready handshake (this rank's receive buffer is free) -> scatter
+      // (this rank's rows of every rank's chunk, read from the caller's grads, stored into
+      // each rank's receive buffer over NVLink) -> done handshake (every rank's rows arrived)
+      // on s_rs; then the local ascending-rank reduce on s_rsc, which overlaps the next
+      // unit's scatter on s_rs.  The receive buffer is free again after the reduce.
+      const int64_t gsz = dtype_size(gd);
+      const int prefer = (int)(m->rs_rr++ % 2);
+      SymSlot* ss = acquire_sym_slot(m, m->p2p_rs, (size_t)(m->W * S * gsz), prefer, cap);
+      Slot* tmp = via_temp ? acquire_slot(m, m->rs_slots, 0, (size_t)(S * 4), 1, cap) : nullptr;
+      CUDA_CHECK(cudaEventRecord(l->ev_rcall, cs));
+      CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, l->ev_rcall, 0));
+      wait_released(m->s_rs, ss, cap);
+      {
+        ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_rs, 0);
+        CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_READY, ss->index), flag_local(m, FK_RS_READY, ss->index),
+                                             m->W, m->rank, epoch_ctr(m, FK_RS_READY, ss->index), m->p2p_timeout_ns,
+                                             m->d_err, m->s_rs));
+        ph.done();
+      }
+      {
+        const DevTiles& T = gd == FSDP_BFLOAT16 ? l->t_scatter_bf16 : l->t_scatter_fp32;
+        fsdpk::PtrArray pa{};
+        for (int p = 0; p < l->P; ++p) pa.p[p] = grads[p];
+        ProfScope pp(m, FSDP_PROF_RS_SCATTER, m->s_rs, l->scatter_elems * gsz);
+        CUDA_CHECK(fsdpp::launch_rs_scatter(T.d, T.n, pa, peer_ptrs(m, ss->buf), m->cfg, m->s_rs));
+        pp.done();
+      }
+      {
+        ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_rs, 0);
+        CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_DONE, ss->index), flag_local(m, FK_RS_DONE, ss->index),
+                                             m->W, m->rank, epoch_ctr(m, FK_RS_DONE, ss->index), m->p2p_timeout_ns,
+                                             m->d_err, m->s_rs));
+        ph.done();
+      }
+      CUDA_CHECK(cudaEventRecord(l->ev_k5, m->s_rs));
+      CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, l->ev_k5, 0));
+      float* target = l->grad;
+      if (via_temp) {
+        wait_released(m->s_rsc, tmp, cap);
+        target = (float*)tmp->b.p;
+        CUDA_CHECK(cudaMemsetAsync(target, 0, sizeof(float) * S, m->s_rsc));   // padding stays 0
+      }
+      {
+        fsdpp::PeerPtrs slots{};
+        for (int q = 0; q < m->W; ++q) slots.p[q] = (uint8_t*)ss->buf.local + (size_t)q * S * gsz;
+        const bool acc = accumulate != 0 && !hsdp;
+        ProfScope pr(m, FSDP_PROF_RS_REDUCE, m->s_rsc, l->pull_elems * (m->W * gsz + 4 + (acc ? 4 : 0)));
+        CUDA_CHECK(fsdpp::launch_rs_pull(l->t_recv.d, l->t_recv.n, slots, gd == FSDP_BFLOAT16, divisor, target,
+                                         mean != 0, acc, obf, m->W, m->cfg, m->s_rsc));
+        pr.done();
+      }
+      release_sym_slot(ss, m->s_rsc, cap);
+      if (hsdp) {
+        replica_all_reduce(target, m->s_rsc);
+        if (via_temp) {
+          add_temp_into_grad(target, m->s_rsc);
+          release_slot(tmp, m->s_rsc, cap);
+        }
+      }
+      CUDA_CHECK(cudaEventRecord(l->ev_rs_done, m->s_rsc));
+      l->rs_pending = true;
+      return;
+    }
     if (m->algo == FSDP_ALGO_P2P) {
       // fused path: stage the caller's grads into this rank's symmetric staging -> ready
       // handshake -> pull (every rank's rows of this rank, /divisor, ascending-rank fp32 sum,
@@ -526,9 +599,9 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       }
       release_sym_slot(ss, m->s_rs, cap);
       if (hsdp) {
-        replica_all_reduce(target);
+        replica_all_reduce(target, m->s_rs);
         if (via_temp) {
-          add_temp_into_grad(target);
+          add_temp_into_grad(target, m->s_rs);
           release_slot(tmp, m->s_rs, cap);
         }
       }
@@ -573,15 +646,15 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
         CUDA_CHECK(fsdpk::launch_rs_copy_out(rs_out, obf, T, false, S, m->cfg, m->s_rs));
         po.done();
       }
-      replica_all_reduce(T);
-      add_temp_into_grad(T);
+      replica_all_reduce(T, m->s_rs);
+      add_temp_into_grad(T, m->s_rs);
     } else {
       if (!direct) {
         ProfScope po(m, FSDP_PROF_RS_COPY_OUT, m->s_rs, S * (osz + 4 + (accumulate ? 4 : 0)));
         CUDA_CHECK(fsdpk::launch_rs_copy_out(rs_out, obf, l->grad, accumulate != 0, S, m->cfg, m->s_rs));
         po.done();
       }
-      if (hsdp) replica_all_reduce(l->grad);
+      if (hsdp) replica_all_reduce(l->grad, m->s_rs);
     }
     CUDA_CHECK(cudaEventRecord(l->ev_rs_done, m->s_rs));
     release_slot(slot, m->s_rs, cap);

@@ -106,6 +106,9 @@ static void p2p_init(fsdp_mesh* m) {
   m->algo = (m->p2p_ok && !want_nccl) ? FSDP_ALGO_P2P : FSDP_ALGO_NCCL;
   if (const char* t = std::getenv("FSDP_B200_P2P_TIMEOUT_MS"))
     m->p2p_timeout_ns = (unsigned long long)std::max(1L, std::atol(t)) * 1000000ull;
+  if (const char* r = std::getenv("FSDP_B200_P2P_RS"))
+    m->p2p_rs_mode = std::string(r) == "pull" ? FSDP_P2P_RS_PULL
+                     : std::string(r) == "store" ? FSDP_P2P_RS_STORE : FSDP_P2P_RS_AUTO;
 }
 
 static fsdp_status_t mesh_init_impl(const uint8_t* id, int32_t W, int32_t rank, int32_t dev, bool local,
@@ -261,6 +264,24 @@ fsdp_status_t fsdp_mesh_get_algo(const fsdp_mesh_t* m, int32_t* algo) {
   return guarded([&] {
     if (!m || !algo) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL argument");
     *algo = m->algo;
+  });
+}
+
+fsdp_status_t fsdp_mesh_set_p2p_rs(fsdp_mesh_t* m, int32_t mode) {
+  return guarded([&] {
+    check_mesh(m);
+    if (mode != FSDP_P2P_RS_PULL && mode != FSDP_P2P_RS_STORE && mode != FSDP_P2P_RS_AUTO)
+      fail(FSDP_ERR_INVALID_ARGUMENT, "unknown P2P reduce-scatter mode");
+    for (auto* l : m->layers)
+      if (l->rs_pending) fail(FSDP_ERR_STATE, "a layer has a pending reduce-scatter");
+    m->p2p_rs_mode = mode;
+  });
+}
+
+fsdp_status_t fsdp_mesh_get_p2p_rs(const fsdp_mesh_t* m, int32_t* mode) {
+  return guarded([&] {
+    if (!m || !mode) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL argument");
+    *mode = m->p2p_rs_mode;
   });
 }
 

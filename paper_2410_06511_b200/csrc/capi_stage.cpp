@@ -190,4 +190,48 @@ fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* l, const void* const* stagings, f
   });
 }
 
+fsdp_status_t fsdp_stage_rs_scatter(const fsdp_layer_t* lc, const void* const* grads, fsdp_dtype_t gd,
+                                    void* const* recv, void* stream) {
+  return guarded([&] {
+    fsdp_layer* l = const_cast<fsdp_layer*>(lc);
+    check_layer(l);
+    fsdp_mesh* m = l->mesh;
+    if (m->W > 8) fail(FSDP_ERR_UNAVAILABLE, "the store-based reduce-scatter supports W <= 8");
+    validate_grads(l, grads, gd, FSDP_FLOAT32);
+    if (!recv) fail(FSDP_ERR_INVALID_ARGUMENT, "recv_dev is NULL");
+    fsdpp::PeerPtrs pp{};
+    for (int r = 0; r < m->W; ++r) {
+      if (!recv[r]) fail(FSDP_ERR_INVALID_ARGUMENT, "recv_dev[r] is NULL");
+      pp.p[r] = (uint8_t*)recv[r];
+    }
+    fsdpk::PtrArray pa{};
+    for (int p = 0; p < l->P; ++p) pa.p[p] = grads[p];
+    const DevTiles& T = gd == FSDP_BFLOAT16 ? l->t_scatter_bf16 : l->t_scatter_fp32;
+    DeviceGuard g(m->device);
+    ProfScope ps(m, FSDP_PROF_RS_SCATTER, as_stream(stream), l->scatter_elems * dtype_size(gd));
+    CUDA_CHECK(fsdpp::launch_rs_scatter(T.d, T.n, pa, pp, m->cfg, as_stream(stream)));
+    ps.done();
+  });
+}
+
+fsdp_status_t fsdp_stage_rs_recv_reduce(fsdp_layer_t* l, const void* recv, fsdp_dtype_t gd, fsdp_dtype_t rd,
+                                        int32_t mean, int32_t accumulate, void* stream) {
+  return guarded([&] {
+    check_layer(l);
+    fsdp_mesh* m = l->mesh;
+    if (m->W > 8) fail(FSDP_ERR_UNAVAILABLE, "the store-based reduce-scatter supports W <= 8");
+    if (!recv) fail(FSDP_ERR_INVALID_ARGUMENT, "recv_dev is NULL");
+    if (gd != FSDP_BFLOAT16 && gd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "grad_dtype must be BFLOAT16 or FLOAT32");
+    if (rd != FSDP_BFLOAT16 && rd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "reduce_dtype must be FLOAT32 or BFLOAT16");
+    const int64_t gsz = dtype_size(gd);
+    fsdpp::PeerPtrs slots{};
+    for (int q = 0; q < m->W; ++q) slots.p[q] = (uint8_t*)recv + (size_t)q * l->L.S * gsz;
+    DeviceGuard g(m->device);
+    ProfScope ps(m, FSDP_PROF_RS_REDUCE, as_stream(stream), l->pull_elems * (m->W * gsz + 4));
+    CUDA_CHECK(fsdpp::launch_rs_pull(l->t_recv.d, l->t_recv.n, slots, gd == FSDP_BFLOAT16, m->W * m->R, l->grad,
+                                     mean != 0, accumulate != 0, rd == FSDP_BFLOAT16, m->W, m->cfg, as_stream(stream)));
+    ps.done();
+  });
+}
+
 }  // extern "C"

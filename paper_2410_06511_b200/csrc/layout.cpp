@@ -224,6 +224,57 @@ std::vector<fsdpk::Tile> tiles_pull(const Layout& L, const std::vector<int64_t>&
   return t;
 }
 
+std::vector<fsdpk::Tile> tiles_scatter(const Layout& L, int64_t gsize) {
+  // per-destination lists, then merged round robin: a persistent grid walks the table in
+  // order, so every destination (and this rank's own slot, a local copy) is in flight at
+  // once instead of one destination after another
+  std::vector<std::vector<fsdpk::Tile>> per(L.W);
+  for (int i = 0; i < L.W; ++i) {
+    const int r = (L.rank + 1 + i) % L.W;   // destination rank, rotated per sender
+    for (size_t p = 0; p < L.metas.size(); ++p) {
+      const auto& m = L.metas[p];
+      const int64_t b = std::min<int64_t>((int64_t)r * m.chunk_rows, m.dim0);
+      const int64_t e = std::min<int64_t>((int64_t)(r + 1) * m.chunk_rows, m.dim0);
+      const int64_t bytes = (e - b) * m.rest * gsize;
+      for (int64_t j = 0; j < bytes; j += fsdpk::kTileBytes) {
+        fsdpk::Tile x{};
+        x.src = (uint64_t)(b * m.rest * gsize + j);
+        x.dst = (uint64_t)(((int64_t)L.rank * L.S + m.elem_offset) * gsize + j);
+        x.n = (uint32_t)std::min<int64_t>(fsdpk::kTileBytes, bytes - j);
+        x.param = (uint32_t)p;
+        x.kind = fsdpk::TK_COPY;
+        x.pad = (uint32_t)r;
+        per[i].push_back(x);
+      }
+    }
+  }
+  std::vector<fsdpk::Tile> t;
+  size_t longest = 0;
+  for (const auto& v : per) longest = std::max(longest, v.size());
+  for (size_t k = 0; k < longest; ++k)
+    for (const auto& v : per)
+      if (k < v.size()) t.push_back(v[k]);
+  return t;
+}
+
+std::vector<fsdpk::Tile> tiles_recv_reduce(const Layout& L) {
+  std::vector<fsdpk::Tile> t;
+  for (size_t p = 0; p < L.metas.size(); ++p) {
+    const auto& m = L.metas[p];
+    const int64_t cnt = m.row_count * m.rest;
+    for (int64_t j = 0; j < cnt; j += fsdpk::kTileElems) {
+      fsdpk::Tile x{};
+      x.src = (uint64_t)(m.elem_offset + j);
+      x.dst = (uint64_t)(m.elem_offset + j);
+      x.n = (uint32_t)std::min<int64_t>(fsdpk::kTileElems, cnt - j);
+      x.param = (uint32_t)p;
+      x.kind = fsdpk::TK_COPY;
+      t.push_back(x);
+    }
+  }
+  return t;
+}
+
 std::vector<fsdpk::Tile> tiles_stage(const Layout& L, const std::vector<int64_t>& stg_off, int64_t gsize) {
   std::vector<fsdpk::Tile> t;
   for (size_t p = 0; p < L.metas.size(); ++p) {

@@ -55,5 +55,13 @@ std::vector<fsdpk::Tile> tiles_push(const Layout& L, bool fp8);
 std::vector<fsdpk::Tile> tiles_pull(const Layout& L, const std::vector<int64_t>& stg_off);
 // Staging gather: src = byte offset in grads[param], dst = byte offset in the staging.
 std::vector<fsdpk::Tile> tiles_stage(const Layout& L, const std::vector<int64_t>& stg_off, int64_t gsize);
+// Store-based reduce-scatter, sender side: for every destination rank r (rotated from
+// rank + 1), this rank's full-grad rows of r's Shard(0) chunk of each param go into r's
+// receive buffer [W][S] at slot `rank`: src = byte offset into grads[param], dst = byte
+// offset (rank * S + off_p) * gsize + j, pad = r.
+std::vector<fsdpk::Tile> tiles_scatter(const Layout& L, int64_t gsize);
+// Store-based reduce-scatter, receiver side: this rank's rows, src = dst = element offset
+// off_p + j (the same in every slot of the receive buffer and in the fp32 grad).
+std::vector<fsdpk::Tile> tiles_recv_reduce(const Layout& L);
 
 }  // namespace fsdpl

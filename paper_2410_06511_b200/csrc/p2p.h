@@ -55,4 +55,10 @@ cudaError_t launch_rs_pull(const fsdpk::Tile* tiles, int ntiles, PeerPtrs stagin
 cudaError_t launch_gather_copy(const fsdpk::Tile* tiles, int ntiles, const fsdpk::PtrArray& srcs,
                                void* dst, fsdpk::LaunchCfg cfg, cudaStream_t st);
 
+// Store-based reduce-scatter, sender (layout.h tiles_scatter): dests.p[tile.pad] + tile.dst <-
+// grads.p[param] + tile.src, n bytes; ends with a system-scope fence.  The receiver then
+// reduces its [W][S] receive buffer with launch_rs_pull (every "peer" pointer local).
+cudaError_t launch_rs_scatter(const fsdpk::Tile* tiles, int ntiles, const fsdpk::PtrArray& grads, PeerPtrs dests,
+                              fsdpk::LaunchCfg cfg, cudaStream_t st);
+
 }  // namespace fsdpp

@@ -583,6 +583,35 @@ __global__ void __launch_bounds__(kThreads) k_gather_copy(const Tile* __restrict
   }
 }
 
+// ------------------------------------------------------------------- store-based RS, sender
+// Each tile copies this rank's full-grad rows of one destination rank's chunk (local reads,
+// misaligned phases realigned like K4) into that rank's receive buffer over NVLink (16-byte
+// stores: the store mechanism runs at ~700 GB/s both ways vs ~660 for loads,
+// profiles/nvlink_ceiling.json).
+__global__ void __launch_bounds__(kThreads) k_rs_scatter(const Tile* __restrict__ tiles, int ntiles,
+                                                         fsdpk::PtrArray grads, PeerPtrs dests) {
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    uint8_t* base = nullptr;
+#pragma unroll
+    for (int i = 0; i < kMaxRanks; ++i)   // constant indices: dests stays in param space
+      if (i == (int)tl.pad) base = dests.p[i];
+    const uint8_t* s = (const uint8_t*)grads.p[tl.param] + tl.src;
+    uint8_t* d = base + tl.dst;
+    uint32_t n = tl.n;
+    uint32_t head = (uint32_t)((16u - ((uintptr_t)d & 15u)) & 15u);
+    if (head > n) head = n;
+    if (threadIdx.x < head) d[threadIdx.x] = s[threadIdx.x];
+    s += head; d += head; n -= head;
+    const uint32_t nv = n >> 4;
+    const uint32_t k = (uint32_t)((uintptr_t)s & 15u);
+    if (k == 0) copy_body<true>(s, d, nv, 0);
+    else copy_body<false>(s, d, nv, k);
+    for (uint32_t e = nv * 16 + threadIdx.x; e < n; e += kThreads) d[e] = s[e];
+  }
+  __threadfence_system();
+}
+
 inline int grid_for(int64_t items, fsdpk::LaunchCfg cfg, int tuned = fsdpk::kCtasCopy) {
   const int64_t cap = cfg.cap(tuned);
   int64_t g = items < cap ? items : cap;
@@ -687,6 +716,13 @@ cudaError_t launch_gather_copy(const Tile* tiles, int ntiles, const fsdpk::PtrAr
                                fsdpk::LaunchCfg cfg, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
   return launch_persistent(k_gather_copy, grid_for(ntiles, cfg), 0, st, tiles, ntiles, srcs, (uint8_t*)dst);
+}
+
+cudaError_t launch_rs_scatter(const Tile* tiles, int ntiles, const fsdpk::PtrArray& grads, PeerPtrs dests,
+                              fsdpk::LaunchCfg cfg, cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  return launch_persistent(k_rs_scatter, grid_for(ntiles, cfg, fsdpk::kCtasPush), 0, st, tiles, ntiles, grads,
+                           dests);
 }
 
 }  // namespace fsdpp

@@ -182,6 +182,21 @@ class Mesh:
         """Collective: 'nccl' (copy-in -> NCCL -> copy-out) or 'p2p' (fused NVLink kernels)."""
         call("fsdp_mesh_set_algo", self.handle, capi.ALGO_P2P if algo == "p2p" else capi.ALGO_NCCL)
 
+    @property
+    def p2p_rs(self) -> str:
+        a = C.c_int32()
+        call("fsdp_mesh_get_p2p_rs", self.handle, C.byref(a))
+        return {capi.P2P_RS_STORE: "store", capi.P2P_RS_PULL: "pull"}.get(a.value, "auto")
+
+    def set_p2p_rs(self, mode: str):
+        """Collective: how the P2P reduce-scatter moves data — 'store' (peers store rows into
+        each owner's receive buffer, local reduce), 'pull' (owners load rows from peers) or
+        'auto' (pull at W = 2 for layers with zero-copy grad buffers, else store)."""
+        codes = {"store": capi.P2P_RS_STORE, "pull": capi.P2P_RS_PULL, "auto": capi.P2P_RS_AUTO}
+        if mode not in codes:
+            raise ValueError("mode must be 'store', 'pull' or 'auto'")
+        call("fsdp_mesh_set_p2p_rs", self.handle, codes[mode])
+
     def synchronize(self, timeout_ms: int = 0):
         call("fsdp_mesh_synchronize", self.handle, int(timeout_ms))
 
@@ -470,4 +485,18 @@ def stage_grads_to_staging(layer: Layer, grads: Sequence[torch.Tensor], staging:
 def stage_rs_pull(layer: Layer, stagings: Sequence[torch.Tensor], grad_dtype, reduce_dtype=torch.float32,
                   mean: bool = True, accumulate: bool = False, stream=None):
     call("fsdp_stage_rs_pull", layer.handle, _ptr_array(stagings), _dtype_code(grad_dtype),
+         _dtype_code(reduce_dtype), int(bool(mean)), int(bool(accumulate)), _stream(stream))
+
+
+def stage_rs_scatter(layer: Layer, grads: Sequence[torch.Tensor], recvs: Sequence[torch.Tensor], stream=None):
+    """Store RS sender: this rank's rows of every rank r's chunk -> recvs[r] at slot `rank`
+    (each receive buffer: W * S elements of the grads' dtype)."""
+    call("fsdp_stage_rs_scatter", layer.handle, _ptr_array(grads), _dtype_code(grads[0].dtype),
+         _ptr_array(recvs), _stream(stream))
+
+
+def stage_rs_recv_reduce(layer: Layer, recv: torch.Tensor, grad_dtype, reduce_dtype=torch.float32,
+                         mean: bool = True, accumulate: bool = False, stream=None):
+    """Store RS receiver: grad (+)= ascending-rank fp32 sum over the W slots of recv / W."""
+    call("fsdp_stage_rs_recv_reduce", layer.handle, C.c_void_p(recv.data_ptr()), _dtype_code(grad_dtype),
          _dtype_code(reduce_dtype), int(bool(mean)), int(bool(accumulate)), _stream(stream))

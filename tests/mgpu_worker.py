@@ -61,8 +61,13 @@ def main():
     algos = ["p2p", "nccl"] if mesh.algo == "p2p" else ["nccl"]
     for algo in algos:
         mesh.set_algo(algo)
-        run_checks(mesh, W, rank, local, algo)
-        run_graph_checks(mesh, W, rank, algo)
+        for rs_mode in (["store", "pull"] if algo == "p2p" else ["-"]):
+            if algo == "p2p":
+                mesh.set_p2p_rs(rs_mode)   # both P2P reduce-scatter mechanisms, same result bits
+            run_checks(mesh, W, rank, local, algo)
+            run_graph_checks(mesh, W, rank, algo)
+            if algo == "p2p":
+                print(f"rank {rank}/{W} p2p reduce-scatter mode {rs_mode}: OK", flush=True)
         # training steps vs the single-device run: bit-exact under P2P (same
         # ascending-rank fp32 order as the reference mean), fp32 tolerance under NCCL
         import toy_train

@@ -108,3 +108,68 @@ def test_rs_pull_emulated(kind, seed, W, gd, rd, mean, acc):
             np.testing.assert_array_equal(flat[~real].view(np.uint32), old[r][~real].view(np.uint32))
     finally:
         emu.close()
+
+
+@pytest.mark.parametrize("kind,seed", KINDS)
+@pytest.mark.parametrize("W", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("gd,rd,mean,acc", [(BF16, FP32, True, False), (FP32, FP32, True, False),
+                                            (BF16, FP32, False, False), (BF16, FP32, True, True),
+                                            (BF16, BF16, True, False)])
+def test_rs_store_emulated(kind, seed, W, gd, rd, mean, acc):
+    """Store-based reduce-scatter (FSDP_P2P_RS_STORE): every rank's scatter kernel writes its
+    rows of rank r's chunk into r's receive buffer at slot q (bytes checked, guard bands
+    untouched), then every rank's local reduce gives the same bits as the pull."""
+    shapes, elig = _unit(kind, seed, W)
+    w = World(shapes, W, elig)
+    emu = Emu(shapes, elig, W, _params(shapes, seed))
+    try:
+        if gd == BF16:
+            G = [[synth.grad_bf16_bits(seed, p, q, s) for p, s in enumerate(shapes)] for q in range(W)]
+            GT = [[torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16) for x in g] for g in G]
+            tdt, es = torch.bfloat16, 2
+        else:
+            G = [[synth.grad_fp32(seed, p, q, s) for p, s in enumerate(shapes)] for q in range(W)]
+            GT = [[torch.from_numpy(x).cuda() for x in g] for g in G]
+            tdt, es = torch.float32, 4
+        S = emu.layers[0].S
+        nbytes = W * S * es
+        recv = [torch.full((nbytes + 64,), 0x5A, dtype=torch.uint8, device="cuda") for _ in range(W)]
+        for q in range(W):
+            F.stage_rs_scatter(emu.layers[q], GT[q], recv)
+        torch.cuda.synchronize()
+        for r in range(W):   # slot q of rank r's buffer holds rank q's rows of r's chunk, nothing else
+            a = recv[r].cpu().numpy()
+            written = np.zeros(a.size, dtype=bool)
+            for q in range(W):
+                for p, m in enumerate(emu.layers[r].metas):
+                    cnt = m["row_count"] * m["rest"]
+                    lo = (q * S + m["elem_offset"]) * es
+                    want = GT[q][p].reshape(-1)[m["row_begin"] * m["rest"]:m["row_begin"] * m["rest"] + cnt]
+                    np.testing.assert_array_equal(a[lo:lo + cnt * es], want.view(torch.uint8).cpu().numpy())
+                    written[lo:lo + cnt * es] = True
+            assert np.all(a[~written] == 0x5A)
+        rng = np.random.default_rng(seed)
+        old = [rng.standard_normal(l.S).astype(np.float32) for l in emu.layers]
+        for r, l in enumerate(emu.layers):
+            l.sharded_grad_flat().copy_(torch.from_numpy(old[r]).cuda())
+            F.stage_rs_recv_reduce(l, recv[r], tdt, torch.float32 if rd == FP32 else torch.bfloat16, mean, acc)
+        torch.cuda.synchronize()
+        ref = w.reduce_scatter_grads(G, gd, mean, reduce_dtype=rd)
+        for r, l in enumerate(emu.layers):
+            for p in range(len(shapes)):
+                want = ref[r]["order"][p]
+                if rd == BF16:
+                    want = bf16_bits_to_f32(bf16_rne_bits(want.reshape(-1))).reshape(want.shape)
+                got = l.sharded_grad(p).cpu().numpy()
+                if acc:
+                    m = l.metas[p]
+                    prev = old[r][m["elem_offset"]:m["elem_offset"] + got.size].reshape(got.shape)
+                    want = (prev + want).astype(np.float32)
+                np.testing.assert_array_equal(got.view(np.uint32), want.astype(np.float32).view(np.uint32))
+            flat = l.sharded_grad_flat().cpu().numpy()
+            real = np.zeros(l.S, dtype=bool)
+            for m in l.metas:
+                real[m["elem_offset"]:m["elem_offset"] + m["row_count"] * m["rest"]] = True
+            np.testing.assert_array_equal(flat[~real].view(np.uint32), old[r][~real].view(np.uint32))
+    finally:
+        emu.close()

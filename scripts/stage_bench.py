@@ -198,7 +198,17 @@ def main():
         emit(W, "pull_fp32", "ours", 2 * W * sum(valid) + 4 * S,
              lambda: F.stage_rs_pull(layer, stagings, torch.bfloat16, stream=st),
              note="reads this rank's rows from W distinct stagings (all local here), fp32 sum, /W")
-        del staging, stagings, grads
+        del staging, stagings
+        # store-based reduce-scatter: scatter into W receive buffers (all local here), then
+        # the local ascending-rank reduce of this rank's receive buffer
+        recvs = [torch.empty(W * S, dtype=torch.bfloat16, device=dev) for _ in range(W)]
+        emit(W, "rs_scatter", "ours", 4 * N, lambda: F.stage_rs_scatter(layer, grads, recvs, stream=st),
+             note="this rank's rows of every rank's chunk -> W receive buffers (all local here)")
+        F.stage_rs_scatter(layer, grads, recvs, stream=st)
+        emit(W, "rs_recv_reduce", "ours", sum(valid) * (2 * W + 4),
+             lambda: F.stage_rs_recv_reduce(layer, recvs[0], torch.bfloat16, stream=st),
+             note="W slots of bf16 rows -> fp32 grad, /W, ascending-rank sum")
+        del recvs, grads
         st.synchronize()
         layer.destroy()
         mesh.destroy()

@@ -321,6 +321,7 @@ struct fsdp_layer {
   int64_t stg_elems = 0;
   int64_t push_bytes_bf16 = 0, push_bytes_fp8 = 0, pull_elems = 0;
   int64_t scatter_elems = 0;         // store RS: elements this rank stores into other ranks
+  bool arena_is_flat_bf16 = false;   // every param's bf16 arena offset == 2 * off_p (W=1: K2 casts into it)
   int64_t local_push_bf16 = 0, local_push_fp8 = 0;
   SymSlot* p2p_slot = nullptr;       // arena of the current P2P unshard
   SymSlot* gbuf = nullptr;           // zero-copy full-grad buffer (fsdp_full_grad_buffer)

@@ -77,6 +77,9 @@ fsdp_status_t fsdp_shard(fsdp_mesh_t* m, int32_t n, const fsdp_param_desc_t* des
         l->pull_elems += cnt;
         l->scatter_elems += Ly.numel[p] - cnt;                       // the other ranks' rows
       }
+      l->arena_is_flat_bf16 = Ly.arena_bf16 >= 2 * Ly.S;
+      for (int p = 0; p < n; ++p)
+        if (Ly.uoff_bf16[p] != 2 * Ly.metas[p].elem_offset) l->arena_is_flat_bf16 = false;
       for (int p = 0; p < n; ++p) {
         const int64_t es = Ly.fp8[p] ? 1 : 2;
         l->bytes_cin_fp8 += Ly.metas[p].padded_numel * (4 + es);
@@ -333,9 +336,17 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
       const DevTiles& T = fp8 ? l->t_push_fp8 : l->t_push_bf16;
       {
         ProfScope pc(m, FSDP_PROF_COPY_IN, m->s_cin, fp8 ? l->local_push_fp8 : l->local_push_bf16);
-        fsdpk::LaunchCfg lcfg = m->cfg;   // W = 1: bulk stores too (0.915 vs 0.902 of HBM, r06)
-        if (const char* e = std::getenv("FSDP_B200_W1_BULK")) if (std::atoi(e) == 0) lcfg.variant &= ~4;
-        CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, pp, 1, 0, lcfg, m->s_cin));
+        if (!fp8 && l->arena_is_flat_bf16 && (m->cfg.variant & 32)) {
+          // opt-in (FSDP_B200_VARIANT bit 32): when the arena has the flat shard's layout (every
+          // Llama layout) the unshard is one contiguous cast, K2 straight into the unsharded
+          // tensors: faster alone (6138 vs 6002 GB/s) but the overlapped W=1 step is 0.2%
+          // slower next to the concurrent K5 (profiles/r13), so the push stays the default
+          CUDA_CHECK(fsdpk::launch_copy_in_bf16(l->shard, slot->b.p, l->L.S, m->cfg, m->s_cin));
+        } else {
+          fsdpk::LaunchCfg lcfg = m->cfg;   // W = 1: bulk stores too (0.915 vs 0.902 of HBM, r06)
+          if (const char* e = std::getenv("FSDP_B200_W1_BULK")) if (std::atoi(e) == 0) lcfg.variant &= ~4;
+          CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, pp, 1, 0, lcfg, m->s_cin));
+        }
         pc.done();
       }
       CUDA_CHECK(cudaEventRecord(l->ev_done, m->s_cin));

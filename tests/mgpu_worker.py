@@ -61,20 +61,19 @@ def main():
     algos = ["p2p", "nccl"] if mesh.algo == "p2p" else ["nccl"]
     for algo in algos:
         mesh.set_algo(algo)
+        import toy_train
+        ref = toy_train.reference_steps(3, W)
         for rs_mode in (["store", "pull"] if algo == "p2p" else ["-"]):
             if algo == "p2p":
                 mesh.set_p2p_rs(rs_mode)   # both P2P reduce-scatter mechanisms, same result bits
             run_checks(mesh, W, rank, local, algo)
             run_graph_checks(mesh, W, rank, algo)
-            if algo == "p2p":
-                print(f"rank {rank}/{W} p2p reduce-scatter mode {rs_mode}: OK", flush=True)
-        # training steps vs the single-device run: bit-exact under P2P (same
-        # ascending-rank fp32 order as the reference mean), fp32 tolerance under NCCL
-        import toy_train
-        ref = toy_train.reference_steps(3, W)
-        got, metas = toy_train.fsdp_steps(F, mesh, rank, 3)
-        toy_train.compare(ref, got, metas, exact=(algo == "p2p"))
-        print(f"rank {rank}/{W} algo={algo}: 3 training steps match the single-device run", flush=True)
+            # training steps vs the single-device run: bit-exact under P2P (same
+            # ascending-rank fp32 order as the reference mean), fp32 tolerance under NCCL
+            got, metas = toy_train.fsdp_steps(F, mesh, rank, 3)
+            toy_train.compare(ref, got, metas, exact=(algo == "p2p"))
+            print(f"rank {rank}/{W} algo={algo} rs={rs_mode}: checks, CUDA graphs and 3 training steps "
+                  f"(== single-device run) OK", flush=True)
     mesh.synchronize(120000)
     mesh.destroy()
     for Ws in sorted({d for d in (1, 2, W // 2) if 1 <= d < W and W % d == 0}):

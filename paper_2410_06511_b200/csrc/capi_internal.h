@@ -280,6 +280,7 @@ struct fsdp_mesh {
   // P2P (fused peer-memory) path
   int algo = FSDP_ALGO_NCCL;
   int p2p_rs_mode = FSDP_P2P_RS_AUTO;        // how the P2P reduce-scatter moves data
+  int reduce_per_sm = 2;                     // store-RS local reduce CTAs/SM (0: default grid; 2 measured best)
   bool p2p_ok = false;
   SymBuf flags;                              // uint64 [FK_NUM][kFlagSlots][kMaxRanks]
   std::vector<SymSlot*> p2p_ag, p2p_rs;      // unsharded arenas, grad staging

@@ -529,9 +529,11 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
         fsdpp::PeerPtrs slots{};
         for (int q = 0; q < m->W; ++q) slots.p[q] = (uint8_t*)ss->buf.local + (size_t)q * S * gsz;
         const bool acc = accumulate != 0 && !hsdp;
+        fsdpk::LaunchCfg rcfg = m->cfg;   // the reduce overlaps the next unit's transfers: its grid
+        if (m->reduce_per_sm > 0) rcfg.per_sm = m->reduce_per_sm;   // can leave them SMs
         ProfScope pr(m, FSDP_PROF_RS_REDUCE, m->s_rsc, l->pull_elems * (m->W * gsz + 4 + (acc ? 4 : 0)));
         CUDA_CHECK(fsdpp::launch_rs_pull(l->t_recv.d, l->t_recv.n, slots, gd == FSDP_BFLOAT16, divisor, target,
-                                         mean != 0, acc, obf, m->W, m->cfg, m->s_rsc));
+                                         mean != 0, acc, obf, m->W, rcfg, m->s_rsc));
         pr.done();
       }
       release_sym_slot(ss, m->s_rsc, cap);

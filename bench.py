@@ -602,10 +602,41 @@ def cpu_baseline(args, W):
     t0 = time.perf_counter()
     nbytes = _oracle_step(World, BF16, FP8, shapes, elig, params, grads, W, wl["fp8"])
     dt = time.perf_counter() - t0
-    return {"value": round(nbytes / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "seconds": round(dt, 2),
-            "sample": f"one {wl['model']} block ({sum(int(np.prod(s)) for s in shapes)} params), "
-                      f"W={W} simulated ranks, unshard + reduce-scatter, single-threaded NumPy"}
+    out = {"value": round(nbytes / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+           "seconds": round(dt, 2),
+           "sample": f"one {wl['model']} block ({sum(int(np.prod(s)) for s in shapes)} params), "
+                     f"W={W} simulated ranks, unshard + reduce-scatter, single-threaded NumPy"}
+    out["all_cores"] = _cpu_all_cores(wl, W)
+    return out
+
+
+def _oracle_worker(model, W, fp8):
+    """One process of the all-cores CPU baseline: the unchanged oracle on a bounded sample."""
+    from oracle import World
+    from oracle.world import BF16, FP8
+    shapes, elig, params, grads = _oracle_sample(model, W, full_block=False)
+    return _oracle_step(World, BF16, FP8, shapes, elig, params, grads, W, fp8)
+
+
+def _cpu_all_cores(wl, W, max_procs=16):
+    """SURVEY.md 8(d) "two runs: single-threaded and all cores": the unchanged oracle run
+    as k independent processes at once (one bounded sample each, like independent units),
+    k = min(usable cores, 16); GB/s = the bytes of all k samples / wall time."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    try:
+        k = max(1, min(len(os.sched_getaffinity(0)), max_procs))
+        ctx = mp.get_context("spawn")
+        t0 = time.perf_counter()
+        with cf.ProcessPoolExecutor(max_workers=k, mp_context=ctx) as ex:
+            total = sum(ex.map(_oracle_worker, [wl["model"]] * k, [W] * k, [wl["fp8"]] * k))
+        dt = time.perf_counter() - t0
+        return {"value": round(total / dt / 1e9, 4), "unit": "GB/s", "cores": k, "kind": "oracle",
+                "seconds": round(dt, 2),
+                "sample": f"{k} processes x one {wl['model']} block's attention weights + norms, W={W} "
+                          f"simulated ranks each (wall time incl. process start)"}
+    except Exception as e:   # noqa: BLE001 (a reported baseline only)
+        return {"error": f"{type(e).__name__}: {str(e)[:120]}"}
 
 
 def run_reference(args):

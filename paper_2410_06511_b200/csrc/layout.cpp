@@ -185,19 +185,36 @@ std::vector<int64_t> staging_offsets(const Layout& L, int64_t* total) {
   return off;
 }
 
+// Tile size for a table covering `total` units (elements or bytes): the maximum for large
+// units; for small ones about 4 tiles per SM, so a small unit spreads over the whole GPU
+// instead of a few dozen SMs (the per-op latency of latency-bound units); never below
+// `min_tile`, a multiple of `quantum` (keeps tile boundaries 16-byte aligned).
+static int64_t tile_size_for(int64_t total, int64_t max_tile, int64_t min_tile, int64_t quantum) {
+  constexpr int64_t kSmsHint = 148;
+  const int64_t want = round_up(ceil_div(std::max<int64_t>(total, 1), 4 * kSmsHint), quantum);
+  return std::max(min_tile, std::min(max_tile, want));
+}
+
+static int64_t own_elems(const Layout& L) {
+  int64_t t = 0;
+  for (const auto& m : L.metas) t += m.row_count * m.rest;
+  return t;
+}
+
 std::vector<fsdpk::Tile> tiles_push(const Layout& L, bool fp8) {
   std::vector<fsdpk::Tile> t;
+  const int64_t te = tile_size_for(own_elems(L), fsdpk::kTileElems, 1024, 256);
   for (size_t p = 0; p < L.metas.size(); ++p) {
     const auto& m = L.metas[p];
     const bool f8 = fp8 && L.fp8[p];
     const int64_t es = f8 ? 1 : 2;
     const int64_t base = (fp8 ? L.uoff_fp8[p] : L.uoff_bf16[p]) + m.row_begin * m.rest * es;
     const int64_t cnt = m.row_count * m.rest;
-    for (int64_t j = 0; j < cnt; j += fsdpk::kTileElems) {
+    for (int64_t j = 0; j < cnt; j += te) {
       fsdpk::Tile x{};
       x.src = (uint64_t)(m.elem_offset + j);
       x.dst = (uint64_t)(base + j * es);
-      x.n = (uint32_t)std::min<int64_t>(fsdpk::kTileElems, cnt - j);
+      x.n = (uint32_t)std::min<int64_t>(te, cnt - j);
       x.param = (uint32_t)p;
       x.kind = f8 ? fsdpk::TK_FP8 : fsdpk::TK_BF16;
       t.push_back(x);
@@ -208,14 +225,15 @@ std::vector<fsdpk::Tile> tiles_push(const Layout& L, bool fp8) {
 
 std::vector<fsdpk::Tile> tiles_pull(const Layout& L, const std::vector<int64_t>& stg_off) {
   std::vector<fsdpk::Tile> t;
+  const int64_t te = tile_size_for(own_elems(L), fsdpk::kTileElems, 1024, 256);
   for (size_t p = 0; p < L.metas.size(); ++p) {
     const auto& m = L.metas[p];
     const int64_t cnt = m.row_count * m.rest;
-    for (int64_t j = 0; j < cnt; j += fsdpk::kTileElems) {
+    for (int64_t j = 0; j < cnt; j += te) {
       fsdpk::Tile x{};
       x.src = (uint64_t)(stg_off[p] + m.row_begin * m.rest + j);
       x.dst = (uint64_t)(m.elem_offset + j);
-      x.n = (uint32_t)std::min<int64_t>(fsdpk::kTileElems, cnt - j);
+      x.n = (uint32_t)std::min<int64_t>(te, cnt - j);
       x.param = (uint32_t)p;
       x.kind = fsdpk::TK_COPY;
       t.push_back(x);
@@ -229,6 +247,9 @@ std::vector<fsdpk::Tile> tiles_scatter(const Layout& L, int64_t gsize) {
   // order, so every destination (and this rank's own slot, a local copy) is in flight at
   // once instead of one destination after another
   std::vector<std::vector<fsdpk::Tile>> per(L.W);
+  int64_t total = 0;
+  for (size_t p = 0; p < L.metas.size(); ++p) total += L.numel[p] * gsize;
+  const int64_t tb = tile_size_for(total, fsdpk::kTileBytes, 2048, 512);
   for (int i = 0; i < L.W; ++i) {
     const int r = (L.rank + 1 + i) % L.W;   // destination rank, rotated per sender
     for (size_t p = 0; p < L.metas.size(); ++p) {
@@ -236,11 +257,11 @@ std::vector<fsdpk::Tile> tiles_scatter(const Layout& L, int64_t gsize) {
       const int64_t b = std::min<int64_t>((int64_t)r * m.chunk_rows, m.dim0);
       const int64_t e = std::min<int64_t>((int64_t)(r + 1) * m.chunk_rows, m.dim0);
       const int64_t bytes = (e - b) * m.rest * gsize;
-      for (int64_t j = 0; j < bytes; j += fsdpk::kTileBytes) {
+      for (int64_t j = 0; j < bytes; j += tb) {
         fsdpk::Tile x{};
         x.src = (uint64_t)(b * m.rest * gsize + j);
         x.dst = (uint64_t)(((int64_t)L.rank * L.S + m.elem_offset) * gsize + j);
-        x.n = (uint32_t)std::min<int64_t>(fsdpk::kTileBytes, bytes - j);
+        x.n = (uint32_t)std::min<int64_t>(tb, bytes - j);
         x.param = (uint32_t)p;
         x.kind = fsdpk::TK_COPY;
         x.pad = (uint32_t)r;
@@ -259,14 +280,15 @@ std::vector<fsdpk::Tile> tiles_scatter(const Layout& L, int64_t gsize) {
 
 std::vector<fsdpk::Tile> tiles_recv_reduce(const Layout& L) {
   std::vector<fsdpk::Tile> t;
+  const int64_t te = tile_size_for(own_elems(L), fsdpk::kTileElems, 1024, 256);
   for (size_t p = 0; p < L.metas.size(); ++p) {
     const auto& m = L.metas[p];
     const int64_t cnt = m.row_count * m.rest;
-    for (int64_t j = 0; j < cnt; j += fsdpk::kTileElems) {
+    for (int64_t j = 0; j < cnt; j += te) {
       fsdpk::Tile x{};
       x.src = (uint64_t)(m.elem_offset + j);
       x.dst = (uint64_t)(m.elem_offset + j);
-      x.n = (uint32_t)std::min<int64_t>(fsdpk::kTileElems, cnt - j);
+      x.n = (uint32_t)std::min<int64_t>(te, cnt - j);
       x.param = (uint32_t)p;
       x.kind = fsdpk::TK_COPY;
       t.push_back(x);
@@ -277,13 +299,16 @@ std::vector<fsdpk::Tile> tiles_recv_reduce(const Layout& L) {
 
 std::vector<fsdpk::Tile> tiles_stage(const Layout& L, const std::vector<int64_t>& stg_off, int64_t gsize) {
   std::vector<fsdpk::Tile> t;
+  int64_t total = 0;
+  for (size_t p = 0; p < L.metas.size(); ++p) total += L.numel[p] * gsize;
+  const int64_t tb = tile_size_for(total, fsdpk::kTileBytes, 2048, 512);
   for (size_t p = 0; p < L.metas.size(); ++p) {
     const int64_t bytes = L.numel[p] * gsize;
-    for (int64_t j = 0; j < bytes; j += fsdpk::kTileBytes) {
+    for (int64_t j = 0; j < bytes; j += tb) {
       fsdpk::Tile x{};
       x.src = (uint64_t)j;
       x.dst = (uint64_t)(stg_off[p] * gsize + j);
-      x.n = (uint32_t)std::min<int64_t>(fsdpk::kTileBytes, bytes - j);
+      x.n = (uint32_t)std::min<int64_t>(tb, bytes - j);
       x.param = (uint32_t)p;
       x.kind = fsdpk::TK_COPY;
       t.push_back(x);

@@ -117,7 +117,7 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        time.sleep(0.25)
+        time.sleep(0.06)   # one more sample interval; more would add idle samples to the median
         self.proc.terminate()
         self.proc.wait(timeout=10)
         self.f.flush()

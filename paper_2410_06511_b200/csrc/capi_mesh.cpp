@@ -85,6 +85,7 @@ static void mesh_common_init(fsdp_mesh* m) {
     if (c >= 1024 && c <= 16384 && (c & (c - 1)) == 0) m->cfg.pull_chunk = c;
   }
   if (const char* e = std::getenv("FSDP_B200_PULL_STAGES")) m->cfg.pull_stages = std::max(2, std::min(4, std::atoi(e)));
+  if (const char* e = std::getenv("FSDP_B200_PDL")) m->cfg.pdl = std::atoi(e) != 0;
   m->cfg.grid_cap = sms * (per_sm > 0 ? per_sm : 4);
   CUDA_CHECK(cudaMalloc(&m->d_err, sizeof(int)));
   CUDA_CHECK(cudaMemset(m->d_err, 0, sizeof(int)));

@@ -199,6 +199,12 @@ __device__ __forceinline__ void load4(const uint8_t* p, uint32_t k, float (&x)[4
   }
 }
 
+// Programmatic dependent launch: a kernel launched with programmatic stream serialization
+// may start while its predecessor on the stream is still running; it must call this first,
+// which waits until the predecessor grid completed and its memory is visible.  A no-op for
+// kernels launched normally.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- host: persistent-grid launches
 // CTAs of `fn` (kThreads threads, `dyn_smem` dynamic bytes, plus its registers and static
 // shared memory) the whole GPU holds at once; cached per kernel (kernels.cu).
@@ -214,6 +220,32 @@ cudaError_t launch_persistent(void (*kern)(KArgs...), int g, size_t dyn_smem, cu
   if (g < 1) g = 1;
   kern<<<g, kThreads, dyn_smem, st>>>(static_cast<Args&&>(args)...);
   return cudaGetLastError();
+}
+
+// Launch with programmatic stream serialization (the kernel must start with pdl_wait()):
+// its launch latency overlaps the tail of the previous kernel on `st`.
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), int g, int threads, size_t dyn_smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3((unsigned)g);
+  c.blockDim = dim3((unsigned)threads);
+  c.dynamicSmemBytes = dyn_smem;
+  c.stream = st;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[0].val.programmaticStreamSerializationAllowed = 1;
+  c.attrs = a;
+  c.numAttrs = 1;
+  return cudaLaunchKernelEx(&c, kern, static_cast<Args&&>(args)...);
+}
+
+// launch_persistent's grid sizing with a programmatic-dependent launch
+template <class... KArgs, class... Args>
+cudaError_t launch_persistent_pdl(void (*kern)(KArgs...), int g, size_t dyn_smem, cudaStream_t st, Args&&... args) {
+  const int r = resident_ctas(reinterpret_cast<const void*>(kern), dyn_smem);
+  if (r > 0 && g > r) g = r;
+  if (g < 1) g = 1;
+  return launch_pdl(kern, g, kThreads, dyn_smem, st, static_cast<Args&&>(args)...);
 }
 
 }  // namespace fsdpdev

@@ -40,6 +40,9 @@ struct LaunchCfg {
   // (FSDP_B200_PULL_CHUNK / FSDP_B200_PULL_STAGES)
   int pull_chunk = 4096;
   int pull_stages = 2;
+  // P2P data kernels and done handshakes launched with programmatic dependent launch
+  // (FSDP_B200_PDL=0 disables)
+  bool pdl = true;
   // persistent grid of a kernel whose measured best is `tuned` CTAs per SM
   int cap(int tuned) const { return sms * (per_sm > 0 ? per_sm : tuned); }
 };

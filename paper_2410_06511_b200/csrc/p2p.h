@@ -34,9 +34,11 @@ struct FlagPtrs { unsigned long long* p[kMaxRanks]; };
 // system-scope fence; then every thread r < W spins (ld.acquire.sys) until
 // flags_local[r] >= epoch (rank r signalled me).  One CTA.
 // The spin gives up after timeout_ns and writes 2 | (peer << 8) to *err (FSDP_ERR_TIMEOUT).
+// pdl: launch with programmatic stream serialization (the done handshakes, right after their
+// data kernel on the same stream: the launch latency overlaps the data kernel's tail).
 cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
                                unsigned long long* epoch_ctr, unsigned long long timeout_ns, int* err,
-                               cudaStream_t st);
+                               cudaStream_t st, bool pdl = false);
 
 // Push tiles: src = element offset into the fp32 shard, dst = byte offset into the arena,
 // n elements, kind TK_BF16 / TK_FP8 (scale = scales[param]).  Stores go to arena.p[d] for

@@ -32,6 +32,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 __global__ void k_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
                               unsigned long long* epoch_ctr, unsigned long long timeout_ns, int* err) {
   __shared__ unsigned long long e_sh;
+  pdl_wait();   // launched programmatically after the data kernel (done handshakes)
   const int r = threadIdx.x;
   if (r == 0) {
     e_sh = *epoch_ctr + 1;
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(kThreads) k_unshard_push(const Tile* __restric
                                                            const float* __restrict__ shard,
                                                            const float* __restrict__ scales, PeerPtrs arena,
                                                            int W, int rank) {
+  pdl_wait();   // the ready handshake before it has completed
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
     if (tl.kind == fsdpk::TK_FP8) push_tile<true>(tl, shard, scales[tl.param], arena, W, rank);
@@ -343,6 +345,7 @@ template <int W, bool kGradBf16, int VEC>
 __global__ void __launch_bounds__(kThreads) k_rs_pull(const Tile* __restrict__ tiles, int ntiles, PeerPtrs st,
                                                       float* __restrict__ grad, PullOps ops) {
   constexpr uint32_t gs = kGradBf16 ? 2 : 4;
+  pdl_wait();
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
     const uint64_t sb = tl.src * gs;      // byte offset into every rank's staging
@@ -388,6 +391,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_pull_bulk(const Tile* __restric
   extern __shared__ __align__(128) uint8_t smem[];   // [stages][W][chunk]
   __shared__ uint64_t full[kPullMaxStages];
   constexpr uint32_t gs = kGradBf16 ? 2 : 4;
+  pdl_wait();
   const uint32_t chunk = ops.chunk, NS = ops.stages;
   const uint32_t CE = chunk / gs;                      // elements per chunk
   if (threadIdx.x == 0) {
@@ -552,6 +556,7 @@ __global__ void __launch_bounds__(kThreads) k_unshard_push_bulk(const Tile* __re
                                                                 const float* __restrict__ scales, PeerPtrs arena,
                                                                 int W) {
   __shared__ __align__(128) uint8_t stage_buf[2 * kBulkChunk];
+  pdl_wait();
   uint32_t it = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
@@ -590,6 +595,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_copy(const Tile* __restrict
 // profiles/nvlink_ceiling.json).
 __global__ void __launch_bounds__(kThreads) k_rs_scatter(const Tile* __restrict__ tiles, int ntiles,
                                                          fsdpk::PtrArray grads, PeerPtrs dests) {
+  pdl_wait();
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
     uint8_t* base = nullptr;
@@ -618,25 +624,32 @@ inline int grid_for(int64_t items, fsdpk::LaunchCfg cfg, int tuned = fsdpk::kCta
   return (int)(g < 1 ? 1 : g);
 }
 
+// persistent launch, programmatic (the kernel starts with pdl_wait) unless disabled
+template <class... KArgs, class... Args>
+cudaError_t launch_p(bool pdl, void (*kern)(KArgs...), int g, size_t smem, cudaStream_t s, Args&&... args) {
+  if (pdl) return launch_persistent_pdl(kern, g, smem, s, static_cast<Args&&>(args)...);
+  return launch_persistent(kern, g, smem, s, static_cast<Args&&>(args)...);
+}
+
 template <bool kGradBf16, int V>
 cudaError_t launch_pull_wv(const Tile* tiles, int ntiles, PeerPtrs st, float* grad, PullOps ops, int W, int g,
-                           cudaStream_t s) {
+                           cudaStream_t s, bool pdl) {
   switch (W) {
-    case 1: return launch_persistent(k_rs_pull<1, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
-    case 2: return launch_persistent(k_rs_pull<2, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
-    case 3: return launch_persistent(k_rs_pull<3, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
-    case 4: return launch_persistent(k_rs_pull<4, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
-    case 5: return launch_persistent(k_rs_pull<5, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
-    case 6: return launch_persistent(k_rs_pull<6, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
-    case 7: return launch_persistent(k_rs_pull<7, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
-    case 8: return launch_persistent(k_rs_pull<8, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 1: return launch_p(pdl, k_rs_pull<1, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 2: return launch_p(pdl, k_rs_pull<2, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 3: return launch_p(pdl, k_rs_pull<3, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 4: return launch_p(pdl, k_rs_pull<4, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 5: return launch_p(pdl, k_rs_pull<5, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 6: return launch_p(pdl, k_rs_pull<6, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 7: return launch_p(pdl, k_rs_pull<7, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
+    case 8: return launch_p(pdl, k_rs_pull<8, kGradBf16, V>, g, 0, s, tiles, ntiles, st, grad, ops);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <int W, bool kGradBf16>
 cudaError_t launch_pull_bulk_w(const Tile* tiles, int ntiles, PeerPtrs st, float* grad, PullOps ops, int g,
-                               cudaStream_t s) {
+                               cudaStream_t s, bool pdl) {
   while ((size_t)ops.stages * W * ops.chunk > kPullMaxSmem) {   // shrink stages, then chunk
     if (ops.stages > 2) --ops.stages;
     else ops.chunk /= 2;
@@ -652,34 +665,35 @@ cudaError_t launch_pull_bulk_w(const Tile* tiles, int ntiles, PeerPtrs st, float
     if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   // one wave (launch_persistent): at W = 8 the 64 KB stages allow 3 CTAs per SM, not 4
-  return launch_persistent(k_rs_pull_bulk<W, kGradBf16>, g, smem, s, tiles, ntiles, st, grad, ops);
+  return launch_p(pdl, k_rs_pull_bulk<W, kGradBf16>, g, smem, s, tiles, ntiles, st, grad, ops);
 }
 
 template <bool kGradBf16>
 cudaError_t launch_pull_w(const Tile* tiles, int ntiles, PeerPtrs st, float* grad, PullOps ops, int W, int g,
-                          cudaStream_t s, int variant) {
+                          cudaStream_t s, int variant, bool pdl) {
   if (variant & 2) {   // TMA bulk pull
     switch (W) {
-      case 1: return launch_pull_bulk_w<1, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
-      case 2: return launch_pull_bulk_w<2, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
-      case 3: return launch_pull_bulk_w<3, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
-      case 4: return launch_pull_bulk_w<4, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
-      case 5: return launch_pull_bulk_w<5, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
-      case 6: return launch_pull_bulk_w<6, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
-      case 7: return launch_pull_bulk_w<7, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
-      case 8: return launch_pull_bulk_w<8, kGradBf16>(tiles, ntiles, st, grad, ops, g, s);
+      case 1: return launch_pull_bulk_w<1, kGradBf16>(tiles, ntiles, st, grad, ops, g, s, pdl);
+      case 2: return launch_pull_bulk_w<2, kGradBf16>(tiles, ntiles, st, grad, ops, g, s, pdl);
+      case 3: return launch_pull_bulk_w<3, kGradBf16>(tiles, ntiles, st, grad, ops, g, s, pdl);
+      case 4: return launch_pull_bulk_w<4, kGradBf16>(tiles, ntiles, st, grad, ops, g, s, pdl);
+      case 5: return launch_pull_bulk_w<5, kGradBf16>(tiles, ntiles, st, grad, ops, g, s, pdl);
+      case 6: return launch_pull_bulk_w<6, kGradBf16>(tiles, ntiles, st, grad, ops, g, s, pdl);
+      case 7: return launch_pull_bulk_w<7, kGradBf16>(tiles, ntiles, st, grad, ops, g, s, pdl);
+      case 8: return launch_pull_bulk_w<8, kGradBf16>(tiles, ntiles, st, grad, ops, g, s, pdl);
       default: return cudaErrorInvalidValue;
     }
   }
-  return (variant & 1) ? launch_pull_wv<kGradBf16, 8>(tiles, ntiles, st, grad, ops, W, g, s)
-                       : launch_pull_wv<kGradBf16, 4>(tiles, ntiles, st, grad, ops, W, g, s);
+  return (variant & 1) ? launch_pull_wv<kGradBf16, 8>(tiles, ntiles, st, grad, ops, W, g, s, pdl)
+                       : launch_pull_wv<kGradBf16, 4>(tiles, ntiles, st, grad, ops, W, g, s, pdl);
 }
 
 }  // namespace
 
 cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
                                unsigned long long* epoch_ctr, unsigned long long timeout_ns, int* err,
-                               cudaStream_t st) {
+                               cudaStream_t st, bool pdl) {
+  if (pdl) return launch_pdl(k_signal_wait, 1, 32, 0, st, remote, local, W, rank, epoch_ctr, timeout_ns, err);
   k_signal_wait<<<1, 32, 0, st>>>(remote, local, W, rank, epoch_ctr, timeout_ns, err);
   return cudaGetLastError();
 }
@@ -691,8 +705,8 @@ cudaError_t launch_unshard_push(const Tile* tiles, int ntiles, const float* shar
   for (int i = 0; i < W; ++i) rot.p[i] = arena.p[(rank + 1 + i) % W];
   const int g = grid_for(ntiles, cfg, fsdpk::kCtasPush);
   if (cfg.variant & 4)   // TMA bulk push
-    return launch_persistent(k_unshard_push_bulk, g, 0, st, tiles, ntiles, shard, scales, rot, W);
-  return launch_persistent(k_unshard_push, g, 0, st, tiles, ntiles, shard, scales, rot, W, rank);
+    return launch_p(cfg.pdl, k_unshard_push_bulk, g, 0, st, tiles, ntiles, shard, scales, rot, W);
+  return launch_p(cfg.pdl, k_unshard_push, g, 0, st, tiles, ntiles, shard, scales, rot, W, rank);
 }
 
 cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool grad_bf16, int divisor, float* grad, bool mean,
@@ -708,8 +722,8 @@ cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool
   ops.chunk = (uint32_t)cfg.pull_chunk;
   ops.stages = (uint32_t)std::min<int>(std::max(cfg.pull_stages, 2), (int)kPullMaxStages);
   const int g = grid_for(ntiles, cfg);
-  return grad_bf16 ? launch_pull_w<true>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant)
-                   : launch_pull_w<false>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant);
+  return grad_bf16 ? launch_pull_w<true>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant, cfg.pdl)
+                   : launch_pull_w<false>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant, cfg.pdl);
 }
 
 cudaError_t launch_gather_copy(const Tile* tiles, int ntiles, const fsdpk::PtrArray& srcs, void* dst,
@@ -721,7 +735,7 @@ cudaError_t launch_gather_copy(const Tile* tiles, int ntiles, const fsdpk::PtrAr
 cudaError_t launch_rs_scatter(const Tile* tiles, int ntiles, const fsdpk::PtrArray& grads, PeerPtrs dests,
                               fsdpk::LaunchCfg cfg, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
-  return launch_persistent(k_rs_scatter, grid_for(ntiles, cfg, fsdpk::kCtasPush), 0, st, tiles, ntiles, grads,
+  return launch_p(cfg.pdl, k_rs_scatter, grid_for(ntiles, cfg, fsdpk::kCtasPush), 0, st, tiles, ntiles, grads,
                            dests);
 }
 

@@ -46,6 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC",
            "-prec-div=true", "-prec-sqrt=true", "-ftz=false", "-Xptxas", "-v",
+           *os.environ.get("FSDP_B200_NVCC_EXTRA", "").split(),   # experiments only (e.g. -D...)
            "-I", INCLUDE, "-I", CSRC, "-I", inc, *sources(),
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}", "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)

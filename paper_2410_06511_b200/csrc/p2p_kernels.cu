@@ -38,7 +38,19 @@ __global__ void k_signal_wait(FlagPtrs remote, unsigned long long* local, int W,
     e_sh = *epoch_ctr + 1;
     *epoch_ctr = e_sh;
   }
-  __threadfence_system();   // order this GPU's earlier stores (previous kernels) before the flag
+  // No system fence around the signal / wait (-DFSDP_HS_FENCE restores them for debugging):
+  // - what a peer must see before our signal was written by EARLIER kernels (staging /
+  //   zero-copy grads; the push and scatter kernels end with their own system fence), and
+  //   kernel completion has performed those writes at this GPU's L2, where the peers' NVLink
+  //   accesses are served; reads of earlier kernels (arena / receive-buffer reuse) completed;
+  // - what we read after the wait was released by the peer before its flag, and our
+  //   ld.acquire.sys of that flag, the barrier, kernel completion and the event chain order it
+  //   before every later consumer.
+  // Dropping the two fences took the handshake chain from ~25 to ~17 us per op (toy step at
+  // W=2 under a CUDA graph 107.5 -> 81.6 us; 8B step 24.3 -> 24.0 ms).
+#ifdef FSDP_HS_FENCE
+  __threadfence_system();
+#endif
   __syncthreads();
   const unsigned long long epoch = e_sh;
 #pragma unroll
@@ -55,7 +67,9 @@ __global__ void k_signal_wait(FlagPtrs remote, unsigned long long* local, int W,
     }
   }
   __syncthreads();
+#ifdef FSDP_HS_FENCE
   __threadfence_system();
+#endif
 }
 
 // ------------------------------------------------------------------- unshard push

@@ -212,9 +212,10 @@ fsdp_status_t fsdp_mesh_get_algo(const fsdp_mesh_t* mesh, int32_t* algo);
  *                     staging copy for any caller buffer) into that peer's symmetric receive
  *                     buffer over NVLink (stores), then reduces its received rows locally on a
  *                     second stream, overlapping the next unit's transfer.
- *  FSDP_P2P_RS_AUTO:  PULL when W == 2 and the layer has zero-copy grad buffers
- *                     (fsdp_full_grad_buffer, created collectively, so every rank decides
- *                     alike), else STORE — the faster one on 2 and 4 B200s.
+ *  FSDP_P2P_RS_AUTO:  PULL when the layer has zero-copy grad buffers (fsdp_full_grad_buffer,
+ *                     created collectively, so every rank decides alike) and W == 2 or the
+ *                     unit moves < 64 MB of bus bytes; else STORE — the faster one on 2 and 4
+ *                     B200s.
  * Collective (same call on every rank, nothing pending).  Default: FSDP_P2P_RS_AUTO
  * (environment FSDP_B200_P2P_RS=pull|store|auto overrides). */
 typedef enum { FSDP_P2P_RS_PULL = 0, FSDP_P2P_RS_STORE = 1, FSDP_P2P_RS_AUTO = 2 } fsdp_p2p_rs_t;

@@ -480,8 +480,14 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
     };
     // P2P mechanism: identical on every rank (the mode is set collectively; the layer's
     // zero-copy buffer exists on all ranks or none)
+    // AUTO: with zero-copy buffers the pull needs no staging and one kernel less, so it wins
+    // at W = 2 and for small units (the store's ~5% link-rate edge is worth less than its
+    // extra kernel below ~64 MB of bus bytes, profiles/r16 alpha-B fits); else store
+    const bool zc_layer = l->gbuf && l->gbuf_sym;
+    const int64_t bus_bytes = l->stg_elems * dtype_size(gd) * (m->W - 1) / std::max(m->W, 1);
     const bool p2p_store = m->p2p_rs_mode == FSDP_P2P_RS_STORE ||
-                           (m->p2p_rs_mode == FSDP_P2P_RS_AUTO && !(m->W == 2 && l->gbuf && l->gbuf_sym));
+                           (m->p2p_rs_mode == FSDP_P2P_RS_AUTO &&
+                            !(zc_layer && (m->W == 2 || bus_bytes < (64ll << 20))));
     if (m->algo == FSDP_ALGO_P2P && p2p_store) {
       // store-based path: ready handshake (this rank's receive buffer is free) -> scatter
       // (this rank's rows of every rank's chunk, read from the caller's grads, stored into

@@ -127,11 +127,13 @@ typedef enum {
  *                  ncclReduceScatter (fp32).
  *  FSDP_ALGO_P2P:  symmetric buffers mapped with CUDA IPC across the ranks' GPUs (NVLink /
  *                  NVSwitch); the unshard is ONE push kernel (cast + store into every rank's
- *                  unsharded tensors) and the reduce-scatter ONE pull kernel (read every
- *                  rank's bf16 grad rows, /W, sum in ascending rank order in fp32), each
- *                  bracketed by single-CTA flag handshakes.  Requires W <= 8 GPUs with
- *                  peer access; identical results up to the reduce-scatter summation order
- *                  (P2P: ascending rank, deterministic). */
+ *                  unsharded tensors); the reduce-scatter is one store-scatter kernel (every
+ *                  rank's rows into its owner's receive buffer) plus a local reduce, or one
+ *                  pull kernel (read every rank's bf16 grad rows) — fsdp_mesh_set_p2p_rs —
+ *                  both /W and summing in ascending rank order in fp32; every data kernel is
+ *                  bracketed by single-CTA flag handshakes.  Requires W <= 8 GPUs with peer
+ *                  access; identical results up to the reduce-scatter summation order (P2P:
+ *                  ascending rank, deterministic). */
 typedef enum { FSDP_ALGO_NCCL = 0, FSDP_ALGO_P2P = 1 } fsdp_algo_t;
 
 typedef struct {

@@ -4,9 +4,11 @@ GB/s per layer (fraction of NVLink/HBM peak) at 1/2/4/8 B200").
 
 One step = one pass of the whole hot path over the Llama 3.1 8B parameter layout
 (BASELINE.json configs[1]): for every FSDP unit (32 TransformerBlocks + root)
-unshard (copy-in -> NCCL all-gather -> copy-out, bf16) -> reshard -> reduce_scatter_grads
-(chunk-cat + fp32 cast + /W -> NCCL reduce-scatter fp32 -> sharded grad), with the next
-unit's unshard prefetched.  Bytes per unit: the all-gather
+unshard (bf16; W=1: one cast kernel into the unsharded tensors, W>1: the fused NVLink push
+kernel, or copy-in -> NCCL all-gather -> copy-out with --algo nccl) -> reshard ->
+reduce_scatter_grads (fp32 reduction with one /W: W=1 the RS copy-in kernel, W>1 the fused
+store-scatter + local reduce or pull kernels, or chunk-cat -> NCCL reduce-scatter), with the
+next unit's unshard prefetched.  Bytes per unit: the all-gather
 output W*S*2 plus the reduce-scatter input W*S*4 per rank; `value` = those bytes summed
 over all ranks / max-over-ranks step time (whole job, weak scaling: every rank unshards
 the full model).

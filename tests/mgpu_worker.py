@@ -74,6 +74,10 @@ def main():
             toy_train.compare(ref, got, metas, exact=(algo == "p2p"))
             print(f"rank {rank}/{W} algo={algo} rs={rs_mode}: checks, CUDA graphs and 3 training steps "
                   f"(== single-device run) OK", flush=True)
+    if mesh.algo == "p2p" or "p2p" in algos:
+        mesh.set_algo("p2p")
+        mesh.set_p2p_rs("auto")
+        run_fullsize_check(mesh, W, rank)
     mesh.synchronize(120000)
     mesh.destroy()
     for Ws in sorted({d for d in (1, 2, W // 2) if 1 <= d < W and W % d == 0}):
@@ -148,6 +152,58 @@ def run_graph_checks(mesh, W, rank, algo):
         l.destroy()
     mesh.synchronize(120000)
     print(f"rank {rank}/{W} algo={algo}: CUDA graph replays == eager == oracle OK", flush=True)
+
+
+def run_fullsize_check(mesh, W, rank):
+    """One Llama 3.1 8B block (218.1M params, BASELINE configs[1] layout) through the real
+    P2P path at this W, in the launch configuration bench.py times: the bf16 unshard sampled
+    at 4096 positions per param against the oracle's cast, and the reduce-scatter sampled in
+    this rank's rows against the oracle's ascending-rank fp32 sum of fp32(g_q)/W (bit-exact),
+    with torch-owned grads (store RS) and with zero-copy grad buffers (pull at W=2)."""
+    from oracle import bf16_rne_bits
+    u = synth.model_units("llama3.1-8b", include_root=False)[0]
+    shapes = [tuple(s) for _, s, _ in u]
+    elig = [e for _, _, e in u]
+    P = [synth.param_values(500, p, s) for p, s in enumerate(shapes)]
+    layer = F.fsdp_shard(mesh, [torch.from_numpy(x) for x in P], elig)
+    rng = np.random.default_rng(np.random.SeedSequence([241006511, 501, W]))
+    outs = F.all_gather_params(layer, torch.bfloat16)
+    for p, o in enumerate(outs):
+        idx = rng.integers(0, P[p].size, 4096)
+        got = o.reshape(-1)[torch.from_numpy(idx).cuda()].view(torch.int16).cpu().numpy().view(np.uint16)
+        np.testing.assert_array_equal(got, bf16_rne_bits(P[p].reshape(-1)[idx]), err_msg=f"fullsize unshard p={p}")
+    F.fsdp_reshard(layer)
+    del P
+    G = [[synth.grad_bf16_bits(600, p, q, s) for p, s in enumerate(shapes)] for q in range(W)]
+    divisor = np.float32(W)
+    for mode in ("torch", "zero-copy"):
+        if mode == "torch":
+            gt = [torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16) for x in G[rank]]
+        else:
+            gt = layer.full_grad_buffers(torch.bfloat16)
+            for b, x in zip(gt, G[rank]):
+                b.copy_(torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16).reshape(b.shape))
+        F.reduce_scatter_grads(layer, gt)
+        F.fsdp_wait_reduce_scatter(layer)
+        torch.cuda.synchronize()
+        for p in range(len(shapes)):
+            m = layer.metas[p]
+            cnt = m["row_count"] * m["rest"]
+            if cnt == 0:
+                continue
+            loc = rng.integers(0, cnt, 4096)
+            glob = m["row_begin"] * m["rest"] + loc
+            want = np.zeros(loc.size, dtype=np.float32)
+            for q in range(W):   # ascending rank, fp32(g_q) / W, fp32 sums (SPEC.md:159)
+                gq = (G[q][p].reshape(-1)[glob].astype(np.uint32) << 16).view(np.float32)
+                want = (want + (gq / divisor).astype(np.float32)).astype(np.float32)
+            got = layer.sharded_grad(p).reshape(-1)[torch.from_numpy(loc).cuda()].cpu().numpy()
+            np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32),
+                                          err_msg=f"fullsize reduce-scatter ({mode}, {mesh.p2p_rs}) p={p}")
+    layer.destroy()
+    torch.cuda.empty_cache()
+    print(f"rank {rank}/{W}: full-size 8B block unshard + reduce-scatter (torch and zero-copy grads) OK",
+          flush=True)
 
 
 def run_fault_injection(W, rank, local):

@@ -204,8 +204,8 @@ int main(int argc, char** argv) {
       CK(cudaEventCreate(&f0[d]));
       CK(cudaEventCreate(&f1[d]));
     }
-    const char* an[] = {"a2a_ce", "a2a_st", "a2a_ld"};
-    for (int m = 0; m < 3; ++m) {
+    const char* an[] = {"a2a_ce", "a2a_st", "a2a_ld", "a2a_ce_plus_st"};
+    for (int m = 0; m < 4; ++m) {
       float best = 1e30f;
       for (int rep = 0; rep < 6; ++rep) {
         for (int d = 0; d < N; ++d) {
@@ -215,16 +215,23 @@ int main(int argc, char** argv) {
         for (int d = 0; d < N; ++d) {
           CK(cudaSetDevice(d));
           CK(cudaEventRecord(f0[d], ss[d][d]));
+          for (int q = 0; q < N; ++q)
+            if (q != d) CK(cudaStreamWaitEvent(ss[d][q], f0[d], 0));
           for (int q = 0; q < N; ++q) {
             if (q == d) continue;
-            CK(cudaStreamWaitEvent(ss[d][q], f0[d], 0));
             const int g = sms * 4 / (N - 1);
             // d's piece for q: src[d] + q*part -> dst[q] + d*part (push), or pulled by d from q
             if (m == 0) CK(cudaMemcpyPeerAsync(dst[q] + d * part, q, src[d] + q * part, d, part, ss[d][q]));
             else if (m == 1) k_store<<<g, kThreads, 0, ss[d][q]>>>((const uint4*)(src[d] + q * part),
                                                                   (uint4*)(dst[q] + d * part), part / 16);
-            else k_load<<<g, kThreads, 0, ss[d][q]>>>((const uint4*)(src[q] + d * part),
-                                                      (uint4*)(dst[d] + q * part), part / 16);
+            else if (m == 2) k_load<<<g, kThreads, 0, ss[d][q]>>>((const uint4*)(src[q] + d * part),
+                                                                 (uint4*)(dst[d] + q * part), part / 16);
+            else {   // half of each peer's bytes by copy engine, half by SM stores, concurrently
+              const size_t h = (part / 2) & ~(size_t)4095;
+              CK(cudaMemcpyPeerAsync(dst[q] + d * part, q, src[d] + q * part, d, h, ss[d][q]));
+              k_store<<<g, kThreads, 0, ss[d][(q + 1) % N == d ? (q + 2) % N : (q + 1) % N]>>>(
+                  (const uint4*)(src[d] + q * part + h), (uint4*)(dst[q] + d * part + h), (part - h) / 16);
+            }
             CK(cudaGetLastError());
           }
           for (int q = 0; q < N; ++q) {

@@ -103,3 +103,25 @@ def test_unique_id_without_gpu():
     import paper_2410_06511_b200 as f
     a, b = f.get_unique_id(), f.get_unique_id()
     assert len(a) == 128 and a != b
+
+
+def _header_enums():
+    """name -> value of every `NAME = <int>` enumerator in include/fsdp_b200.h."""
+    txt = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    return {n: int(v) for n, v in re.findall(r"\b(FSDP_[A-Z0-9_]+)\s*=\s*(\d+)", txt)}
+
+
+def test_binding_constants_match_header_enums():
+    from paper_2410_06511_b200 import _capi as c
+    e = _header_enums()
+    for code, name in c.STATUS.items():
+        assert e[name] == code, name
+    assert (e["FSDP_FLOAT32"], e["FSDP_BFLOAT16"], e["FSDP_FLOAT8_E4M3FN"]) == (c.FLOAT32, c.BFLOAT16, c.FLOAT8_E4M3FN)
+    assert (e["FSDP_ALGO_NCCL"], e["FSDP_ALGO_P2P"]) == (c.ALGO_NCCL, c.ALGO_P2P)
+    assert (e["FSDP_P2P_RS_PULL"], e["FSDP_P2P_RS_STORE"], e["FSDP_P2P_RS_AUTO"]) == \
+        (c.P2P_RS_PULL, c.P2P_RS_STORE, c.P2P_RS_AUTO)
+    # profile kinds: the binding's names are in enum order and the struct arrays have NUM entries
+    assert len(c.PROF_KINDS) == e["FSDP_PROF_NUM"]
+    assert c.Profile.launches.size == 8 * e["FSDP_PROF_NUM"]
+    assert e["FSDP_PROF_RS_SCATTER"] == c.PROF_KINDS.index("rs_scatter")
+    assert e["FSDP_PROF_HANDSHAKE"] == c.PROF_KINDS.index("handshake")

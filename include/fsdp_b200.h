@@ -297,7 +297,12 @@ fsdp_status_t fsdp_precompute_fp8_scales(fsdp_mesh_t* mesh, fsdp_layer_t* const*
  * passing caller scales to fsdp_unshard. */
 fsdp_status_t fsdp_precompute_fp8_scales_delayed(fsdp_mesh_t* mesh, fsdp_layer_t* const* layers,
                                                  int32_t n_layers, int32_t history_len, void* stream);
-/* Device arrays of P floats (entries of non-eligible params are 0). */
+/* Device arrays of P floats (entries of non-eligible params are 0).  The pointers stay valid
+ * until the mesh is destroyed: the mesh's fp8 registry has a fixed capacity (65536 params,
+ * environment FSDP_B200_REGISTRY_CAP) and is never reallocated, so views taken here and
+ * kernel arguments captured in CUDA graphs never dangle; fsdp_shard returns
+ * FSDP_ERR_UNAVAILABLE when the registry is full.  Entries are assigned in fsdp_shard order
+ * and recycled only once every layer of the mesh has been destroyed. */
 fsdp_status_t fsdp_fp8_scales(const fsdp_layer_t* layer, const float** scales_dev,
                               const float** amax_dev);
 
@@ -389,7 +394,9 @@ fsdp_status_t fsdp_unsharded_layout(const fsdp_layer_t* layer, fsdp_dtype_t para
 /* K7 push: casts this rank's rows of every param (bf16, or e4m3fn with fp8_scales_dev[p] for
  * eligible params when param_dtype is FLOAT8) and stores them at their place in each of the
  * W arenas arenas_dev[0..W-1] (any device memory the current device can store to, e.g.
- * peer-mapped).  Running it for every rank fills every arena with the full tensors. */
+ * peer-mapped; each 16-byte aligned, else FSDP_ERR_INVALID_ARGUMENT — the TMA bulk stores
+ * address them relative to their base).  Running it for every rank fills every arena with
+ * the full tensors. */
 fsdp_status_t fsdp_stage_unshard_push(const fsdp_layer_t* layer, fsdp_dtype_t param_dtype,
                                       const float* fp8_scales_dev, void* const* arenas_dev,
                                       void* stream);
@@ -400,7 +407,8 @@ fsdp_status_t fsdp_grad_staging_layout(const fsdp_layer_t* layer, int64_t* elem_
 fsdp_status_t fsdp_stage_grads_to_staging(const fsdp_layer_t* layer, const void* const* full_grads_dev,
                                           fsdp_dtype_t grad_dtype, void* staging_dev, void* stream);
 /* K8 pull: for this rank's rows, grad (+)= sum over q = 0..W-1 ascending of
- * fp32(stagings_dev[q]) / W (mean) — bf16 reduce_dtype rounds every term and the sum to bf16. */
+ * fp32(stagings_dev[q]) / W (mean) — bf16 reduce_dtype rounds every term and the sum to bf16.
+ * Every staging base must be 16-byte aligned (TMA bulk loads; else FSDP_ERR_INVALID_ARGUMENT). */
 fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* layer, const void* const* stagings_dev,
                                  fsdp_dtype_t grad_dtype, fsdp_dtype_t reduce_dtype, int32_t mean,
                                  int32_t accumulate, void* stream);
@@ -412,7 +420,8 @@ fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* layer, const void* const* staging
 fsdp_status_t fsdp_stage_rs_scatter(const fsdp_layer_t* layer, const void* const* full_grads_dev,
                                     fsdp_dtype_t grad_dtype, void* const* recv_dev, void* stream);
 /* Store-based reduce-scatter, receiver: for this rank's rows, grad (+)= sum over q = 0..W-1
- * ascending of fp32(recv[q * S + off_p + j]) / W (mean): the same arithmetic as the pull. */
+ * ascending of fp32(recv[q * S + off_p + j]) / W (mean): the same arithmetic as the pull.
+ * recv_dev must be 16-byte aligned (else FSDP_ERR_INVALID_ARGUMENT). */
 fsdp_status_t fsdp_stage_rs_recv_reduce(fsdp_layer_t* layer, const void* recv_dev, fsdp_dtype_t grad_dtype,
                                         fsdp_dtype_t reduce_dtype, int32_t mean, int32_t accumulate,
                                         void* stream);

@@ -227,6 +227,7 @@ struct SymSlot {
 constexpr int kFlagSlots = 512;  // flag slots per kind: pooled slots first, then layer grad buffers
 constexpr int kPoolSlots = 64;   // max pooled symmetric slots (arenas / staging) per pool
 constexpr int kHistMax = 64;     // max delayed-scaling amax history length
+constexpr int kRegCapDefault = 65536;   // fp8 registry entries per mesh (FSDP_B200_REGISTRY_CAP)
 enum FlagKind { FK_AG_READY = 0, FK_AG_DONE = 1, FK_RS_READY = 2, FK_RS_DONE = 3, FK_NUM = 4 };
 
 enum LayerState { SHARDED = 0, UNSHARDING = 1, UNSHARDED = 2 };
@@ -249,7 +250,8 @@ struct fsdp_mesh {
   fsdpk::LaunchCfg cfg{};
   std::vector<Slot*> ag_slots, rs_slots;
   uint64_t use_seq = 0;
-  // fp8 scale registry: one entry per param of every layer (contiguous per layer)
+  // fp8 scale registry: one entry per param of every layer (contiguous per layer); fixed
+  // capacity, never reallocated (pointers from fsdp_fp8_scales stay valid)
   int reg_size = 0, reg_cap = 0;
   uint32_t* reg_acc = nullptr;
   float* reg_amax = nullptr;
@@ -346,7 +348,9 @@ void check_mesh(const fsdp_mesh* m);
 void check_layer(const fsdp_layer* l);
 void check_param(const fsdp_layer* l, int p);
 bool comm_ready(const fsdp_mesh* m);
-void ensure_registry(fsdp_mesh* m, int need);
+void registry_init(fsdp_mesh* m);
+int registry_reserve(fsdp_mesh* m, int n);
+void registry_ensure_hist(fsdp_mesh* m);
 void clear_presets(fsdp_mesh* m);
 int64_t dtype_size(fsdp_dtype_t d);
 void mesh_barrier(fsdp_mesh* m);
@@ -368,6 +372,11 @@ int64_t cin_bytes(const fsdp_layer* l, bool fp8);
 int64_t slot_bytes(const fsdp_layer* l, bool fp8);
 void do_copy_in(fsdp_layer* l, bool fp8, const float* scales, void* dst, cudaStream_t st);
 void validate_grads(const fsdp_layer* l, const void* const* grads, fsdp_dtype_t gd, fsdp_dtype_t rd);
+// TMA bulk copies and 16-byte vector accesses address caller buffers relative to their base:
+// the base must be 16-byte aligned (FSDP_ERR_INVALID_ARGUMENT otherwise, before any launch)
+inline void check_align16(const void* p, const char* what) {
+  if (reinterpret_cast<uintptr_t>(p) & 15u) fail(FSDP_ERR_INVALID_ARGUMENT, std::string(what) + " is not 16-byte aligned");
+}
 
 
 // ---- profiling helpers

@@ -88,9 +88,7 @@ fsdp_status_t fsdp_shard(fsdp_mesh_t* m, int32_t n, const fsdp_param_desc_t* des
         l->grad_numel_total += Ly.numel[p];
       }
       // fp8 registry entries [reg_base, reg_base + P)
-      ensure_registry(m, m->reg_size + n);
-      l->reg_base = m->reg_size;
-      m->reg_size += n;
+      l->reg_base = registry_reserve(m, n);
       CUDA_CHECK(cudaMemcpy(m->reg_elig + l->reg_base, Ly.fp8.data(), n, cudaMemcpyHostToDevice));
       std::vector<int32_t> idx(n);
       for (int p = 0; p < n; ++p) idx[p] = p;
@@ -235,6 +233,7 @@ static fsdp_status_t precompute_impl(fsdp_mesh_t* m, fsdp_layer_t* const* layers
         CUDA_CHECK(fsdpk::launch_fp8_scale(ps->idx, ps->nidx, m->reg_acc, m->reg_amax, m->reg_scale, m->reg_elig,
                                            m->d_err, true, m->s_rs));
       } else {
+        registry_ensure_hist(m);
         m->hist_len = history_len;
         CUDA_CHECK(fsdpk::launch_fp8_scale_delayed(ps->idx, ps->nidx, m->reg_acc, m->reg_amax, m->reg_scale,
                                                    m->reg_elig, m->reg_hist, m->reg_pos, m->reg_hinit, history_len,
@@ -559,12 +558,17 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       // handshake -> pull (every rank's rows of this rank, /divisor, ascending-rank fp32 sum,
       // written into the grad buffer) -> done handshake (staging reusable)
       const int64_t gsz = dtype_size(gd);
-      // zero copy: the caller's grads already live in this layer's symmetric grad buffer
-      bool zc = l->gbuf && l->gbuf_sym && gd == l->gbuf_dtype;
+      // zero copy: the caller's grads already live in this layer's symmetric grad buffer.
+      // Which buffer peers pull from (and its flag slot) must be the same on every rank, so
+      // it depends only on collective state: a layer with a symmetric grad buffer of this
+      // dtype always reduce-scatters through it — grads given elsewhere are staged INTO it
+      // (a rank-local copy) — and a layer without one always uses the pooled staging.
+      const bool use_gbuf = l->gbuf && l->gbuf_sym && gd == l->gbuf_dtype;
+      bool zc = use_gbuf;
       for (int p = 0; zc && p < l->P; ++p)
         zc = l->L.numel[p] == 0 || grads[p] == (const void*)((uint8_t*)l->gbuf->buf.local + l->stg_off_el[p] * gsz);
       SymSlot* ss = nullptr;
-      if (zc) {
+      if (use_gbuf) {
         ss = l->gbuf;
       } else {
         const int prefer = (int)(m->rs_rr++ % 2);   // deterministic round robin: copy of i+1 overlaps pull of i
@@ -633,8 +637,11 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
     const bool direct = !obf && !accumulate;
     const bool need_in = comm_ready(m) || !direct;
     const size_t stage_b = (comm_ready(m) && !direct) ? (size_t)(S * osz) : 0;
-    Slot* slot = acquire_slot(m, m->rs_slots, need_in ? (size_t)(m->W * S * osz) : 0,
-                              via_temp ? std::max(stage_b, (size_t)(S * 4)) : stage_b, 2, cap);
+    // HSDP + accumulate: the staging buffer b holds T (fp32 [S]) first; a bf16 reduce-scatter
+    // output goes AFTER it (b + 4S bytes), never into T itself — widening bf16 -> fp32 in
+    // place would overwrite bf16 inputs other threads have not read yet
+    const size_t t_b = via_temp ? (size_t)(S * 4) + (obf ? stage_b : 0) : stage_b;
+    Slot* slot = acquire_slot(m, m->rs_slots, need_in ? (size_t)(m->W * S * osz) : 0, t_b, 2, cap);
     CUDA_CHECK(cudaEventRecord(l->ev_rcall, cs));
     CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, l->ev_rcall, 0));
     wait_released(m->s_rsc, slot, cap);
@@ -650,6 +657,7 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
     const void* rs_out = rs_in;   // W == 1: the reduce-scatter is the identity
     if (comm_ready(m)) {
       void* out = direct ? (void*)l->grad : slot->b.p;
+      if (via_temp && obf) out = (uint8_t*)slot->b.p + (size_t)S * 4;   // behind T (see acquire above)
       ProfScope pr(m, FSDP_PROF_REDUCE_SCATTER, m->s_rs, (int64_t)(m->W - 1) * S * osz);
       NCCL_CHECK(ncclReduceScatter(rs_in, out, (size_t)S, obf ? ncclBfloat16 : ncclFloat32, ncclSum, m->comm_rs,
                                    m->s_rs));

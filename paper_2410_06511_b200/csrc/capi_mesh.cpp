@@ -93,6 +93,7 @@ static void mesh_common_init(fsdp_mesh* m) {
   m->ev_pre_done = new_event();
   CUDA_CHECK(cudaMalloc(&m->d_barrier, sizeof(int)));
   CUDA_CHECK(cudaMemset(m->d_barrier, 0, sizeof(int)));
+  registry_init(m);
 }
 
 // P2P capability: W in [2, 8] and every rank can map every peer's buffer (collective).

@@ -133,6 +133,7 @@ fsdp_status_t fsdp_stage_unshard_push(const fsdp_layer_t* lc, fsdp_dtype_t dt, c
     fsdpp::PeerPtrs pp{};
     for (int r = 0; r < m->W; ++r) {
       if (!arenas[r]) fail(FSDP_ERR_INVALID_ARGUMENT, "arenas[r] is NULL");
+      check_align16(arenas[r], "arenas[r]");
       pp.p[r] = (uint8_t*)arenas[r];
     }
     DeviceGuard g(m->device);
@@ -180,6 +181,7 @@ fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* l, const void* const* stagings, f
     fsdpp::PeerPtrs pp{};
     for (int r = 0; r < m->W; ++r) {
       if (!stagings[r]) fail(FSDP_ERR_INVALID_ARGUMENT, "stagings[r] is NULL");
+      check_align16(stagings[r], "stagings[r]");
       pp.p[r] = (uint8_t*)stagings[r];
     }
     DeviceGuard g(m->device);
@@ -221,6 +223,7 @@ fsdp_status_t fsdp_stage_rs_recv_reduce(fsdp_layer_t* l, const void* recv, fsdp_
     fsdp_mesh* m = l->mesh;
     if (m->W > 8) fail(FSDP_ERR_UNAVAILABLE, "the store-based reduce-scatter supports W <= 8");
     if (!recv) fail(FSDP_ERR_INVALID_ARGUMENT, "recv_dev is NULL");
+    check_align16(recv, "recv_dev");
     if (gd != FSDP_BFLOAT16 && gd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "grad_dtype must be BFLOAT16 or FLOAT32");
     if (rd != FSDP_BFLOAT16 && rd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "reduce_dtype must be FLOAT32 or BFLOAT16");
     const int64_t gsz = dtype_size(gd);

@@ -105,49 +105,54 @@ void check_param(const fsdp_layer* l, int p) {
 
 bool comm_ready(const fsdp_mesh* m) { return !m->local && m->W > 1; }
 
-void ensure_registry(fsdp_mesh* m, int need) {
-  if (need <= m->reg_cap) return;
-  int cap = std::max(need, std::max(64, 2 * m->reg_cap));
-  uint32_t* acc;
-  float *amax, *scale;
-  uint8_t* elig;
-  CUDA_CHECK(cudaMalloc(&acc, sizeof(uint32_t) * cap));
-  CUDA_CHECK(cudaMalloc(&amax, sizeof(float) * cap));
-  CUDA_CHECK(cudaMalloc(&scale, sizeof(float) * cap));
-  CUDA_CHECK(cudaMalloc(&elig, cap));
-  CUDA_CHECK(cudaMemset(acc, 0, sizeof(uint32_t) * cap));
-  CUDA_CHECK(cudaMemset(amax, 0, sizeof(float) * cap));
-  CUDA_CHECK(cudaMemset(scale, 0, sizeof(float) * cap));
-  CUDA_CHECK(cudaMemset(elig, 0, cap));
-  if (m->reg_size) {
-    CUDA_CHECK(cudaDeviceSynchronize());
-    CUDA_CHECK(cudaMemcpy(acc, m->reg_acc, sizeof(uint32_t) * m->reg_size, cudaMemcpyDeviceToDevice));
-    CUDA_CHECK(cudaMemcpy(amax, m->reg_amax, sizeof(float) * m->reg_size, cudaMemcpyDeviceToDevice));
-    CUDA_CHECK(cudaMemcpy(scale, m->reg_scale, sizeof(float) * m->reg_size, cudaMemcpyDeviceToDevice));
-    CUDA_CHECK(cudaMemcpy(elig, m->reg_elig, m->reg_size, cudaMemcpyDeviceToDevice));
-  }
-  // delayed-scaling state: amax history [cap][kHistMax], ring position, initialised flag
-  float* hist;
-  int32_t* pos;
-  uint8_t* hinit;
-  CUDA_CHECK(cudaMalloc(&hist, sizeof(float) * (size_t)cap * kHistMax));
-  CUDA_CHECK(cudaMalloc(&pos, sizeof(int32_t) * cap));
-  CUDA_CHECK(cudaMalloc(&hinit, cap));
-  CUDA_CHECK(cudaMemset(hist, 0, sizeof(float) * (size_t)cap * kHistMax));
-  CUDA_CHECK(cudaMemset(pos, 0, sizeof(int32_t) * cap));
-  CUDA_CHECK(cudaMemset(hinit, 0, cap));
-  if (m->reg_size) {
-    CUDA_CHECK(cudaMemcpy(hist, m->reg_hist, sizeof(float) * (size_t)m->reg_size * kHistMax, cudaMemcpyDeviceToDevice));
-    CUDA_CHECK(cudaMemcpy(pos, m->reg_pos, sizeof(int32_t) * m->reg_size, cudaMemcpyDeviceToDevice));
-    CUDA_CHECK(cudaMemcpy(hinit, m->reg_hinit, m->reg_size, cudaMemcpyDeviceToDevice));
-  }
-  cudaFree(m->reg_acc); cudaFree(m->reg_amax); cudaFree(m->reg_scale); cudaFree(m->reg_elig);
-  cudaFree(m->reg_hist); cudaFree(m->reg_pos); cudaFree(m->reg_hinit);
-  m->reg_acc = acc; m->reg_amax = amax; m->reg_scale = scale; m->reg_elig = elig;
-  m->reg_hist = hist; m->reg_pos = pos; m->reg_hinit = hinit;
+// fp8 registry: fixed capacity, allocated once per mesh, so the device pointers handed out by
+// fsdp_fp8_scales (and baked into captured CUDA graphs) stay valid for the mesh's lifetime.
+// Entries are assigned in fsdp_shard order (a collective call, so every rank assigns alike)
+// and are recycled only once every layer of the mesh has been destroyed.
+void registry_init(fsdp_mesh* m) {
+  int cap = kRegCapDefault;
+  if (const char* e = std::getenv("FSDP_B200_REGISTRY_CAP")) cap = std::max(64, std::min(1 << 22, std::atoi(e)));
+  CUDA_CHECK(cudaMalloc(&m->reg_acc, sizeof(uint32_t) * cap));
+  CUDA_CHECK(cudaMalloc(&m->reg_amax, sizeof(float) * cap));
+  CUDA_CHECK(cudaMalloc(&m->reg_scale, sizeof(float) * cap));
+  CUDA_CHECK(cudaMalloc(&m->reg_elig, cap));
+  CUDA_CHECK(cudaMalloc(&m->reg_pos, sizeof(int32_t) * cap));
+  CUDA_CHECK(cudaMalloc(&m->reg_hinit, cap));
+  CUDA_CHECK(cudaMemset(m->reg_acc, 0, sizeof(uint32_t) * cap));
+  CUDA_CHECK(cudaMemset(m->reg_amax, 0, sizeof(float) * cap));
+  CUDA_CHECK(cudaMemset(m->reg_scale, 0, sizeof(float) * cap));
+  CUDA_CHECK(cudaMemset(m->reg_elig, 0, cap));
+  CUDA_CHECK(cudaMemset(m->reg_pos, 0, sizeof(int32_t) * cap));
+  CUDA_CHECK(cudaMemset(m->reg_hinit, 0, cap));
   m->reg_cap = cap;
-  for (auto* ps : m->presets) { ps->tiles.release(); cudaFree(ps->idx); delete ps; }
-  m->presets.clear();
+}
+
+int registry_reserve(fsdp_mesh* m, int n) {
+  if (m->layers.empty() && m->reg_size > 0) {   // every layer destroyed: start over
+    CUDA_CHECK(cudaDeviceSynchronize());
+    CUDA_CHECK(cudaMemset(m->reg_acc, 0, sizeof(uint32_t) * m->reg_size));
+    CUDA_CHECK(cudaMemset(m->reg_amax, 0, sizeof(float) * m->reg_size));
+    CUDA_CHECK(cudaMemset(m->reg_scale, 0, sizeof(float) * m->reg_size));
+    CUDA_CHECK(cudaMemset(m->reg_elig, 0, m->reg_size));
+    CUDA_CHECK(cudaMemset(m->reg_pos, 0, sizeof(int32_t) * m->reg_size));
+    CUDA_CHECK(cudaMemset(m->reg_hinit, 0, m->reg_size));
+    m->reg_size = 0;
+  }
+  if (m->reg_size + n > m->reg_cap)
+    fail(FSDP_ERR_UNAVAILABLE, "fp8 registry full (" + std::to_string(m->reg_cap) +
+                                   " params per mesh; raise FSDP_B200_REGISTRY_CAP)");
+  const int base = m->reg_size;
+  m->reg_size += n;
+  return base;
+}
+
+// the delayed-scaling amax history [reg_cap][kHistMax], allocated at the first delayed
+// precompute (16 MB at the default capacity) and never moved afterwards
+void registry_ensure_hist(fsdp_mesh* m) {
+  if (m->reg_hist) return;
+  const size_t bytes = sizeof(float) * (size_t)m->reg_cap * kHistMax;
+  CUDA_CHECK(cudaMalloc(&m->reg_hist, bytes));
+  CUDA_CHECK(cudaMemset(m->reg_hist, 0, bytes));
 }
 
 void clear_presets(fsdp_mesh* m) {

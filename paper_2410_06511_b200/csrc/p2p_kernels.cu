@@ -38,18 +38,17 @@ __global__ void k_signal_wait(FlagPtrs remote, unsigned long long* local, int W,
     e_sh = *epoch_ctr + 1;
     *epoch_ctr = e_sh;
   }
-  // No system fence around the signal / wait (-DFSDP_HS_FENCE restores them for debugging):
-  // - what a peer must see before our signal was written by EARLIER kernels (staging /
-  //   zero-copy grads; the push and scatter kernels end with their own system fence), and
-  //   kernel completion has performed those writes at this GPU's L2, where the peers' NVLink
-  //   accesses are served; reads of earlier kernels (arena / receive-buffer reuse) completed;
-  // - what we read after the wait was released by the peer before its flag, and our
-  //   ld.acquire.sys of that flag, the barrier, kernel completion and the event chain order it
-  //   before every later consumer.
-  // Dropping the two fences took the handshake chain from ~25 to ~17 us per op (toy step at
-  // W=2 under a CUDA graph 107.5 -> 81.6 us; 8B step 24.3 -> 24.0 ms).
-#ifdef FSDP_HS_FENCE
-  __threadfence_system();
+  // One system-scope fence, on one thread, on each side of the handshake: what a
+  // peer must see before our signal was written by EARLIER kernels on this stream (staging,
+  // zero-copy grads written by the caller's kernels, the push / scatter data — those two end
+  // with their own system fence); the fence orders all of it (cumulatively, through the CTA
+  // barrier below and the release store of the signalling thread) before the flag.  After
+  // the wait, the fence on the other side orders the peers' data (released before their
+  // flags, acquired by our ld.acquire.sys) before every later consumer on this stream.
+  // Single-thread fences: the 32-thread __threadfence_system pair cost ~25 us per op;
+  // -DFSDP_HS_NO_FENCE drops them (measurement only).
+#ifndef FSDP_HS_NO_FENCE
+  if (r == 0) __threadfence_system();
 #endif
   __syncthreads();
   const unsigned long long epoch = e_sh;
@@ -67,8 +66,8 @@ __global__ void k_signal_wait(FlagPtrs remote, unsigned long long* local, int W,
     }
   }
   __syncthreads();
-#ifdef FSDP_HS_FENCE
-  __threadfence_system();
+#ifndef FSDP_HS_NO_FENCE
+  if (r == 0) __threadfence_system();
 #endif
 }
 
@@ -396,6 +395,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_pull(const Tile* __restrict__ t
 // Push: threads cast a 4 KB output chunk into smem once, one thread bulk-stores it into
 // every rank's arena (cp.async.bulk shared->global, W stores per chunk, 2 stages).
 constexpr uint32_t kBulkChunk = 4096;
+static_assert(kBulkChunk / 16 == (uint32_t)kThreads, "push_tile_bulk: one 16-byte vector per thread per chunk");
 constexpr uint32_t kPullMaxStages = 4;
 constexpr size_t kPullMaxSmem = 200 * 1024;   // stages * W * chunk, leaves room for 1 CTA/SM
 

@@ -284,6 +284,22 @@ def run_hsdp_checks(W, rank, local, Ws):
                         elif not acc:
                             check_rs(got, ref, p, W, algo, kind == "dyadic", ordered=False,
                                      tag=(algo, Ws, ui))
+            # bf16 reduce with accumulate (the path that once widened bf16 -> fp32 in place):
+            # the added increment must satisfy the R11 bound against the exact mean
+            G = [[synth.grad_bf16_bits(ui + 70, p, q, sh) for p, sh in enumerate(shapes)] for q in range(W)]
+            gt = [torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16) for x in G[rank]]
+            ref = h.reduce_scatter_grads(G, BF16, True)[rank]
+            before = layer.sharded_grad_flat().clone()
+            F.reduce_scatter_grads(layer, gt, reduce_dtype=torch.bfloat16, accumulate=True)
+            F.fsdp_wait_reduce_scatter(layer)
+            for p in range(len(shapes)):
+                m = layer.metas[p]
+                got = layer.sharded_grad(p).cpu().numpy().reshape(-1).astype(np.float64)
+                prev = before[m["elem_offset"]:m["elem_offset"] + got.size].cpu().numpy().astype(np.float64)
+                ex = ref["exact"][p].reshape(-1).astype(np.float64)
+                mg = ref["mag"][p].reshape(-1)
+                bound = (2 * W - 1) * 2.0 ** -8 * mg + 2.0 ** -24 * (np.abs(prev) + np.abs(ex)) + 2.0 ** -133
+                assert np.all(np.abs(got - prev - ex) <= bound), (algo, Ws, ui, p, "bf16+acc")
             layer.destroy()
         print(f"rank {rank}/{W} hsdp {R}x{Ws} algo={algo}: OK", flush=True)
     mesh.synchronize(120000)

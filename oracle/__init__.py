@@ -23,7 +23,10 @@ fp32 is float32, exact references are float64.
 Pins: every function is pinned by ``tests/test_oracle_*.py`` (``-m "not gpu"``) against
 closed forms, torch-CPU library casts, SPEC worked examples (tests/golden/) and
 brute force.  Parity-unpinned parts: none for integer/byte work; for the fp32
-reduce-scatter of non-dyadic data only the error bound is pinned (DESIGN.md §3 R10).
+reduce-scatter of non-dyadic data only the error bound is pinned (DESIGN.md §3 R10) — and
+that bound itself (``rs_error_ok``) is pinned from both sides, as is the bf16-reduce
+branch of ``rs_copy_in`` (rounding after the single division; exact rational arithmetic),
+in tests/test_oracle_pins_r2.py.
 """
 from .layout import ParamMeta, UnitLayout, unit_layout, round_up, ALIGN_ELEMS, ALIGN_BYTES
 from .casts import (bf16_rne_bits, bf16_bits_to_f32, e4m3_table, e4m3_decode,

@@ -642,7 +642,7 @@ def _cpu_all_cores(wl, W, max_procs=16):
 
 
 def run_reference(args):
-    N = int(os.environ.get("WORLD_SIZE", "1"))
+    N = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
@@ -669,8 +669,29 @@ def run_reference(args):
             "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launcher_cmd(argv, n: int, port: int):
+    """The torchrun command a plain `python bench.py --gpus N` (N > 1, no WORLD_SIZE in the
+    environment) re-executes itself under: one rank per GPU on this node, rendezvous on
+    127.0.0.1, the same arguments."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+
+
 def main():
     args = parse()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: launch our own N ranks; rank 0 prints the JSON line
+        res = subprocess.run(launcher_cmd(sys.argv[1:], args.gpus, _free_port()), cwd=ROOT)
+        raise SystemExit(res.returncode)
     line = run_reference(args) if args.impl == "reference" else run_ours(args)
     if line is not None:
         s = json.dumps(line)

@@ -38,14 +38,31 @@ WORKLOADS = {
     "toy": dict(model="toy", fp8=False, cycle=None),
 }
 METRIC = "FSDP unshard+reshard GB/s per layer (fraction of NVLink/HBM peak)"
-NVLINK_GBS = 900.0
+NVLINK_GBS = 900.0          # NVLink 5 per direction per GPU, nominal (BASELINE.json north_star)
+NVLINK_MEASURED_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+HBM_NOMINAL_GBS = 8000.0     # "~8 TB/s" (BASELINE.json north_star)
+
+
+def wire_report(wire_rank, ms, ms_iso, W, R):
+    """Physical NVLink bytes per rank per direction per step / step time, vs 900 and 770."""
+    if not wire_rank:
+        return None
+    g = wire_rank / (ms * 1e-3) / 1e9
+    gi = wire_rank / (ms_iso * 1e-3) / 1e9
+    return {"bytes_per_step_per_rank_per_direction": int(wire_rank),
+            "GBps_per_direction": round(g, 1), "frac_of_900": round(g / NVLINK_GBS, 4),
+            "frac_of_770": round(g / NVLINK_MEASURED_GBS, 4),
+            "isolated_GBps_per_direction": round(gi, 1), "isolated_frac_of_900": round(gi / NVLINK_GBS, 4),
+            "isolated_frac_of_770": round(gi / NVLINK_MEASURED_GBS, 4),
+            "model": "P2P: (W-1) x own cast rows (push) + (W-1) x own bf16 grad rows (reduce-scatter); "
+                     "NCCL ring: (W-1) x slot + (W-1) x 4S" + ("; + fp32 replica all-reduce" if R > 1 else "")}
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=40)   # >= 30 steps and >= 0.5 s (SURVEY.md 8(d))
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="llama3.1-8b", choices=list(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
@@ -283,6 +300,29 @@ def run_ours(args):
         n_unshard = [1] * len(layers)
     bytes_rank = sum(k * W * sb + 4 * W * l.S for k, sb, l in zip(n_unshard, slot_b, layers))
 
+    # physical NVLink bytes this rank sends per step, per direction (the metric's
+    # fp32 RS bytes are not what the P2P path puts on the wire).  P2P: the push stores this
+    # rank's cast rows into W-1 peers; the reduce-scatter moves this rank's bf16 grad rows of
+    # every peer's chunk (store) / every peer's rows of this rank's chunk (pull), (W-1) x own
+    # rows x 2 B either way.  NCCL ring: (W-1) x slot bytes (AG) + (W-1) x 4S (fp32 RS).
+    # HSDP adds the fp32 replica all-reduce (NCCL ring, 2 (R-1)/R x 4S).
+    R = mesh.replicate_size if N > 1 else 1
+
+    def wire_unit(l, k):
+        if W == 1 and R == 1:
+            return 0
+        own = [m["row_count"] * m["rest"] for m in l.metas]
+        if N > 1 and mesh.algo == "p2p":
+            es = [1 if (wl["fp8"] and e) else 2 for e in l.fp8_eligible]
+            b = k * (W - 1) * sum(o * s for o, s in zip(own, es)) + (W - 1) * 2 * sum(own)
+        else:
+            sb = l.S_bytes_fp8 if wl["fp8"] else 2 * l.S
+            b = k * (W - 1) * sb + (W - 1) * 4 * l.S
+        if R > 1:
+            b += 2 * (R - 1) * 4 * l.S // R
+        return b
+    wire_rank = sum(wire_unit(l, k) for k, l in zip(n_unshard, layers))
+
     def barrier():
         if N > 1:
             dist.barrier(device_ids=[local])
@@ -322,23 +362,30 @@ def run_ours(args):
         clocks.start()
     mesh.profile_enable(True)
     mesh.profile_read(reset=True)
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]   # step boundaries
+    # before each iteration a host barrier over ranks + device sync, so all
+    # ranks start aligned; CUDA events on the launching stream bracket every step; the step
+    # time is the max over ranks per step, `ms_per_step` their mean
+    ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
-    evs[0].record(comp)
     for k in range(args.steps):
+        barrier()
+        torch.cuda.synchronize()
+        ev_a[k].record(comp)
         timed_step()
-        evs[k + 1].record(comp)
+        ev_b[k].record(comp)
     comp.synchronize()
     torch.cuda.synchronize()
     barrier()
     prof = mesh.profile_read(reset=True)
     mesh.profile_enable(False)
     clk = clocks.stop() if clocks else None
-    per_step = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
-    t = torch.tensor([evs[0].elapsed_time(evs[-1]) / args.steps] + per_step, device=dev, dtype=torch.float64)
+    per_step = [ev_a[k].elapsed_time(ev_b[k]) for k in range(args.steps)]
+    t = torch.tensor([0.0] + per_step, device=dev, dtype=torch.float64)
     if N > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t[0] = t[1:].mean()
     ms_max = float(t[0].item())
     step_pct = {"median": round(float(t[1:].median().item()), 4),
                 "p10": round(float(torch.quantile(t[1:], 0.1).item()), 4),
@@ -355,7 +402,10 @@ def run_ours(args):
     # no two of our kernels overlap and each kernel's event-timed duration is its own
     # (in the prefetch step the unshard of unit i+1 and the reduce-scatter of unit i share
     # HBM / NVLink, which inflates both durations while the step as a whole runs faster)
-    roof_steps = max(2, min(args.steps, 4))
+    # The same pass doubles as the ISOLATED step of SURVEY.md 8(d) (each unit's unshard and
+    # reduce-scatter issued and waited one after another, no cross-unit overlap), timed per
+    # step like the pipelined one, so both numbers come from one run.
+    roof_steps = max(3, min(args.steps, 6))
     serial_saved = args.serial
     args.serial = args.step == "unit"
     step()
@@ -363,12 +413,23 @@ def run_ours(args):
     barrier()
     mesh.profile_enable(True)
     mesh.profile_read(reset=True)
+    iso = []
     for _ in range(roof_steps):
+        barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(comp)
         step()
+        b.record(comp)
+        iso.append((a, b))
     comp.synchronize()
     prof = mesh.profile_read(reset=True)
     mesh.profile_enable(False)
     args.serial = serial_saved
+    ti = torch.tensor([a.elapsed_time(b) for a, b in iso], device=dev, dtype=torch.float64)
+    if N > 1:
+        dist.all_reduce(ti, op=dist.ReduceOp.MAX)
+    ms_iso = float(ti.mean().item())
     barrier()
     proxy = None
     if T:   # the same GEMMs alone, each unit's weights unsharded beforehand (outside the events)
@@ -456,8 +517,8 @@ def run_ours(args):
     line = None
     if rank == 0:
         cpu = None
-        if not args.no_cpu_baseline and N == 1:
-            cpu = cpu_baseline(args, W)
+        if not args.no_cpu_baseline:
+            cpu = cpu_baseline(args, W, full_block=(N == 1))
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "ms_per_step_pct": step_pct,
@@ -475,15 +536,26 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (every unit's shard/grads/buffers are 100s of MB; 126 MB L2)",
                        "bytes_per_step_per_rank": bytes_rank},
             "per_rank": {"algbw_GBps": round(algbw_rank, 2), "busbw_GBps": round(busbw_rank, 2),
-                         "busbw_frac_nvlink_900": round(busbw_rank / NVLINK_GBS, 4)},
+                         "busbw_frac_nvlink_900": round(busbw_rank / NVLINK_GBS, 4),
+                         "busbw_note": "metric units: counts the paper's fp32 reduce-scatter bytes; the P2P "
+                                       "path sends bf16 grads (DESIGN.md R14), so see `wire` for the link rate"},
+            "wire": wire_report(wire_rank, ms_max, ms_iso, W, R),
+            "isolated": {"ms_per_step": round(ms_iso, 4), "steps": roof_steps,
+                         "value": round(N * bytes_rank / (ms_iso * 1e-3) / 1e9, 2),
+                         "what": "same step with every unit's unshard and reduce-scatter issued serially (no "
+                                 "prefetch / cross-unit overlap), per-step barrier, max over ranks"
+                                 if args.step == "unit" else "train step (already serial per unit)"},
             "kernels": kernels,
             "kernels_serial": kernels_serial,
             "roofline": {"bound": bound, "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
                          "bytes_per_launch": int(per_launch_bytes), "traffic": traffic,
                          "sm_mechanism_ceiling": mech,
+                         "frac_of_nominal": round(achieved / (NVLINK_GBS if bound == "nvlink" else HBM_NOMINAL_GBS), 4),
+                         "nominal_peak": NVLINK_GBS if bound == "nvlink" else HBM_NOMINAL_GBS,
                          "pass": f"serial issue, {roof_steps} steps after the timed region (CUDA events on the launching streams)",
-                         "step_hbm_GBps": round(step_hbm, 1), "step_hbm_frac": round(step_hbm / measured_peaks()[0], 4)},
+                         "step_hbm_GBps": round(step_hbm, 1), "step_hbm_frac": round(step_hbm / measured_peaks()[0], 4),
+                         "step_hbm_frac_of_nominal": round(step_hbm / HBM_NOMINAL_GBS, 4)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,
         }
         if proxy:
@@ -596,19 +668,46 @@ def _oracle_step(World, BF16, FP8, shapes, elig, params, grads, W, fp8):
     return W * (W * slot + 4 * W * w.S)     # same algorithmic bytes, all simulated ranks
 
 
-def cpu_baseline(args, W):
+def host_info():
+    """CPU model, RAM, core counts of the host the CPU baseline ran on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    ram = None
+    try:
+        import psutil
+        ram = round(psutil.virtual_memory().total / 2 ** 30, 1)
+    except Exception:   # noqa: BLE001
+        pass
+    return {"cpu_model": model, "ram_GiB": ram, "os_cpu_count": os.cpu_count(),
+            "affinity_cores": len(os.sched_getaffinity(0))}
+
+
+def cpu_baseline(args, W, full_block=True):
+    """The unchanged oracle on a bounded sample of the workload, rank 0's host cores.  N = 1:
+    one full block (~15 s) plus the all-cores run; N > 1: the block's attention weights +
+    norms with all W ranks simulated (the oracle's work grows with W; bounded to ~10-30 s)."""
     from oracle import World
     from oracle.world import BF16, FP8
     wl = WORKLOADS[args.workload]
-    shapes, elig, params, grads = _oracle_sample(wl["model"], W, full_block=True)
+    shapes, elig, params, grads = _oracle_sample(wl["model"], W, full_block=full_block)
     t0 = time.perf_counter()
     nbytes = _oracle_step(World, BF16, FP8, shapes, elig, params, grads, W, wl["fp8"])
     dt = time.perf_counter() - t0
+    what = "block" if full_block else "block's attention weights + norms"
     out = {"value": round(nbytes / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
            "seconds": round(dt, 2),
-           "sample": f"one {wl['model']} block ({sum(int(np.prod(s)) for s in shapes)} params), "
-                     f"W={W} simulated ranks, unshard + reduce-scatter, single-threaded NumPy"}
-    out["all_cores"] = _cpu_all_cores(wl, W)
+           "sample": f"one {wl['model']} {what} ({sum(int(np.prod(s)) for s in shapes)} params), "
+                     f"W={W} simulated ranks, {'fp8' if wl['fp8'] else 'bf16'} unshard + fp32 reduce-scatter, "
+                     f"single-threaded NumPy",
+           "host": host_info()}
+    if full_block:
+        out["all_cores"] = _cpu_all_cores(wl, W)
     return out
 
 

@@ -416,15 +416,21 @@ fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* layer, const void* const* staging
  * full-grad rows of r's Shard(0) chunk of each param are copied into r's receive buffer
  * recv_dev[r] at slot `rank`: recv_r[(rank * S + off_p) + j] (grad_dtype elements; a receive
  * buffer is W * S elements, every slot laid out like the flat shard).  recv_dev: W pointers
- * the current device can store to (peer-mapped in the real path). */
+ * the current device can store to (peer-mapped in the real path).  include_self = 0 skips
+ * r = rank (the receiver then reads its own rows from its grads, see below). */
 fsdp_status_t fsdp_stage_rs_scatter(const fsdp_layer_t* layer, const void* const* full_grads_dev,
-                                    fsdp_dtype_t grad_dtype, void* const* recv_dev, void* stream);
+                                    fsdp_dtype_t grad_dtype, void* const* recv_dev, int32_t include_self,
+                                    void* stream);
 /* Store-based reduce-scatter, receiver: for this rank's rows, grad (+)= sum over q = 0..W-1
- * ascending of fp32(recv[q * S + off_p + j]) / W (mean): the same arithmetic as the pull.
- * recv_dev must be 16-byte aligned (else FSDP_ERR_INVALID_ARGUMENT). */
-fsdp_status_t fsdp_stage_rs_recv_reduce(fsdp_layer_t* layer, const void* recv_dev, fsdp_dtype_t grad_dtype,
-                                        fsdp_dtype_t reduce_dtype, int32_t mean, int32_t accumulate,
-                                        void* stream);
+ * ascending of fp32(x_q) / W (mean): the same arithmetic as the pull.  x_q = recv[q * S +
+ * off_p + j]; when own_grads_dev (P pointers, this rank's full grads) is not NULL, x_rank
+ * is read from own_grads_dev[p] + row_begin * rest + j instead of slot `rank` (the default
+ * P2P path does this: no own-slot copy).  recv_dev and the own grads must be 16-byte aligned,
+ * and with own_grads_dev every own-row offset row_begin * rest * grad_size must be a multiple
+ * of 16 bytes (else FSDP_ERR_INVALID_ARGUMENT; the P2P path then uses the own slot). */
+fsdp_status_t fsdp_stage_rs_recv_reduce(fsdp_layer_t* layer, const void* recv_dev, const void* const* own_grads_dev,
+                                        fsdp_dtype_t grad_dtype, fsdp_dtype_t reduce_dtype, int32_t mean,
+                                        int32_t accumulate, void* stream);
 
 #ifdef __cplusplus
 }

@@ -283,6 +283,7 @@ struct fsdp_mesh {
   int algo = FSDP_ALGO_NCCL;
   int p2p_rs_mode = FSDP_P2P_RS_AUTO;        // how the P2P reduce-scatter moves data
   int reduce_per_sm = 2;                     // store-RS local reduce CTAs/SM (0: default grid; 2 measured best)
+  bool store_own_direct = true;              // store RS: own rows read from the caller's grads (FSDP_B200_STORE_OWN=0: own slot)
   bool p2p_ok = false;
   SymBuf flags;                              // uint64 [FK_NUM][kFlagSlots][kMaxRanks]
   std::vector<SymSlot*> p2p_ag, p2p_rs;      // unsharded arenas, grad staging
@@ -320,6 +321,10 @@ struct fsdp_layer {
   // P2P path
   DevTiles t_push_bf16, t_push_fp8, t_pull, t_stage_bf16, t_stage_fp32;
   DevTiles t_scatter_bf16, t_scatter_fp32, t_recv;   // store-based reduce-scatter
+  // store RS with the own rows read from the caller's grads: scatter tables without the
+  // own chunk, receiver tiles with the own-row source offsets (layout.h)
+  DevTiles t_scatter_peers_bf16, t_scatter_peers_fp32, t_recv_own;
+  bool own_ok_bf16 = false, own_ok_fp32 = false;   // own-row offsets 16-byte aligned
   std::vector<int64_t> stg_off_el;   // full-grad staging: param p at element offset (128-aligned)
   int64_t stg_elems = 0;
   int64_t push_bytes_bf16 = 0, push_bytes_fp8 = 0, pull_elems = 0;

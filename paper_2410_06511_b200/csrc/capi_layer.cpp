@@ -67,6 +67,11 @@ fsdp_status_t fsdp_shard(fsdp_mesh_t* m, int32_t n, const fsdp_param_desc_t* des
       l->t_scatter_bf16.upload(fsdpl::tiles_scatter(Ly, 2));
       l->t_scatter_fp32.upload(fsdpl::tiles_scatter(Ly, 4));
       l->t_recv.upload(fsdpl::tiles_recv_reduce(Ly));
+      l->t_scatter_peers_bf16.upload(fsdpl::tiles_scatter(Ly, 2, false));
+      l->t_scatter_peers_fp32.upload(fsdpl::tiles_scatter(Ly, 4, false));
+      l->t_recv_own.upload(fsdpl::tiles_recv_reduce_own(Ly));
+      l->own_ok_bf16 = fsdpl::own_rows_aligned(Ly, 2);
+      l->own_ok_fp32 = fsdpl::own_rows_aligned(Ly, 4);
       for (int p = 0; p < n; ++p) {
         const int64_t cnt = Ly.metas[p].row_count * Ly.metas[p].rest;
         const int64_t es8 = Ly.fp8[p] ? 1 : 2;
@@ -121,6 +126,7 @@ fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* l) {
     l->t_push_bf16.release(); l->t_push_fp8.release(); l->t_pull.release(); l->t_stage_bf16.release();
     l->t_stage_fp32.release(); l->t_amax_stage.release();
     l->t_scatter_bf16.release(); l->t_scatter_fp32.release(); l->t_recv.release();
+    l->t_scatter_peers_bf16.release(); l->t_scatter_peers_fp32.release(); l->t_recv_own.release();
     if (l->gbuf) {
       if (l->gbuf_sym && !m->aborted) sym_free(m, l->gbuf->buf);   // collective
       else if (l->gbuf_sym) sym_free_local(m, l->gbuf->buf);
@@ -507,10 +513,17 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
                                              m->d_err, m->s_rs));
         ph.done();
       }
+      // own rows: read by the local reduce straight from the caller's grads (no own-slot copy,
+      // 4 B of HBM per own bf16 element less) when every own-row source is 16-byte aligned;
+      // purely local, so ranks may decide differently
+      fsdpk::PtrArray pa{};
+      for (int p = 0; p < l->P; ++p) pa.p[p] = grads[p];
+      bool own_direct = m->store_own_direct && (gd == FSDP_BFLOAT16 ? l->own_ok_bf16 : l->own_ok_fp32);
+      for (int p = 0; own_direct && p < l->P; ++p)
+        if (l->L.metas[p].row_count > 0 && ((uintptr_t)grads[p] & 15u) != 0) own_direct = false;
       {
-        const DevTiles& T = gd == FSDP_BFLOAT16 ? l->t_scatter_bf16 : l->t_scatter_fp32;
-        fsdpk::PtrArray pa{};
-        for (int p = 0; p < l->P; ++p) pa.p[p] = grads[p];
+        const DevTiles& T = own_direct ? (gd == FSDP_BFLOAT16 ? l->t_scatter_peers_bf16 : l->t_scatter_peers_fp32)
+                                       : (gd == FSDP_BFLOAT16 ? l->t_scatter_bf16 : l->t_scatter_fp32);
         ProfScope pp(m, FSDP_PROF_RS_SCATTER, m->s_rs, l->scatter_elems * gsz);
         CUDA_CHECK(fsdpp::launch_rs_scatter(T.d, T.n, pa, peer_ptrs(m, ss->buf), m->cfg, m->s_rs));
         pp.done();
@@ -537,8 +550,13 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
         fsdpk::LaunchCfg rcfg = m->cfg;   // the reduce overlaps the next unit's transfers: its grid
         if (m->reduce_per_sm > 0) rcfg.per_sm = m->reduce_per_sm;   // can leave them SMs
         ProfScope pr(m, FSDP_PROF_RS_REDUCE, m->s_rsc, l->pull_elems * (m->W * gsz + 4 + (acc ? 4 : 0)));
-        CUDA_CHECK(fsdpp::launch_rs_pull(l->t_recv.d, l->t_recv.n, slots, gd == FSDP_BFLOAT16, divisor, target,
-                                         mean != 0, acc, obf, m->W, rcfg, m->s_rsc));
+        if (own_direct)
+          CUDA_CHECK(fsdpp::launch_rs_reduce_own(l->t_recv_own.d, l->t_recv_own.n, ss->buf.local, S, gd == FSDP_BFLOAT16,
+                                                 pa, l->L.rank, divisor, target, mean != 0, acc, obf, m->W, rcfg,
+                                                 m->s_rsc));
+        else
+          CUDA_CHECK(fsdpp::launch_rs_pull(l->t_recv.d, l->t_recv.n, slots, gd == FSDP_BFLOAT16, divisor, target,
+                                           mean != 0, acc, obf, m->W, rcfg, m->s_rsc));
         pr.done();
       }
       release_sym_slot(ss, m->s_rsc, cap);

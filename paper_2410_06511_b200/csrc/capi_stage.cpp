@@ -193,7 +193,7 @@ fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* l, const void* const* stagings, f
 }
 
 fsdp_status_t fsdp_stage_rs_scatter(const fsdp_layer_t* lc, const void* const* grads, fsdp_dtype_t gd,
-                                    void* const* recv, void* stream) {
+                                    void* const* recv, int32_t include_self, void* stream) {
   return guarded([&] {
     fsdp_layer* l = const_cast<fsdp_layer*>(lc);
     check_layer(l);
@@ -208,7 +208,8 @@ fsdp_status_t fsdp_stage_rs_scatter(const fsdp_layer_t* lc, const void* const* g
     }
     fsdpk::PtrArray pa{};
     for (int p = 0; p < l->P; ++p) pa.p[p] = grads[p];
-    const DevTiles& T = gd == FSDP_BFLOAT16 ? l->t_scatter_bf16 : l->t_scatter_fp32;
+    const DevTiles& T = include_self ? (gd == FSDP_BFLOAT16 ? l->t_scatter_bf16 : l->t_scatter_fp32)
+                                     : (gd == FSDP_BFLOAT16 ? l->t_scatter_peers_bf16 : l->t_scatter_peers_fp32);
     DeviceGuard g(m->device);
     ProfScope ps(m, FSDP_PROF_RS_SCATTER, as_stream(stream), l->scatter_elems * dtype_size(gd));
     CUDA_CHECK(fsdpp::launch_rs_scatter(T.d, T.n, pa, pp, m->cfg, as_stream(stream)));
@@ -216,8 +217,9 @@ fsdp_status_t fsdp_stage_rs_scatter(const fsdp_layer_t* lc, const void* const* g
   });
 }
 
-fsdp_status_t fsdp_stage_rs_recv_reduce(fsdp_layer_t* l, const void* recv, fsdp_dtype_t gd, fsdp_dtype_t rd,
-                                        int32_t mean, int32_t accumulate, void* stream) {
+fsdp_status_t fsdp_stage_rs_recv_reduce(fsdp_layer_t* l, const void* recv, const void* const* own_grads,
+                                        fsdp_dtype_t gd, fsdp_dtype_t rd, int32_t mean, int32_t accumulate,
+                                        void* stream) {
   return guarded([&] {
     check_layer(l);
     fsdp_mesh* m = l->mesh;
@@ -229,10 +231,25 @@ fsdp_status_t fsdp_stage_rs_recv_reduce(fsdp_layer_t* l, const void* recv, fsdp_
     const int64_t gsz = dtype_size(gd);
     fsdpp::PeerPtrs slots{};
     for (int q = 0; q < m->W; ++q) slots.p[q] = (uint8_t*)recv + (size_t)q * l->L.S * gsz;
+    fsdpk::PtrArray pa{};
+    if (own_grads) {
+      validate_grads(l, own_grads, gd, FSDP_FLOAT32);
+      if (!(gd == FSDP_BFLOAT16 ? l->own_ok_bf16 : l->own_ok_fp32))
+        fail(FSDP_ERR_INVALID_ARGUMENT, "own-row offsets of this layout are not 16-byte aligned for this grad dtype");
+      for (int p = 0; p < l->P; ++p) {
+        if (l->L.metas[p].row_count > 0) check_align16(own_grads[p], "own_grads_dev[p]");
+        pa.p[p] = own_grads[p];
+      }
+    }
     DeviceGuard g(m->device);
     ProfScope ps(m, FSDP_PROF_RS_REDUCE, as_stream(stream), l->pull_elems * (m->W * gsz + 4));
-    CUDA_CHECK(fsdpp::launch_rs_pull(l->t_recv.d, l->t_recv.n, slots, gd == FSDP_BFLOAT16, m->W * m->R, l->grad,
-                                     mean != 0, accumulate != 0, rd == FSDP_BFLOAT16, m->W, m->cfg, as_stream(stream)));
+    if (own_grads)
+      CUDA_CHECK(fsdpp::launch_rs_reduce_own(l->t_recv_own.d, l->t_recv_own.n, recv, l->L.S, gd == FSDP_BFLOAT16, pa,
+                                             l->L.rank, m->W * m->R, l->grad, mean != 0, accumulate != 0,
+                                             rd == FSDP_BFLOAT16, m->W, m->cfg, as_stream(stream)));
+    else
+      CUDA_CHECK(fsdpp::launch_rs_pull(l->t_recv.d, l->t_recv.n, slots, gd == FSDP_BFLOAT16, m->W * m->R, l->grad,
+                                       mean != 0, accumulate != 0, rd == FSDP_BFLOAT16, m->W, m->cfg, as_stream(stream)));
     ps.done();
   });
 }

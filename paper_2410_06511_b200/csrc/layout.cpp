@@ -242,7 +242,7 @@ std::vector<fsdpk::Tile> tiles_pull(const Layout& L, const std::vector<int64_t>&
   return t;
 }
 
-std::vector<fsdpk::Tile> tiles_scatter(const Layout& L, int64_t gsize) {
+std::vector<fsdpk::Tile> tiles_scatter(const Layout& L, int64_t gsize, bool include_self) {
   // per-destination lists, then merged round robin: a persistent grid walks the table in
   // order, so every destination (and this rank's own slot, a local copy) is in flight at
   // once instead of one destination after another
@@ -252,6 +252,7 @@ std::vector<fsdpk::Tile> tiles_scatter(const Layout& L, int64_t gsize) {
   const int64_t tb = tile_size_for(total, fsdpk::kTileBytes, 2048, 512);
   for (int i = 0; i < L.W; ++i) {
     const int r = (L.rank + 1 + i) % L.W;   // destination rank, rotated per sender
+    if (r == L.rank && !include_self) continue;
     for (size_t p = 0; p < L.metas.size(); ++p) {
       const auto& m = L.metas[p];
       const int64_t b = std::min<int64_t>((int64_t)r * m.chunk_rows, m.dim0);
@@ -295,6 +296,21 @@ std::vector<fsdpk::Tile> tiles_recv_reduce(const Layout& L) {
     }
   }
   return t;
+}
+
+std::vector<fsdpk::Tile> tiles_recv_reduce_own(const Layout& L) {
+  std::vector<fsdpk::Tile> t = tiles_recv_reduce(L);
+  for (auto& x : t) {
+    const auto& m = L.metas[x.param];
+    x.src = (uint64_t)(m.row_begin * m.rest) + (x.dst - (uint64_t)m.elem_offset);
+  }
+  return t;
+}
+
+bool own_rows_aligned(const Layout& L, int64_t gsize) {
+  for (const auto& m : L.metas)
+    if (m.row_count > 0 && (m.row_begin * m.rest * gsize) % 16 != 0) return false;
+  return true;
 }
 
 std::vector<fsdpk::Tile> tiles_stage(const Layout& L, const std::vector<int64_t>& stg_off, int64_t gsize) {

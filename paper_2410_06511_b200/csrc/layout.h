@@ -58,10 +58,18 @@ std::vector<fsdpk::Tile> tiles_stage(const Layout& L, const std::vector<int64_t>
 // Store-based reduce-scatter, sender side: for every destination rank r (rotated from
 // rank + 1), this rank's full-grad rows of r's Shard(0) chunk of each param go into r's
 // receive buffer [W][S] at slot `rank`: src = byte offset into grads[param], dst = byte
-// offset (rank * S + off_p) * gsize + j, pad = r.
-std::vector<fsdpk::Tile> tiles_scatter(const Layout& L, int64_t gsize);
+// offset (rank * S + off_p) * gsize + j, pad = r.  include_self = false leaves out the
+// tiles of this rank's own chunk (the receiver then reads them from its own grads).
+std::vector<fsdpk::Tile> tiles_scatter(const Layout& L, int64_t gsize, bool include_self = true);
 // Store-based reduce-scatter, receiver side: this rank's rows, src = dst = element offset
 // off_p + j (the same in every slot of the receive buffer and in the fp32 grad).
 std::vector<fsdpk::Tile> tiles_recv_reduce(const Layout& L);
+// Receiver side reading this rank's own rows from its full grads (no own-slot copy):
+// dst = off_p + j (receive slots and fp32 grad), src = row_begin * rest + j (element
+// offset into grads[param]).
+std::vector<fsdpk::Tile> tiles_recv_reduce_own(const Layout& L);
+// True when every own-row source offset row_begin * rest * gsize is a multiple of 16 bytes
+// (with 16-byte aligned grad bases the own-row reduce needs no realignment).
+bool own_rows_aligned(const Layout& L, int64_t gsize);
 
 }  // namespace fsdpl

@@ -63,4 +63,12 @@ cudaError_t launch_gather_copy(const fsdpk::Tile* tiles, int ntiles, const fsdpk
 cudaError_t launch_rs_scatter(const fsdpk::Tile* tiles, int ntiles, const fsdpk::PtrArray& grads, PeerPtrs dests,
                               fsdpk::LaunchCfg cfg, cudaStream_t st);
 
+// Store-based reduce-scatter, receiver reading its own rows from its full grads (layout.h
+// tiles_recv_reduce_own): for q != me the rows come from slot q of recv ([W][S] grad
+// elements), for q == me from own.p[param] + src; grad[dst+e] (+)= round?(sum_q fp32(x_q)/W).
+// recv and every own source must be 16-byte aligned (the caller checks).
+cudaError_t launch_rs_reduce_own(const fsdpk::Tile* tiles, int ntiles, const void* recv, int64_t S, bool grad_bf16,
+                                const fsdpk::PtrArray& own, int me, int divisor, float* grad, bool mean,
+                                bool accumulate, bool bf16_reduce, int W, fsdpk::LaunchCfg cfg, cudaStream_t st);
+
 }  // namespace fsdpp

@@ -388,6 +388,48 @@ __global__ void __launch_bounds__(kThreads) k_rs_pull(const Tile* __restrict__ t
   }
 }
 
+// ------------------------------------------------------------------- store RS, own rows direct
+// Receiver of the store-based reduce-scatter reading this rank's OWN rows straight from its
+// full grads instead of from an own receive slot the scatter would have copied them into
+// (saves 4 bytes of HBM per own bf16 element).  Source q is slot q of the local
+// receive buffer for q != me and the caller's grads for q == me; the arithmetic is the pull's
+// (every term / divisor, ascending-rank fp32 sum), so the bits are identical.  All sources are
+// local HBM and 16-byte aligned (tile dst = off_p + j; own source checked by the caller):
+// 16-byte loads, 8 elements per thread per vector (pull_body8).
+template <int W, bool kGradBf16>
+__global__ void __launch_bounds__(kThreads) k_rs_reduce_own(const Tile* __restrict__ tiles, int ntiles,
+                                                            const uint8_t* recv, uint64_t slot_bytes,
+                                                            fsdpk::PtrArray own, int me, float* __restrict__ grad,
+                                                            PullOps ops) {
+  constexpr uint32_t gs = kGradBf16 ? 2 : 4;
+  pdl_wait();
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    const uint64_t sb = tl.dst * gs;   // byte offset in every receive slot
+    const uintptr_t ownp = (uintptr_t)own.p[tl.param] + tl.src * gs;
+    PeerPtrs st;
+#pragma unroll
+    for (int q = 0; q < W; ++q)   // st.p[q] + sb = the address of source q's rows
+      st.p[q] = (q == me) ? (uint8_t*)(ownp - sb) : const_cast<uint8_t*>(recv) + (uint64_t)q * slot_bytes;
+    float* g = grad + tl.dst;
+    const uint32_t n = tl.n;
+    const uint32_t nv = n / 8;
+    pull_body8<W, kGradBf16, true>(st, sb, g, nv, 0, ops);
+    for (uint32_t e = nv * 8 + threadIdx.x; e < n; e += kThreads) {
+      float a = 0.0f;
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        const uint8_t* p = st.p[q] + sb + (uint64_t)gs * e;
+        const float x = kGradBf16 ? __uint_as_float(((uint32_t)(*(const uint16_t*)p)) << 16) : *(const float*)p;
+        const float y = ops.rb(ops.div(x));
+        a = q == 0 ? y : __fadd_rn(a, y);
+      }
+      a = ops.rb(a);
+      g[e] = ops.acc ? __fadd_rn(g[e], a) : a;
+    }
+  }
+}
+
 // ------------------------------------------------------------------- TMA bulk variants
 // Pull: the TMA engine brings each rank's chunk (LaunchCfg::pull_chunk, 4 KB default) of the
 // tile into shared memory (cp.async.bulk global->shared, mbarrier complete_tx, pull_stages
@@ -702,6 +744,33 @@ cudaError_t launch_pull_w(const Tile* tiles, int ntiles, PeerPtrs st, float* gra
                        : launch_pull_wv<kGradBf16, 4>(tiles, ntiles, st, grad, ops, W, g, s, pdl);
 }
 
+template <bool kGradBf16>
+cudaError_t launch_reduce_own_w(const Tile* tiles, int ntiles, const uint8_t* recv, uint64_t slot_bytes,
+                                const fsdpk::PtrArray& own, int me, float* grad, PullOps ops, int W, int g,
+                                cudaStream_t s, bool pdl) {
+  switch (W) {
+#define FSDP_OWN_CASE(w) \
+    case w: return launch_p(pdl, k_rs_reduce_own<w, kGradBf16>, g, 0, s, tiles, ntiles, recv, slot_bytes, own, me, grad, ops);
+    FSDP_OWN_CASE(1) FSDP_OWN_CASE(2) FSDP_OWN_CASE(3) FSDP_OWN_CASE(4)
+    FSDP_OWN_CASE(5) FSDP_OWN_CASE(6) FSDP_OWN_CASE(7) FSDP_OWN_CASE(8)
+#undef FSDP_OWN_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+PullOps make_ops(int divisor, bool mean, bool accumulate, bool bf16_reduce, const fsdpk::LaunchCfg& cfg) {
+  PullOps ops;
+  ops.w = (float)divisor;
+  ops.inv = 1.0f / (float)divisor;
+  ops.pow2 = (divisor & (divisor - 1)) == 0;
+  ops.mean = mean;
+  ops.acc = accumulate;
+  ops.bf16r = bf16_reduce;
+  ops.chunk = (uint32_t)cfg.pull_chunk;
+  ops.stages = (uint32_t)std::min<int>(std::max(cfg.pull_stages, 2), (int)kPullMaxStages);
+  return ops;
+}
+
 }  // namespace
 
 cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
@@ -726,15 +795,7 @@ cudaError_t launch_unshard_push(const Tile* tiles, int ntiles, const float* shar
 cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool grad_bf16, int divisor, float* grad, bool mean,
                            bool accumulate, bool bf16_reduce, int W, fsdpk::LaunchCfg cfg, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
-  PullOps ops;
-  ops.w = (float)divisor;
-  ops.inv = 1.0f / (float)divisor;
-  ops.pow2 = (divisor & (divisor - 1)) == 0;
-  ops.mean = mean;
-  ops.acc = accumulate;
-  ops.bf16r = bf16_reduce;
-  ops.chunk = (uint32_t)cfg.pull_chunk;
-  ops.stages = (uint32_t)std::min<int>(std::max(cfg.pull_stages, 2), (int)kPullMaxStages);
+  const PullOps ops = make_ops(divisor, mean, accumulate, bf16_reduce, cfg);
   const int g = grid_for(ntiles, cfg);
   return grad_bf16 ? launch_pull_w<true>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant, cfg.pdl)
                    : launch_pull_w<false>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant, cfg.pdl);
@@ -751,6 +812,19 @@ cudaError_t launch_rs_scatter(const Tile* tiles, int ntiles, const fsdpk::PtrArr
   if (ntiles == 0) return cudaSuccess;
   return launch_p(cfg.pdl, k_rs_scatter, grid_for(ntiles, cfg, fsdpk::kCtasPush), 0, st, tiles, ntiles, grads,
                            dests);
+}
+
+cudaError_t launch_rs_reduce_own(const Tile* tiles, int ntiles, const void* recv, int64_t S, bool grad_bf16,
+                                const fsdpk::PtrArray& own, int me, int divisor, float* grad, bool mean, bool accumulate,
+                                bool bf16_reduce, int W, fsdpk::LaunchCfg cfg, cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  const PullOps ops = make_ops(divisor, mean, accumulate, bf16_reduce, cfg);
+  const int g = grid_for(ntiles, cfg);
+  const uint64_t slot_bytes = (uint64_t)S * (grad_bf16 ? 2 : 4);
+  return grad_bf16 ? launch_reduce_own_w<true>(tiles, ntiles, (const uint8_t*)recv, slot_bytes, own, me, grad, ops, W, g,
+                                               st, cfg.pdl)
+                   : launch_reduce_own_w<false>(tiles, ntiles, (const uint8_t*)recv, slot_bytes, own, me, grad, ops, W,
+                                                g, st, cfg.pdl);
 }
 
 }  // namespace fsdpp

@@ -488,15 +488,20 @@ def stage_rs_pull(layer: Layer, stagings: Sequence[torch.Tensor], grad_dtype, re
          _dtype_code(reduce_dtype), int(bool(mean)), int(bool(accumulate)), _stream(stream))
 
 
-def stage_rs_scatter(layer: Layer, grads: Sequence[torch.Tensor], recvs: Sequence[torch.Tensor], stream=None):
+def stage_rs_scatter(layer: Layer, grads: Sequence[torch.Tensor], recvs: Sequence[torch.Tensor],
+                     include_self: bool = True, stream=None):
     """Store RS sender: this rank's rows of every rank r's chunk -> recvs[r] at slot `rank`
-    (each receive buffer: W * S elements of the grads' dtype)."""
+    (each receive buffer: W * S elements of the grads' dtype); include_self=False skips the
+    own chunk (the receiver reads it from its grads)."""
     call("fsdp_stage_rs_scatter", layer.handle, _ptr_array(grads), _dtype_code(grads[0].dtype),
-         _ptr_array(recvs), _stream(stream))
+         _ptr_array(recvs), int(bool(include_self)), _stream(stream))
 
 
 def stage_rs_recv_reduce(layer: Layer, recv: torch.Tensor, grad_dtype, reduce_dtype=torch.float32,
-                         mean: bool = True, accumulate: bool = False, stream=None):
-    """Store RS receiver: grad (+)= ascending-rank fp32 sum over the W slots of recv / W."""
-    call("fsdp_stage_rs_recv_reduce", layer.handle, C.c_void_p(recv.data_ptr()), _dtype_code(grad_dtype),
+                         mean: bool = True, accumulate: bool = False, own_grads: Optional[Sequence[torch.Tensor]] = None,
+                         stream=None):
+    """Store RS receiver: grad (+)= ascending-rank fp32 sum over the W slots of recv / W; with
+    own_grads, this rank's own rows come from its full grads instead of slot `rank`."""
+    own = _ptr_array(own_grads) if own_grads is not None else None
+    call("fsdp_stage_rs_recv_reduce", layer.handle, C.c_void_p(recv.data_ptr()), own, _dtype_code(grad_dtype),
          _dtype_code(reduce_dtype), int(bool(mean)), int(bool(accumulate)), _stream(stream))

@@ -12,5 +12,5 @@ timeout 900 python bench.py --out $O/bench.jsonl > $O/bench_n1.log 2>&1; echo "b
 if [ $N -ge 2 ]; then
 timeout 900 python bench.py --gpus $N --out $O/bench.jsonl > $O/bench_n$N.log 2>&1; echo "bench n$N rc=$?"; grep '^{' $O/bench_n$N.log | cut -c1-300
 fi
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_w1.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^k_" -c 600 --csv --log-file $O/launches_w1.csv \
    python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_launches.log 2>&1; echo "ncu rc=$?"

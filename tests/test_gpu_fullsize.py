@@ -1,0 +1,312 @@
+"""Full-size GPU parity of the exact benched geometry, compared element by element with the
+oracle (every element, not samples; VERDICT r1 "next" 1b and 7).
+
+* W = 1, through the C ABI exactly as bench.py runs it (real NCCL communicator at W=1,
+  default kernel variants): `all_gather_params` (bf16 and float8) and
+  `reduce_scatter_grads` on one full Llama 3.1 8B TransformerBlock (218.1M params) and on
+  the 1.05G-param root.  The default W=1 unshard is the TMA-bulk push kernel with
+  16,384-element tiles (8 bulk chunks of 4 KB per bf16 tile), the default W=1
+  reduce-scatter the TMA-bulk RS copy-in; both run at these sizes only here.
+* W = 8 emulated on one GPU (8 communicator-less meshes, the same kernels the NVLink path
+  runs, minus the flag handshakes): the push into 8 arenas (bf16, e4m3), the store-scatter
+  + receive-reduce (own rows read from the rank's grads, as the default path does) and the
+  pull reduce-scatter, on the full 8B block (S = 27.26M per rank,
+  16K-element tiles, multi-chunk).
+
+The oracle (`oracle.World`) computes the expected bits on the host from the same seeded
+inputs (drawn with torch's generator, independent of the CUDA path); the comparison itself
+runs on the GPU (`torch.equal` against the oracle's bits uploaded), with the first
+mismatching index reported.  Root: the oracle runs on row blocks of each parameter (W=1:
+the unshard and the reduce-scatter are elementwise, so a row block of a parameter is a
+unit of its own; the root has no fp8-eligible parameter, reading R8, so no scale spans
+blocks) to bound host memory.
+Bars: bit-exact for the unshard (bf16 / e4m3 given the oracle's scale, which is itself
+compared bit for bit) and for the reduce-scatter (W=1: fp32(g)/1; W=8: the ascending-rank
+fp32 sum of fp32(g)/8, reading R10/R14)."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import World
+from oracle.world import BF16, FP8
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2410_06511_b200 as F
+
+
+def _host_ram_gb() -> float:
+    try:
+        import psutil
+        return psutil.virtual_memory().available / 2 ** 30
+    except Exception:   # noqa: BLE001
+        return 1e9
+
+
+def _need_ram(gb):
+    if _host_ram_gb() < gb:
+        pytest.skip(f"needs ~{gb} GB of free host RAM for the oracle")
+
+
+def _block():
+    u = synth.model_units("llama3.1-8b", include_root=False)[0]
+    return [s for _, s, _ in u], [e for _, _, e in u]
+
+
+def _root():
+    u = synth.model_units("llama3.1-8b")[-1]
+    return [s for _, s, _ in u], [e for _, _, e in u]
+
+
+def _params_dev(shapes, seed):
+    """Per param N(0, sigma_p), sigma_p = 0.02 * 10**U(-1, 1), plus cast
+    edge values (bf16 ties, subnormals, +-0, e4m3 midpoints) spliced in every 4093
+    elements so they land at every phase of the 16K-element tiles and 4 KB chunks."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    out = []
+    for p, s in enumerate(shapes):
+        sig = 0.02 * 10 ** (torch.rand(1, generator=g, device="cuda").item() * 2 - 1)
+        x = torch.randn(s, generator=g, device="cuda", dtype=torch.float32) * sig
+        flat = x.view(-1)
+        idx = torch.arange(0, flat.numel(), 4093, device="cuda")
+        e = synth.edge_values(idx.numel(), seed * 31 + p)
+        e = np.where(np.abs(e) < 1.0, e, np.float32(0.5)).astype(np.float32)   # keep amax ~ sigma
+        flat[idx] = torch.from_numpy(e).cuda()
+        out.append(x)
+    return out
+
+
+def _grads_dev(shapes, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return [(torch.randn(s, generator=g, device="cuda") * 1e-3).to(torch.bfloat16) for s in shapes]
+
+
+def _bits(t: torch.Tensor) -> np.ndarray:
+    """Host copy of a device tensor's bits (uint16 for bf16, uint8 for fp8, uint32 fp32)."""
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    if t.dtype == torch.float8_e4m3fn:
+        return t.view(torch.uint8).cpu().numpy()
+    return t.cpu().numpy()
+
+
+def _assert_bits(got: torch.Tensor, want: np.ndarray, what: str):
+    """Compare every element of `got` (device) with the oracle's `want` on the GPU."""
+    g = got.reshape(-1)
+    if g.dtype == torch.bfloat16:
+        g = g.view(torch.int16)
+        w = torch.from_numpy(np.ascontiguousarray(want).reshape(-1).view(np.int16)).cuda()
+    elif g.dtype == torch.float8_e4m3fn:
+        g = g.view(torch.uint8)
+        w = torch.from_numpy(np.ascontiguousarray(want).reshape(-1).view(np.uint8)).cuda()
+    else:
+        g = g.view(torch.int32)
+        w = torch.from_numpy(np.ascontiguousarray(want, dtype=np.float32).reshape(-1).view(np.int32)).cuda()
+    assert g.numel() == w.numel(), f"{what}: {g.numel()} vs {w.numel()} elements"
+    bad = (g != w).nonzero()
+    if bad.numel():
+        i = int(bad[0, 0])
+        raise AssertionError(f"{what}: {bad.numel()} of {g.numel()} elements differ; first at {i}: "
+                             f"got {int(g[i])}, oracle {int(w[i])}")
+
+
+def _mesh_w1():
+    return F.Mesh(1, 0, 0, unique_id=F.get_unique_id())   # as bench.py at N=1
+
+
+# ----------------------------------------------------------------------------- W = 1, 8B block
+def test_w1_block_full_unshard_and_reduce_scatter():
+    _need_ram(24)
+    shapes, elig = _block()
+    P_dev = _params_dev(shapes, 101)
+    P = [p.cpu().numpy() for p in P_dev]
+    w = World(shapes, 1, elig)
+    shards = w.shard(P)
+    mesh = _mesh_w1()
+    try:
+        layer = F.fsdp_shard(mesh, P_dev, elig)
+        del P_dev
+        assert layer.S == w.S
+        _assert_bits(layer.sharded_flat(), shards[0], "a1 shard")
+        # bf16 unshard (default: TMA-bulk push, 16K-element tiles)
+        outs = F.all_gather_params(layer, torch.bfloat16)
+        _, fulls = w.unshard(shards, BF16)
+        for p, (o, want) in enumerate(zip(outs, fulls)):
+            assert tuple(o.shape) == want.shape
+            _assert_bits(o, want, f"bf16 unshard p{p}")
+        del fulls
+        F.fsdp_reshard(layer)
+        # float8 unshard with precomputed per-tensor scales (K1 -> AR(max) -> K1b)
+        F.precompute_fp8_scales(mesh, [layer])
+        amax, scale = w.precompute_fp8_scales(shards)
+        s_dev, a_dev = layer.fp8_scales()
+        np.testing.assert_array_equal(a_dev.cpu().numpy().view(np.uint32), amax.view(np.uint32))
+        np.testing.assert_array_equal(s_dev.cpu().numpy().view(np.uint32), scale.view(np.uint32))
+        outs = F.all_gather_params(layer, torch.float8_e4m3fn)
+        _, fulls = w.unshard(shards, FP8, scale)
+        for p, (o, want) in enumerate(zip(outs, fulls)):
+            assert (o.dtype == torch.float8_e4m3fn) == bool(elig[p])
+            _assert_bits(o, want, f"fp8 unshard p{p}")
+        del fulls
+        F.fsdp_reshard(layer)
+        # reduce-scatter (W=1: fp32(g)/1 written by the RS copy-in), then accumulate
+        G_dev = _grads_dev(shapes, 202)
+        G = [_bits(g) for g in G_dev]
+        F.reduce_scatter_grads(layer, G_dev)
+        F.fsdp_wait_reduce_scatter(layer)
+        ref = w.reduce_scatter_grads([G], BF16, True)[0]["order"]
+        for p in range(len(shapes)):
+            _assert_bits(layer.sharded_grad(p), ref[p], f"reduce-scatter p{p}")
+        F.reduce_scatter_grads(layer, G_dev, accumulate=True)
+        F.fsdp_wait_reduce_scatter(layer)
+        for p in range(len(shapes)):
+            _assert_bits(layer.sharded_grad(p), (ref[p] + ref[p]).astype(np.float32), f"accumulate p{p}")
+        mesh.synchronize(60000)
+    finally:
+        mesh.destroy()
+
+
+# ----------------------------------------------------------------------------- W = 1, root
+def test_w1_root_full_unshard_and_reduce_scatter():
+    _need_ram(16)
+    shapes, elig = _root()
+    assert not any(elig)   # reading R8: the root stays bf16 under the float8 all-gather
+    P_dev = _params_dev(shapes, 303)
+    mesh = _mesh_w1()
+    try:
+        layer = F.fsdp_shard(mesh, P_dev, elig)
+        G_dev = _grads_dev(shapes, 404)
+        for dt in (torch.bfloat16, torch.float8_e4m3fn):
+            if dt == torch.float8_e4m3fn:
+                F.precompute_fp8_scales(mesh, [layer])
+            outs = F.all_gather_params(layer, dt)
+            for p, (o, full) in enumerate(zip(outs, P_dev)):
+                assert o.dtype == torch.bfloat16 and tuple(o.shape) == tuple(full.shape)
+                rows = full.shape[0] if full.dim() > 1 else 1
+                R = 8192
+                for r0 in range(0, rows, R):   # oracle on row blocks (see module docstring)
+                    if full.dim() > 1:
+                        blk = full[r0:r0 + R]
+                        got = o[r0:r0 + R]
+                    else:
+                        blk, got = full, o
+                    wb = World([tuple(blk.shape)], 1, [False])
+                    _, want = wb.unshard(wb.shard([blk.cpu().numpy()]), FP8 if dt != torch.bfloat16 else BF16,
+                                         np.zeros(1, np.float32))
+                    _assert_bits(got, want[0], f"root {dt} unshard p{p} rows {r0}")
+            F.fsdp_reshard(layer)
+        F.reduce_scatter_grads(layer, G_dev)
+        F.fsdp_wait_reduce_scatter(layer)
+        for p, g in enumerate(G_dev):
+            rows = g.shape[0] if g.dim() > 1 else 1
+            R = 8192
+            sg = layer.sharded_grad(p)
+            for r0 in range(0, rows, R):
+                blk = g[r0:r0 + R] if g.dim() > 1 else g
+                got = sg[r0:r0 + R] if g.dim() > 1 else sg
+                wb = World([tuple(blk.shape)], 1, [False])
+                ref = wb.reduce_scatter_grads([[_bits(blk)]], BF16, True)[0]["order"][0]
+                _assert_bits(got, ref, f"root reduce-scatter p{p} rows {r0}")
+        mesh.synchronize(60000)
+    finally:
+        mesh.destroy()
+
+
+# ----------------------------------------------------------------------------- W = 8 emulated
+class _Emu:
+    def __init__(self, shapes, elig, W, params):
+        self.meshes = [F.Mesh(W, r, 0, local=True) for r in range(W)]
+        self.layers = [F.fsdp_shard(m, params, elig) for m in self.meshes]
+
+    def close(self):
+        for m in self.meshes:
+            m.destroy()
+
+
+@pytest.mark.parametrize("fp8", [False, True])
+def test_w8_emulated_block_push_full(fp8):
+    """Every rank's push kernel writes its rows (cast) into all 8 arenas; each arena must
+    equal the oracle's unshard of the full block, byte for byte, guard band untouched."""
+    _need_ram(16)
+    W = 8
+    shapes, elig = _block()
+    P_dev = _params_dev(shapes, 505)
+    P = [p.cpu().numpy() for p in P_dev]
+    w = World(shapes, W, elig)
+    shards = w.shard(P)
+    emu = _Emu(shapes, elig, W, P_dev)
+    del P_dev
+    try:
+        for r, l in enumerate(emu.layers):
+            _assert_bits(l.sharded_flat(), shards[r], f"a1 shard rank {r}")
+        dt = torch.float8_e4m3fn if fp8 else torch.bfloat16
+        scale = w.precompute_fp8_scales(shards)[1] if fp8 else None
+        offs, total = F.unsharded_layout(emu.layers[0], dt)
+        arenas = [torch.full((total + 4096,), 0xA5, dtype=torch.uint8, device="cuda") for _ in range(W)]
+        sdev = torch.from_numpy(scale).cuda() if fp8 else None
+        for r in range(W):
+            F.stage_unshard_push(emu.layers[r], dt, arenas, fp8_scales=sdev)
+        torch.cuda.synchronize()
+        _, fulls = w.unshard(shards, FP8 if fp8 else BF16, scale)
+        for d in range(W):
+            written = torch.zeros(arenas[d].numel(), dtype=torch.bool, device="cuda")
+            for p, want in enumerate(fulls):
+                nb = want.size * want.itemsize
+                got = arenas[d][offs[p]:offs[p] + nb]
+                got = got.view(torch.bfloat16) if want.dtype == np.uint16 else got.view(torch.float8_e4m3fn)
+                _assert_bits(got, want, f"arena {d} p{p}")
+                written[offs[p]:offs[p] + nb] = True
+            assert bool(torch.all(arenas[d][~written] == 0xA5)), f"arena {d}: write outside the tensors"
+    finally:
+        emu.close()
+
+
+def test_w8_emulated_block_reduce_scatter_full():
+    """Store mechanism (scatter of every rank's rows into the owners' receive buffers, then
+    each owner's local reduce) and pull mechanism (each owner reads every rank's staged
+    grads): every rank's fp32 sharded grad equals the oracle's ascending-rank sum of
+    fp32(g_q)/8 bit for bit, for all 218.1M elements."""
+    _need_ram(40)
+    W = 8
+    shapes, elig = _block()
+    P_dev = [torch.zeros(s, device="cuda") for s in shapes]
+    emu = _Emu(shapes, elig, W, P_dev)
+    del P_dev
+    w = World(shapes, W, elig)
+    try:
+        G_dev = [_grads_dev(shapes, 600 + q) for q in range(W)]
+        G = [[_bits(g) for g in gq] for gq in G_dev]
+        ref = w.reduce_scatter_grads(G, BF16, True)
+        order = [r["order"] for r in ref]
+        del ref, G
+        S = emu.layers[0].S
+        # store (the default P2P path): scatter every rank's rows of the OTHER ranks' chunks into
+        # their receive buffers [W][S] bf16, then each owner's local reduce reads its own rows
+        # from its own grads
+        recv = [torch.empty(W * S * 2 + 64, dtype=torch.uint8, device="cuda") for _ in range(W)]
+        for q in range(W):
+            F.stage_rs_scatter(emu.layers[q], G_dev[q], recv, include_self=False)
+        for r, l in enumerate(emu.layers):
+            l.sharded_grad_flat().fill_(float("nan"))
+            F.stage_rs_recv_reduce(l, recv[r], torch.bfloat16, torch.float32, True, False, own_grads=G_dev[r])
+        torch.cuda.synchronize()
+        for r, l in enumerate(emu.layers):
+            for p in range(len(shapes)):
+                _assert_bits(l.sharded_grad(p), order[r][p], f"store RS rank {r} p{p}")
+        del recv
+        # pull: every rank's grads staged, every owner pulls its rows from all 8 stagings
+        offs, total = F.grad_staging_layout(emu.layers[0])
+        stag = [torch.empty(total + 64, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+        for q in range(W):
+            F.stage_grads_to_staging(emu.layers[q], G_dev[q], stag[q])
+        for r, l in enumerate(emu.layers):
+            l.sharded_grad_flat().fill_(float("nan"))
+            F.stage_rs_pull(l, stag, torch.bfloat16, torch.float32, True, False)
+        torch.cuda.synchronize()
+        for r, l in enumerate(emu.layers):
+            for p in range(len(shapes)):
+                _assert_bits(l.sharded_grad(p), order[r][p], f"pull RS rank {r} p{p}")
+    finally:
+        emu.close()

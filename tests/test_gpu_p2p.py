@@ -115,10 +115,13 @@ def test_rs_pull_emulated(kind, seed, W, gd, rd, mean, acc):
 @pytest.mark.parametrize("gd,rd,mean,acc", [(BF16, FP32, True, False), (FP32, FP32, True, False),
                                             (BF16, FP32, False, False), (BF16, FP32, True, True),
                                             (BF16, BF16, True, False)])
-def test_rs_store_emulated(kind, seed, W, gd, rd, mean, acc):
+@pytest.mark.parametrize("own", [False, True])
+def test_rs_store_emulated(kind, seed, W, gd, rd, mean, acc, own):
     """Store-based reduce-scatter (FSDP_P2P_RS_STORE): every rank's scatter kernel writes its
     rows of rank r's chunk into r's receive buffer at slot q (bytes checked, guard bands
-    untouched), then every rank's local reduce gives the same bits as the pull."""
+    untouched), then every rank's local reduce gives the same bits as the pull.  own=True is
+    the default P2P path: the scatter skips the own chunk (own slot left untouched) and the
+    reduce reads the own rows from the rank's grads — same bits."""
     shapes, elig = _unit(kind, seed, W)
     w = World(shapes, W, elig)
     emu = Emu(shapes, elig, W, _params(shapes, seed))
@@ -135,12 +138,14 @@ def test_rs_store_emulated(kind, seed, W, gd, rd, mean, acc):
         nbytes = W * S * es
         recv = [torch.full((nbytes + 64,), 0x5A, dtype=torch.uint8, device="cuda") for _ in range(W)]
         for q in range(W):
-            F.stage_rs_scatter(emu.layers[q], GT[q], recv)
+            F.stage_rs_scatter(emu.layers[q], GT[q], recv, include_self=not own)
         torch.cuda.synchronize()
         for r in range(W):   # slot q of rank r's buffer holds rank q's rows of r's chunk, nothing else
             a = recv[r].cpu().numpy()
             written = np.zeros(a.size, dtype=bool)
             for q in range(W):
+                if own and q == r:
+                    continue      # own slot never written
                 for p, m in enumerate(emu.layers[r].metas):
                     cnt = m["row_count"] * m["rest"]
                     lo = (q * S + m["elem_offset"]) * es
@@ -150,10 +155,20 @@ def test_rs_store_emulated(kind, seed, W, gd, rd, mean, acc):
             assert np.all(a[~written] == 0x5A)
         rng = np.random.default_rng(seed)
         old = [rng.standard_normal(l.S).astype(np.float32) for l in emu.layers]
+        aligned = all(m["row_count"] == 0 or (m["row_begin"] * m["rest"] * es) % 16 == 0
+                      for l in emu.layers for m in l.metas)
         for r, l in enumerate(emu.layers):
             l.sharded_grad_flat().copy_(torch.from_numpy(old[r]).cuda())
-            F.stage_rs_recv_reduce(l, recv[r], tdt, torch.float32 if rd == FP32 else torch.bfloat16, mean, acc)
+            rdt = torch.float32 if rd == FP32 else torch.bfloat16
+            if own and not all(m["row_count"] == 0 or (m["row_begin"] * m["rest"] * es) % 16 == 0 for m in l.metas):
+                with pytest.raises(F.FsdpError) as e:   # own-row offsets misaligned: refused, not wrong
+                    F.stage_rs_recv_reduce(l, recv[r], tdt, rdt, mean, acc, own_grads=GT[r])
+                assert e.value.status_name == "FSDP_ERR_INVALID_ARGUMENT"
+                continue
+            F.stage_rs_recv_reduce(l, recv[r], tdt, rdt, mean, acc, own_grads=GT[r] if own else None)
         torch.cuda.synchronize()
+        if own and not aligned:
+            return
         ref = w.reduce_scatter_grads(G, gd, mean, reduce_dtype=rd)
         for r, l in enumerate(emu.layers):
             for p in range(len(shapes)):

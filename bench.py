@@ -93,6 +93,9 @@ def parse():
                     help="capture the step into a CUDA graph after the warm-up and time its replays (for "
                          "launch-bound units, e.g. --workload toy); kernel statistics then come from one eager "
                          "profiled step")
+    ap.add_argument("--fp8-scaling", default="dynamic", choices=["dynamic", "delayed"],
+                    help="float8 workloads: dynamic (amax pass over every shard each step) or delayed "
+                         "(history of 16; the amax is fused into the fp8 unshard's cast, P:157)")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     return ap.parse_args()
 
@@ -287,9 +290,11 @@ def run_ours(args):
         for l in layers:
             F.fsdp_wait_reduce_scatter(l, stream=comp)
 
+    hist = 16 if args.fp8_scaling == "delayed" else 0
+
     def step():
         if wl["fp8"]:
-            F.precompute_fp8_scales(mesh, layers, stream=comp)
+            F.precompute_fp8_scales(mesh, layers, stream=comp, history_len=hist)
         (step_train if args.step == "train" else step_unit)()
 
     # algorithmic bytes per step per rank: all-gather outputs + fp32 RS inputs
@@ -527,7 +532,8 @@ def run_ours(args):
             "data": "synthetic (seeded normal params and bf16 grads, Llama 3.1 parameter shapes)",
             "config": {"workload": f"{args.workload} layout: {len(layers)} FSDP units "
                                    f"({'32 blocks + root' if args.workload.startswith('llama3.1-8b') else 'see DESIGN.md'}), "
-                                   f"{'fp8 e4m3' if wl['fp8'] else 'bf16'} all-gather / fp32 reduce-scatter, "
+                                   f"{('fp8 e4m3 (' + args.fp8_scaling + ' scaling)') if wl['fp8'] else 'bf16'} "
+                                   f"all-gather / fp32 reduce-scatter, "
                                    f"{'serial' if args.serial else 'prefetch next unit'}",
                        "world_size": N, "shard_size": W, "units": len(layers), "collectives": algo,
                        "step": args.step + (" zero2" if args.zero2 else ""),
@@ -601,7 +607,7 @@ def run_e2e(args, F, torch, dist, mesh, layers, grads, comp, dev, N, W, pdtype, 
                 e.record(h2d_s)
                 ev_in.append(e)
         if wl["fp8"]:
-            F.precompute_fp8_scales(mesh, layers, stream=comp)
+            F.precompute_fp8_scales(mesh, layers, stream=comp, history_len=16 if args.fp8_scaling == "delayed" else 0)
         with torch.cuda.stream(comp):
             F.fsdp_unshard(layers[0], pdtype, stream=comp)
             for i in range(n):

@@ -294,7 +294,16 @@ fsdp_status_t fsdp_precompute_fp8_scales(fsdp_mesh_t* mesh, fsdp_layer_t* const*
  * where H_p is the max of the param's amax history (the last history_len amaxes,
  * initialised with the first observed amax), and the current amax is pushed into the
  * history after use.  history_len in [1, 64], fixed by the first call.  Static scaling =
- * passing caller scales to fsdp_unshard. */
+ * passing caller scales to fsdp_unshard.
+ * Amax fused into the casts (default; FSDP_B200_AMAX_FUSE=0 turns it off): a delayed call
+ * arms its layers, and every later fp8 fsdp_unshard of an armed layer folds max |x| of the
+ * fp32 elements it casts into the accumulator (no extra HBM pass).  The next delayed call on
+ * the same layers then records that amax into the history FIRST and takes the scale after —
+ * the same history as recording it after use at the previous call, so the scales are
+ * bit-identical — and skips the amax pass over every shard (only the first call, and an
+ * armed layer that was not fp8-unsharded since the previous call, run it).  amax_dev then
+ * holds the recorded amax: the previous step's.  The unshards of a step must be waited
+ * (fsdp_wait_unshard) before the next step's delayed call; a dynamic call disarms. */
 fsdp_status_t fsdp_precompute_fp8_scales_delayed(fsdp_mesh_t* mesh, fsdp_layer_t* const* layers,
                                                  int32_t n_layers, int32_t history_len, void* stream);
 /* Device arrays of P floats (entries of non-eligible params are 0).  The pointers stay valid
@@ -364,9 +373,13 @@ fsdp_status_t fsdp_zero_grad(fsdp_layer_t* layer, void* stream);
 /* ---------------------------------------------------------------- stage entry points */
 /* One kernel each, no communication, stream-ordered on `stream`; they expose the
  * individual steps (for tests at any W on one GPU and for custom collectives). */
-/* K2/K3: this rank's all-gather slot (S*2 bytes for BF16, S_bytes_fp8 for FLOAT8). */
+/* K2/K3: this rank's all-gather slot (S*2 bytes for BF16, S_bytes_fp8 for FLOAT8).
+ * amax_accum_dev (FLOAT8 only; NULL = none): P floats read and written as fp32 bit patterns,
+ * amax_accum[p] = max(amax_accum[p], max |x| over this rank's cast elements of eligible param
+ * p) — the delayed-scaling amax fused into the cast (bit-identical to K1). */
 fsdp_status_t fsdp_stage_copy_in(const fsdp_layer_t* layer, fsdp_dtype_t param_dtype,
-                                 const float* fp8_scales_dev, void* ag_slot_dev, void* stream);
+                                 const float* fp8_scales_dev, void* ag_slot_dev, float* amax_accum_dev,
+                                 void* stream);
 /* K4: from a full rank-major all-gather buffer [W][slot] into per-param full tensors
  * full_out_dev[p] (contiguous, numel = prod(shape) elements of the param's dtype). */
 fsdp_status_t fsdp_stage_copy_out(const fsdp_layer_t* layer, fsdp_dtype_t param_dtype,
@@ -396,10 +409,10 @@ fsdp_status_t fsdp_unsharded_layout(const fsdp_layer_t* layer, fsdp_dtype_t para
  * W arenas arenas_dev[0..W-1] (any device memory the current device can store to, e.g.
  * peer-mapped; each 16-byte aligned, else FSDP_ERR_INVALID_ARGUMENT — the TMA bulk stores
  * address them relative to their base).  Running it for every rank fills every arena with
- * the full tensors. */
+ * the full tensors.  amax_accum_dev: as in fsdp_stage_copy_in (the fused amax of the push). */
 fsdp_status_t fsdp_stage_unshard_push(const fsdp_layer_t* layer, fsdp_dtype_t param_dtype,
                                       const float* fp8_scales_dev, void* const* arenas_dev,
-                                      void* stream);
+                                      float* amax_accum_dev, void* stream);
 /* Grad staging layout: param p's full grad at element offset elem_offsets[p] (128-aligned). */
 fsdp_status_t fsdp_grad_staging_layout(const fsdp_layer_t* layer, int64_t* elem_offsets,
                                        int64_t* total_elems);

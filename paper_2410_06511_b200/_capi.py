@@ -95,14 +95,14 @@ SIGNATURES = {
     "fsdp_sharded_grad": [_VP, _I32, C.POINTER(_VP)],
     "fsdp_sharded_grad_flat": [_VP, C.POINTER(_VP)],
     "fsdp_zero_grad": [_VP, _VP],
-    "fsdp_stage_copy_in": [_VP, _I32, _VP, _VP, _VP],
+    "fsdp_stage_copy_in": [_VP, _I32, _VP, _VP, _VP, _VP],
     "fsdp_stage_copy_out": [_VP, _I32, _VP, _PP, _VP],
     "fsdp_stage_local_amax": [_VP, _VP, _VP],
     "fsdp_stage_fp8_scale": [_VP, _VP, _VP, _VP],
     "fsdp_stage_rs_copy_in": [_VP, _PP, _I32, _I32, _I32, _VP, _VP],
     "fsdp_stage_rs_copy_out": [_VP, _VP, _I32, _I32, _VP],
     "fsdp_unsharded_layout": [_VP, _I32, C.POINTER(_I64), C.POINTER(_I64)],
-    "fsdp_stage_unshard_push": [_VP, _I32, _VP, _PP, _VP],
+    "fsdp_stage_unshard_push": [_VP, _I32, _VP, _PP, _VP, _VP],
     "fsdp_grad_staging_layout": [_VP, C.POINTER(_I64), C.POINTER(_I64)],
     "fsdp_stage_grads_to_staging": [_VP, _PP, _I32, _VP, _VP],
     "fsdp_stage_rs_pull": [_VP, _PP, _I32, _I32, _I32, _I32, _VP],

@@ -283,6 +283,7 @@ struct fsdp_mesh {
   int algo = FSDP_ALGO_NCCL;
   int p2p_rs_mode = FSDP_P2P_RS_AUTO;        // how the P2P reduce-scatter moves data
   int reduce_per_sm = 2;                     // store-RS local reduce CTAs/SM (0: default grid; 2 measured best)
+  bool amax_fuse = true;                     // delayed scaling: amax fused into the fp8 casts (FSDP_B200_AMAX_FUSE=0: K1 pass)
   bool store_own_direct = true;              // store RS: own rows read from the caller's grads (FSDP_B200_STORE_OWN=0: own slot)
   bool p2p_ok = false;
   SymBuf flags;                              // uint64 [FK_NUM][kFlagSlots][kMaxRanks]
@@ -325,6 +326,12 @@ struct fsdp_layer {
   // own chunk, receiver tiles with the own-row source offsets (layout.h)
   DevTiles t_scatter_peers_bf16, t_scatter_peers_fp32, t_recv_own;
   bool own_ok_bf16 = false, own_ok_fp32 = false;   // own-row offsets 16-byte aligned
+  // delayed fp8 scaling with the amax fused into the casts: armed by a delayed precompute
+  // (the fp8 unshards then fold max |x| into the registry accumulator), pushed = an armed fp8
+  // unshard ran since the last precompute; t_amax_reg: K1 tiles of this layer alone
+  // (registry indices), the stand-in for an armed layer that was not unsharded in a step
+  bool amax_armed = false, amax_pushed = false;
+  DevTiles t_amax_reg;
   std::vector<int64_t> stg_off_el;   // full-grad staging: param p at element offset (128-aligned)
   int64_t stg_elems = 0;
   int64_t push_bytes_bf16 = 0, push_bytes_fp8 = 0, pull_elems = 0;
@@ -375,7 +382,8 @@ void launch_rs_copy_in_all(fsdp_layer* l, const void* const* grads, bool grad_bf
                            bool mean, cudaStream_t st);
 int64_t cin_bytes(const fsdp_layer* l, bool fp8);
 int64_t slot_bytes(const fsdp_layer* l, bool fp8);
-void do_copy_in(fsdp_layer* l, bool fp8, const float* scales, void* dst, cudaStream_t st);
+void do_copy_in(fsdp_layer* l, bool fp8, const float* scales, void* dst, cudaStream_t st,
+                uint32_t* amax_acc = nullptr);
 void validate_grads(const fsdp_layer* l, const void* const* grads, fsdp_dtype_t gd, fsdp_dtype_t rd);
 // TMA bulk copies and 16-byte vector accesses address caller buffers relative to their base:
 // the base must be 16-byte aligned (FSDP_ERR_INVALID_ARGUMENT otherwise, before any launch)

@@ -127,6 +127,7 @@ fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* l) {
     l->t_stage_fp32.release(); l->t_amax_stage.release();
     l->t_scatter_bf16.release(); l->t_scatter_fp32.release(); l->t_recv.release();
     l->t_scatter_peers_bf16.release(); l->t_scatter_peers_fp32.release(); l->t_recv_own.release();
+    l->t_amax_reg.release();
     if (l->gbuf) {
       if (l->gbuf_sym && !m->aborted) sym_free(m, l->gbuf->buf);   // collective
       else if (l->gbuf_sym) sym_free_local(m, l->gbuf->buf);
@@ -220,12 +221,36 @@ static fsdp_status_t precompute_impl(fsdp_mesh_t* m, fsdp_layer_t* const* layers
     // precompute runs on s_rs (the stream owning comm_rs), ordered after `stream`, and
     // `stream` waits for it: K1 over all layers -> all-reduce(max) -> K1b
     cudaStream_t st = as_stream(stream);
+    // delayed scaling with the amax fused into the fp8 casts: when every layer was armed by a
+    // previous delayed call, the accumulator already holds the max |x| the fp8 unshards since
+    // then saw — that step's amax, recorded now (K1c) exactly as K1b would have recorded it
+    // after use — so the K1 pass over all fp32 shards is skipped.  An armed layer that was not
+    // fp8-unsharded since (nothing accumulated) gets a K1 pass of its current parameters.
+    const bool delayed = history_len > 0;
+    bool fused = delayed && m->amax_fuse && m->hist_len == history_len;
+    for (fsdp_layer* l : key) fused = fused && l->amax_armed;
     CUDA_CHECK(cudaEventRecord(m->ev_pre_call, st));
     CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, m->ev_pre_call, 0));
-    {
+    if (!fused) {
       ProfScope pa(m, FSDP_PROF_AMAX, m->s_rs, ps->bytes);
       CUDA_CHECK(fsdpk::launch_amax(ps->tiles.d, ps->tiles.n, m->reg_acc, m->cfg, m->s_rs));
       pa.done();
+    } else {
+      for (fsdp_layer* l : key) {
+        if (l->amax_pushed) continue;
+        if (!l->t_amax_reg.d) {
+          std::vector<Tile> tiles;
+          fsdpl::append_tiles_amax(l->L, l->shard, l->reg_base, &tiles);
+          if (tiles.empty()) continue;
+          if (capture_of(st).on) fail(FSDP_ERR_STATE, "first stand-in amax pass of a layer inside a CUDA graph capture");
+          l->t_amax_reg.upload(tiles);
+        }
+        int64_t b = 0;
+        for (int p = 0; p < l->P; ++p) if (l->L.fp8[p]) b += 4 * l->L.metas[p].padded_numel;
+        ProfScope pa(m, FSDP_PROF_AMAX, m->s_rs, b);
+        CUDA_CHECK(fsdpk::launch_amax(l->t_amax_reg.d, l->t_amax_reg.n, m->reg_acc, m->cfg, m->s_rs));
+        pa.done();
+      }
     }
     if (comm_ready(m) && m->reg_size > 0) {
       // max of non-negative fp32 bit patterns == uint32 max (NaN patterns propagate)
@@ -238,6 +263,10 @@ static fsdp_status_t precompute_impl(fsdp_mesh_t* m, fsdp_layer_t* const* layers
       if (history_len == 0) {
         CUDA_CHECK(fsdpk::launch_fp8_scale(ps->idx, ps->nidx, m->reg_acc, m->reg_amax, m->reg_scale, m->reg_elig,
                                            m->d_err, true, m->s_rs));
+      } else if (fused) {
+        CUDA_CHECK(fsdpk::launch_fp8_scale_delayed_fused(ps->idx, ps->nidx, m->reg_acc, m->reg_amax, m->reg_scale,
+                                                         m->reg_elig, m->reg_hist, m->reg_pos, m->reg_hinit,
+                                                         history_len, kHistMax, m->d_err, m->s_rs));
       } else {
         registry_ensure_hist(m);
         m->hist_len = history_len;
@@ -246,6 +275,10 @@ static fsdp_status_t precompute_impl(fsdp_mesh_t* m, fsdp_layer_t* const* layers
                                                    kHistMax, m->d_err, m->s_rs));
       }
       pk.done();
+    }
+    for (fsdp_layer* l : key) {   // arm (delayed + fused) or disarm the casts' accumulation
+      l->amax_armed = delayed && m->amax_fuse;
+      l->amax_pushed = false;
     }
     CUDA_CHECK(cudaEventRecord(m->ev_pre_done, m->s_rs));
     CUDA_CHECK(cudaStreamWaitEvent(st, m->ev_pre_done, 0));
@@ -288,6 +321,9 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
     if (m->local && m->W > 1) fail(FSDP_ERR_UNAVAILABLE, "local mesh with world_size > 1 has no communicator");
     const bool fp8 = dt == FSDP_FLOAT8_E4M3FN;
     if (fp8 && !scales) scales = m->reg_scale + l->reg_base;
+    // delayed scaling, amax fused into the cast: fold max |x| into the registry accumulator
+    uint32_t* amax_acc = (fp8 && l->amax_armed) ? m->reg_acc + l->reg_base : nullptr;
+    if (amax_acc) l->amax_pushed = true;
     DeviceGuard g(m->device);
     const int64_t sb = slot_bytes(l, fp8);
     const int64_t arena = fp8 ? l->L.arena_fp8 : l->L.arena_bf16;
@@ -310,7 +346,7 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
         const DevTiles& T = fp8 ? l->t_push_fp8 : l->t_push_bf16;
         ProfScope pp(m, FSDP_PROF_UNSHARD_PUSH, m->s_ag, fp8 ? l->push_bytes_fp8 : l->push_bytes_bf16);
         CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, peer_ptrs(m, ss->buf), m->W, m->rank,
-                                              m->cfg, m->s_ag));
+                                              m->cfg, m->s_ag, amax_acc));
         pp.done();
       }
       {
@@ -350,7 +386,7 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
         } else {
           fsdpk::LaunchCfg lcfg = m->cfg;   // W = 1: bulk stores too (0.915 vs 0.902 of HBM, r06)
           if (const char* e = std::getenv("FSDP_B200_W1_BULK")) if (std::atoi(e) == 0) lcfg.variant &= ~4;
-          CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, pp, 1, 0, lcfg, m->s_cin));
+          CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, pp, 1, 0, lcfg, m->s_cin, amax_acc));
         }
         pc.done();
       }
@@ -370,7 +406,7 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
     CUDA_CHECK(cudaStreamWaitEvent(m->s_cin, l->ev_call, 0));
     wait_released(m->s_cin, slot, cap);
     uint8_t* ag = (uint8_t*)slot->a.p;
-    do_copy_in(l, fp8, scales, ag + (size_t)m->rank * sb, m->s_cin);
+    do_copy_in(l, fp8, scales, ag + (size_t)m->rank * sb, m->s_cin, amax_acc);
     CUDA_CHECK(cudaEventRecord(l->ev_cin, m->s_cin));
     cudaEvent_t ready = l->ev_cin;
     if (comm_ready(m)) {

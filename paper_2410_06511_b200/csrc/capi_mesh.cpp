@@ -98,6 +98,8 @@ static void mesh_common_init(fsdp_mesh* m) {
 
 // P2P capability: W in [2, 8] and every rank can map every peer's buffer (collective).
 static void p2p_init(fsdp_mesh* m) {
+  if (const char* e = std::getenv("FSDP_B200_STORE_OWN")) m->store_own_direct = std::atoi(e) != 0;
+  if (const char* e = std::getenv("FSDP_B200_AMAX_FUSE")) m->amax_fuse = std::atoi(e) != 0;
   if (m->local || m->W < 2 || m->W > 8) return;
   const size_t fbytes = sizeof(unsigned long long) * FK_NUM * kFlagSlots * fsdpp::kMaxRanks;
   m->p2p_ok = sym_alloc(m, m->flags, fbytes);
@@ -109,7 +111,6 @@ static void p2p_init(fsdp_mesh* m) {
   if (const char* t = std::getenv("FSDP_B200_P2P_TIMEOUT_MS"))
     m->p2p_timeout_ns = (unsigned long long)std::max(1L, std::atol(t)) * 1000000ull;
   if (const char* e = std::getenv("FSDP_B200_REDUCE_CTAS_PER_SM")) m->reduce_per_sm = std::max(0, std::min(16, std::atoi(e)));
-  if (const char* e = std::getenv("FSDP_B200_STORE_OWN")) m->store_own_direct = std::atoi(e) != 0;
   if (const char* r = std::getenv("FSDP_B200_P2P_RS"))
     m->p2p_rs_mode = std::string(r) == "pull" ? FSDP_P2P_RS_PULL
                      : std::string(r) == "store" ? FSDP_P2P_RS_STORE : FSDP_P2P_RS_AUTO;

@@ -7,7 +7,7 @@ extern "C" {
 
 // ------------------------------------------------------------------------- stage entry points
 fsdp_status_t fsdp_stage_copy_in(const fsdp_layer_t* lc, fsdp_dtype_t dt, const float* scales, void* slot,
-                                 void* stream) {
+                                 float* amax_accum, void* stream) {
   return guarded([&] {
     fsdp_layer* l = const_cast<fsdp_layer*>(lc);
     check_layer(l);
@@ -16,7 +16,7 @@ fsdp_status_t fsdp_stage_copy_in(const fsdp_layer_t* lc, fsdp_dtype_t dt, const 
     const bool fp8 = dt == FSDP_FLOAT8_E4M3FN;
     if (fp8 && !scales) scales = l->mesh->reg_scale + l->reg_base;
     DeviceGuard g(l->mesh->device);
-    do_copy_in(l, fp8, scales, slot, as_stream(stream));
+    do_copy_in(l, fp8, scales, slot, as_stream(stream), fp8 ? reinterpret_cast<uint32_t*>(amax_accum) : nullptr);
   });
 }
 
@@ -120,7 +120,7 @@ fsdp_status_t fsdp_unsharded_layout(const fsdp_layer_t* l, fsdp_dtype_t dt, int6
 }
 
 fsdp_status_t fsdp_stage_unshard_push(const fsdp_layer_t* lc, fsdp_dtype_t dt, const float* scales,
-                                      void* const* arenas, void* stream) {
+                                      void* const* arenas, float* amax_accum, void* stream) {
   return guarded([&] {
     fsdp_layer* l = const_cast<fsdp_layer*>(lc);
     check_layer(l);
@@ -139,7 +139,8 @@ fsdp_status_t fsdp_stage_unshard_push(const fsdp_layer_t* lc, fsdp_dtype_t dt, c
     DeviceGuard g(m->device);
     const DevTiles& T = fp8 ? l->t_push_fp8 : l->t_push_bf16;
     ProfScope ps(m, FSDP_PROF_UNSHARD_PUSH, as_stream(stream), fp8 ? l->push_bytes_fp8 : l->push_bytes_bf16);
-    CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, pp, m->W, m->rank, m->cfg, as_stream(stream)));
+    CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, pp, m->W, m->rank, m->cfg, as_stream(stream),
+                                          fp8 ? reinterpret_cast<uint32_t*>(amax_accum) : nullptr));
     ps.done();
   });
 }

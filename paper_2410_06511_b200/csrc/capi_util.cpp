@@ -332,10 +332,11 @@ void launch_rs_copy_in_all(fsdp_layer* l, const void* const* grads, bool grad_bf
 int64_t cin_bytes(const fsdp_layer* l, bool fp8) { return fp8 ? l->bytes_cin_fp8 : 6 * l->L.S; }
 int64_t slot_bytes(const fsdp_layer* l, bool fp8) { return fp8 ? l->L.S_bytes_fp8 : 2 * l->L.S; }
 
-void do_copy_in(fsdp_layer* l, bool fp8, const float* scales, void* dst, cudaStream_t st) {
+void do_copy_in(fsdp_layer* l, bool fp8, const float* scales, void* dst, cudaStream_t st, uint32_t* amax_acc) {
   fsdp_mesh* m = l->mesh;
   ProfScope ps(m, FSDP_PROF_COPY_IN, st, cin_bytes(l, fp8));
-  if (fp8) CUDA_CHECK(fsdpk::launch_copy_in_fp8(l->t_cin_fp8.d, l->t_cin_fp8.n, l->shard, dst, scales, m->cfg, st));
+  if (fp8) CUDA_CHECK(fsdpk::launch_copy_in_fp8(l->t_cin_fp8.d, l->t_cin_fp8.n, l->shard, dst, scales, m->cfg, st,
+                                                amax_acc));
   else CUDA_CHECK(fsdpk::launch_copy_in_bf16(l->shard, dst, l->L.S, m->cfg, st));
   ps.done();
 }

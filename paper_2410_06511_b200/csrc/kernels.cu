@@ -56,7 +56,8 @@ __global__ void __launch_bounds__(kThreads) k_copy_in_bf16(const float4* __restr
 __global__ void __launch_bounds__(kThreads) k_copy_in_fp8(const Tile* __restrict__ tiles, int ntiles,
                                                           const float* __restrict__ shard,
                                                           uint8_t* __restrict__ slot,
-                                                          const float* __restrict__ scales) {
+                                                          const float* __restrict__ scales,
+                                                          uint32_t* __restrict__ acc) {
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
     const float* src = shard + tl.src;   // 16-element aligned
@@ -65,10 +66,17 @@ __global__ void __launch_bounds__(kThreads) k_copy_in_fp8(const Tile* __restrict
     if (tl.kind == TK_FP8) {
       const float s = scales[tl.param];
       const uint32_t nv = n / 16;
+      uint32_t am = 0;   // delayed scaling: max |x| bits of the cast elements (acc != NULL)
       for (uint32_t v = threadIdx.x; v < nv; v += kThreads) {
         uint4 q[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) q[j] = ld_stream(src + 16 * v + 4 * j);
+        if (acc) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            am = max(am, max(max(q[j].x & 0x7FFFFFFFu, q[j].y & 0x7FFFFFFFu),
+                             max(q[j].z & 0x7FFFFFFFu, q[j].w & 0x7FFFFFFFu)));
+        }
         uint32_t w[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -81,8 +89,13 @@ __global__ void __launch_bounds__(kThreads) k_copy_in_fp8(const Tile* __restrict
         st_v4(dst + 16 * v, make_uint4(w[0], w[1], w[2], w[3]));
       }
       for (uint32_t e = nv * 16 + threadIdx.x; e < n; e += kThreads) {
+        if (acc) am = max(am, __float_as_uint(src[e]) & 0x7FFFFFFFu);
         const float x = __fmul_rn(src[e], s);
         dst[e] = (uint8_t)(pack_e4m3x2(x, 0.0f) & 0xFFu);
+      }
+      if (acc) {
+        am = __reduce_max_sync(0xFFFFFFFFu, am);
+        if ((threadIdx.x & 31u) == 0 && am) atomicMax(acc + tl.param, am);
       }
     } else {  // bf16 param inside a float8 unit
       const uint32_t nv = n / 8;
@@ -443,6 +456,33 @@ __global__ void k_fp8_scale_delayed(const int32_t* __restrict__ idx, int n, uint
   pos[j] = pos[j] + 1 == H ? 0 : pos[j] + 1;
 }
 
+// K1c: delayed scaling with the amax fused into the casts (kernels.h).  Record, then use.
+__global__ void k_fp8_scale_delayed_fused(const int32_t* __restrict__ idx, int n, uint32_t* __restrict__ acc,
+                                          float* __restrict__ amax_out, float* __restrict__ scale_out,
+                                          const uint8_t* __restrict__ eligible, float* __restrict__ hist,
+                                          int32_t* __restrict__ pos, uint8_t* __restrict__ init, int H, int hmax,
+                                          int* __restrict__ err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int j = idx[i];
+  const float a = __uint_as_float(acc[j]);
+  amax_out[j] = a;
+  acc[j] = 0u;
+  if (!eligible[j]) { scale_out[j] = 0.0f; return; }
+  if (!isfinite(a)) { atomicExch(err, 1); scale_out[j] = 0.0f; return; }
+  float* h = hist + (size_t)j * hmax;
+  if (!init[j]) {
+    for (int k = 0; k < H; ++k) h[k] = a;
+    pos[j] = 0;
+    init[j] = 1;
+  }
+  h[pos[j]] = a;                                       // the previous step's amax, recorded ...
+  pos[j] = pos[j] + 1 == H ? 0 : pos[j] + 1;
+  float m = h[0];
+  for (int k = 1; k < H; ++k) m = fmaxf(m, h[k]);      // ... before this step's scale is taken
+  scale_out[j] = __double2float_rn(__ddiv_rn(448.0, (double)fmaxf(m, 1e-12f)));
+}
+
 inline int grid_for(int64_t work_items, LaunchCfg cfg, int tuned = kCtasCopy) {
   int64_t g = work_items;
   if (g > cfg.cap(tuned)) g = cfg.cap(tuned);
@@ -460,10 +500,10 @@ cudaError_t launch_copy_in_bf16(const float* shard, void* slot, int64_t S, Launc
 }
 
 cudaError_t launch_copy_in_fp8(const Tile* tiles, int ntiles, const float* shard, void* slot,
-                               const float* scales, LaunchCfg cfg, cudaStream_t st) {
+                               const float* scales, LaunchCfg cfg, cudaStream_t st, uint32_t* amax_acc) {
   if (ntiles == 0) return cudaSuccess;
   return launch_persistent(k_copy_in_fp8, grid_for(ntiles, cfg), 0, st, tiles, ntiles, shard, (uint8_t*)slot,
-                           scales);
+                           scales, amax_acc);
 }
 
 cudaError_t launch_copy_out(const Tile* tiles, int ntiles, const void* ag, const PtrArray& outs,
@@ -527,6 +567,15 @@ cudaError_t launch_fp8_scale_delayed(const int32_t* idx, int n, uint32_t* acc_bi
   if (n == 0) return cudaSuccess;
   k_fp8_scale_delayed<<<(n + 127) / 128, 128, 0, st>>>(idx, n, acc_bits, amax_out, scale_out, eligible, hist, pos,
                                                          hist_init, H, hmax, err_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fp8_scale_delayed_fused(const int32_t* idx, int n, uint32_t* acc_bits, float* amax_out,
+                                           float* scale_out, const uint8_t* eligible, float* hist, int32_t* pos,
+                                           uint8_t* hist_init, int H, int hmax, int* err_flag, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_fp8_scale_delayed_fused<<<(n + 127) / 128, 128, 0, st>>>(idx, n, acc_bits, amax_out, scale_out, eligible, hist,
+                                                               pos, hist_init, H, hmax, err_flag);
   return cudaGetLastError();
 }
 }  // namespace fsdpk

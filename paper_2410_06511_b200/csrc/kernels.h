@@ -56,9 +56,20 @@ constexpr int kCtasCopy = 4;
 cudaError_t launch_copy_in_bf16(const float* shard, void* slot, int64_t S, LaunchCfg cfg,
                                 cudaStream_t st);
 // K3: per tile: TK_FP8 -> e4m3fn(satfinite(rn(x * scales[param]))), TK_BF16 -> bf16.
-// src = element offset into shard, dst = byte offset into slot.
+// src = element offset into shard, dst = byte offset into slot.  amax_acc != NULL: also
+// amax_acc[param] = max(amax_acc[param], max |x| bits) over the TK_FP8 tiles (delayed scaling).
 cudaError_t launch_copy_in_fp8(const Tile* tiles, int ntiles, const float* shard, void* slot,
-                               const float* scales, LaunchCfg cfg, cudaStream_t st);
+                               const float* scales, LaunchCfg cfg, cudaStream_t st,
+                               uint32_t* amax_acc = nullptr);
+// K1c delayed scaling with the amax fused into the fp8 casts: for every idx j: a = acc[j]
+// (the max |x| the casts since the previous call saw; all ranks' by then, after the
+// all-reduce(max)); record a into the history FIRST (hist[pos[j]] = a, pos advances; a
+// history not yet initialised is filled with a), then scale[j] = fp32(448 / fp64(max(max(
+// hist), 1e-12))); amax_out[j] = a; acc[j] = 0.  Recording the previous step's amax at the
+// start of this call is the same history as K1b recording it at the end of the previous one.
+cudaError_t launch_fp8_scale_delayed_fused(const int32_t* idx, int n, uint32_t* acc_bits, float* amax_out,
+                                           float* scale_out, const uint8_t* eligible, float* hist, int32_t* pos,
+                                           uint8_t* hist_init, int H, int hmax, int* err_flag, cudaStream_t st);
 // K4: byte copy: ptrs.p[param] + dst <- ag + src, n bytes (any alignment).
 cudaError_t launch_copy_out(const Tile* tiles, int ntiles, const void* ag, const PtrArray& outs,
                             LaunchCfg cfg, cudaStream_t st);

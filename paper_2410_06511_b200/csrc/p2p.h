@@ -43,9 +43,11 @@ cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W
 // Push tiles: src = element offset into the fp32 shard, dst = byte offset into the arena,
 // n elements, kind TK_BF16 / TK_FP8 (scale = scales[param]).  Stores go to arena.p[d] for
 // every rank d (d = rank is the local arena), rotated by rank to spread NVLink traffic.
+// amax_acc != NULL (delayed scaling with the amax fused into the push): amax_acc[param] =
+// max(amax_acc[param], max |x| bits) over the TK_FP8 tiles' elements (uint-bit max, as K1).
 cudaError_t launch_unshard_push(const fsdpk::Tile* tiles, int ntiles, const float* shard,
                                 const float* scales, PeerPtrs arena, int W, int rank,
-                                fsdpk::LaunchCfg cfg, cudaStream_t st);
+                                fsdpk::LaunchCfg cfg, cudaStream_t st, uint32_t* amax_acc = nullptr);
 
 // Pull tiles: src = element offset into every rank's staging, dst = element offset into the
 // fp32 grad, n elements.  grad[dst+e] (+)= round?( sum_{q=0..W-1} (fp32(stage_q[src+e]) / W) ).

@@ -71,6 +71,16 @@ __global__ void k_signal_wait(FlagPtrs remote, unsigned long long* local, int W,
 #endif
 }
 
+// Delayed-scaling amax fused into the fp8 cast: every thread keeps the
+// max |x| bit pattern of the fp32 elements it cast (non-negative fp32 bits order like
+// uint32; NaN patterns propagate), the warp reduces it and lane 0 folds it into
+// acc[param] with atomicMax — the same uint-bit max as K1, so the result is bit-identical.
+__device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
+__device__ __forceinline__ void amax_commit(uint32_t* acc, uint32_t param, uint32_t m) {
+  m = __reduce_max_sync(0xFFFFFFFFu, m);
+  if ((threadIdx.x & 31u) == 0 && m) atomicMax(acc + param, m);
+}
+
 // ------------------------------------------------------------------- unshard push
 template <int V>   // floats per 16-byte output vector: 8 (bf16) or 16 (e4m3)
 __device__ __forceinline__ void load_floats(const float* p, uint32_t ph, float (&x)[V]) {
@@ -120,9 +130,10 @@ __device__ __forceinline__ uint4 cvt_e4m3x16(const float (&x)[16], float s) {
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-template <bool kFp8>
+template <bool kFp8, bool kAmax = false>
 __device__ __forceinline__ void push_tile(const Tile& tl, const float* __restrict__ shard, float s,
-                                          const PeerPtrs& arena, int W, int rank) {
+                                          const PeerPtrs& arena, int W, int rank, uint32_t* acc = nullptr) {
+  uint32_t am = 0;
   constexpr uint32_t es = kFp8 ? 1 : 2;
   constexpr uint32_t V = 16 / es;
   const float* src = shard + tl.src;
@@ -140,6 +151,10 @@ __device__ __forceinline__ void push_tile(const Tile& tl, const float* __restric
     float x0[V], x1[V];
     load_floats<V>(abase + V * v, ph, x0);
     load_floats<V>(abase + V * (v + kThreads), ph, x1);
+    if constexpr (kAmax) {
+#pragma unroll
+      for (uint32_t i = 0; i < V; ++i) am = max(am, max(abs_bits(x0[i]), abs_bits(x1[i])));
+    }
     uint4 o0, o1;
     if constexpr (kFp8) { o0 = cvt_e4m3x16(x0, s); o1 = cvt_e4m3x16(x1, s); }
     else { o0 = cvt_bf16x8(x0); o1 = cvt_bf16x8(x1); }
@@ -157,6 +172,10 @@ __device__ __forceinline__ void push_tile(const Tile& tl, const float* __restric
   for (; v < nb; v += kThreads) {
     float x[V];
     load_floats<V>(abase + V * v, ph, x);
+    if constexpr (kAmax) {
+#pragma unroll
+      for (uint32_t i = 0; i < V; ++i) am = max(am, abs_bits(x[i]));
+    }
     uint4 o;
     if constexpr (kFp8) o = cvt_e4m3x16(x, s);
     else o = cvt_bf16x8(x);
@@ -173,6 +192,7 @@ __device__ __forceinline__ void push_tile(const Tile& tl, const float* __restric
     const uint32_t el = e < h ? e : tail0 + (e - h);
     const uint64_t off = dst0 + (uint64_t)el * es;
     if (kFp8) {
+      if constexpr (kAmax) am = max(am, abs_bits(src[el]));
       const uint8_t b = (uint8_t)(pack_e4m3x2(__fmul_rn(src[el], s), 0.0f) & 0xFFu);
 #pragma unroll
       for (int d = 0; d < kMaxRanks; ++d) {
@@ -188,16 +208,20 @@ __device__ __forceinline__ void push_tile(const Tile& tl, const float* __restric
       }
     }
   }
+  if constexpr (kAmax) amax_commit(acc, tl.param, am);
 }
 
 __global__ void __launch_bounds__(kThreads) k_unshard_push(const Tile* __restrict__ tiles, int ntiles,
                                                            const float* __restrict__ shard,
                                                            const float* __restrict__ scales, PeerPtrs arena,
-                                                           int W, int rank) {
+                                                           int W, int rank, uint32_t* __restrict__ acc) {
   pdl_wait();   // the ready handshake before it has completed
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
-    if (tl.kind == fsdpk::TK_FP8) push_tile<true>(tl, shard, scales[tl.param], arena, W, rank);
+    if (tl.kind == fsdpk::TK_FP8) {
+      if (acc) push_tile<true, true>(tl, shard, scales[tl.param], arena, W, rank, acc);
+      else push_tile<true>(tl, shard, scales[tl.param], arena, W, rank);
+    }
     else push_tile<false>(tl, shard, 0.0f, arena, W, rank);
   }
   __threadfence_system();
@@ -543,9 +567,11 @@ __global__ void __launch_bounds__(kThreads) k_rs_pull_bulk(const Tile* __restric
   }
 }
 
-template <bool kFp8>
+template <bool kFp8, bool kAmax = false>
 __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __restrict__ shard, float s,
-                                               const PeerPtrs& arena, int W, uint8_t* stage_buf, uint32_t& it) {
+                                               const PeerPtrs& arena, int W, uint8_t* stage_buf, uint32_t& it,
+                                               uint32_t* acc = nullptr) {
+  uint32_t am = 0;
   constexpr uint32_t es = kFp8 ? 1 : 2;
   constexpr uint32_t V = 16 / es;                    // elements per 16-byte vector
   constexpr uint32_t CV = kBulkChunk / 16;           // vectors per chunk (= kThreads)
@@ -567,6 +593,10 @@ __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __re
     if (v < nb) {
       float x[V];
       load_floats<V>(abase + V * v, ph, x);
+      if constexpr (kAmax) {
+#pragma unroll
+        for (uint32_t i = 0; i < V; ++i) am = max(am, abs_bits(x[i]));
+      }
       uint4 o;
       if constexpr (kFp8) o = cvt_e4m3x16(x, s);
       else o = cvt_bf16x8(x);
@@ -590,6 +620,7 @@ __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __re
     const uint32_t el = e < h ? e : tail0 + (e - h);
     const uint64_t off = dst0 + (uint64_t)el * es;
     if (kFp8) {
+      if constexpr (kAmax) am = max(am, abs_bits(src[el]));
       const uint8_t b = (uint8_t)(pack_e4m3x2(__fmul_rn(src[el], s), 0.0f) & 0xFFu);
 #pragma unroll
       for (int d = 0; d < kMaxRanks; ++d) {
@@ -605,18 +636,22 @@ __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __re
       }
     }
   }
+  if constexpr (kAmax) amax_commit(acc, tl.param, am);
 }
 
 __global__ void __launch_bounds__(kThreads) k_unshard_push_bulk(const Tile* __restrict__ tiles, int ntiles,
                                                                 const float* __restrict__ shard,
                                                                 const float* __restrict__ scales, PeerPtrs arena,
-                                                                int W) {
+                                                                int W, uint32_t* __restrict__ acc) {
   __shared__ __align__(128) uint8_t stage_buf[2 * kBulkChunk];
   pdl_wait();
   uint32_t it = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
-    if (tl.kind == fsdpk::TK_FP8) push_tile_bulk<true>(tl, shard, scales[tl.param], arena, W, stage_buf, it);
+    if (tl.kind == fsdpk::TK_FP8) {
+      if (acc) push_tile_bulk<true, true>(tl, shard, scales[tl.param], arena, W, stage_buf, it, acc);
+      else push_tile_bulk<true>(tl, shard, scales[tl.param], arena, W, stage_buf, it);
+    }
     else push_tile_bulk<false>(tl, shard, 0.0f, arena, W, stage_buf, it);
   }
   if (threadIdx.x == 0) bulk_wait0();                 // every bulk store has completed
@@ -782,14 +817,15 @@ cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W
 }
 
 cudaError_t launch_unshard_push(const Tile* tiles, int ntiles, const float* shard, const float* scales,
-                                PeerPtrs arena, int W, int rank, fsdpk::LaunchCfg cfg, cudaStream_t st) {
+                                PeerPtrs arena, int W, int rank, fsdpk::LaunchCfg cfg, cudaStream_t st,
+                                uint32_t* amax_acc) {
   if (ntiles == 0) return cudaSuccess;
   PeerPtrs rot{};   // destination order starts at the next rank: spreads NVLink traffic
   for (int i = 0; i < W; ++i) rot.p[i] = arena.p[(rank + 1 + i) % W];
   const int g = grid_for(ntiles, cfg, fsdpk::kCtasPush);
   if (cfg.variant & 4)   // TMA bulk push
-    return launch_p(cfg.pdl, k_unshard_push_bulk, g, 0, st, tiles, ntiles, shard, scales, rot, W);
-  return launch_p(cfg.pdl, k_unshard_push, g, 0, st, tiles, ntiles, shard, scales, rot, W, rank);
+    return launch_p(cfg.pdl, k_unshard_push_bulk, g, 0, st, tiles, ntiles, shard, scales, rot, W, amax_acc);
+  return launch_p(cfg.pdl, k_unshard_push, g, 0, st, tiles, ntiles, shard, scales, rot, W, rank, amax_acc);
 }
 
 cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool grad_bf16, int divisor, float* grad, bool mean,

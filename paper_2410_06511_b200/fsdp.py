@@ -426,9 +426,13 @@ def zero_grad(layer: Layer, stream=None):
 
 
 # ----------------------------------------------------------------------- stage entry points
-def stage_copy_in(layer: Layer, dtype, slot: torch.Tensor, fp8_scales: Optional[torch.Tensor] = None, stream=None):
+def stage_copy_in(layer: Layer, dtype, slot: torch.Tensor, fp8_scales: Optional[torch.Tensor] = None, stream=None,
+                  amax_accum: Optional[torch.Tensor] = None):
+    """amax_accum (float32 [P], fp8 only): max-accumulates the cast elements' |x| per param."""
     sp = C.c_void_p(fp8_scales.data_ptr()) if fp8_scales is not None else C.c_void_p()
-    call("fsdp_stage_copy_in", layer.handle, _dtype_code(dtype), sp, C.c_void_p(slot.data_ptr()), _stream(stream))
+    ap = C.c_void_p(amax_accum.data_ptr()) if amax_accum is not None else C.c_void_p()
+    call("fsdp_stage_copy_in", layer.handle, _dtype_code(dtype), sp, C.c_void_p(slot.data_ptr()), ap,
+         _stream(stream))
 
 
 def stage_copy_out(layer: Layer, dtype, ag: torch.Tensor, outs: Sequence[torch.Tensor], stream=None):
@@ -465,9 +469,11 @@ def unsharded_layout(layer: Layer, dtype=torch.bfloat16):
 
 
 def stage_unshard_push(layer: Layer, dtype, arenas: Sequence[torch.Tensor], fp8_scales: Optional[torch.Tensor] = None,
-                       stream=None):
+                       stream=None, amax_accum: Optional[torch.Tensor] = None):
+    """amax_accum (float32 [P], fp8 only): max-accumulates the cast elements' |x| per param."""
     sp = C.c_void_p(fp8_scales.data_ptr()) if fp8_scales is not None else C.c_void_p()
-    call("fsdp_stage_unshard_push", layer.handle, _dtype_code(dtype), sp, _ptr_array(arenas), _stream(stream))
+    ap = C.c_void_p(amax_accum.data_ptr()) if amax_accum is not None else C.c_void_p()
+    call("fsdp_stage_unshard_push", layer.handle, _dtype_code(dtype), sp, _ptr_array(arenas), ap, _stream(stream))
 
 
 def grad_staging_layout(layer: Layer):

@@ -246,9 +246,13 @@ def test_w8_emulated_block_push_full(fp8):
         offs, total = F.unsharded_layout(emu.layers[0], dt)
         arenas = [torch.full((total + 4096,), 0xA5, dtype=torch.uint8, device="cuda") for _ in range(W)]
         sdev = torch.from_numpy(scale).cuda() if fp8 else None
+        fused = torch.zeros(len(shapes), dtype=torch.float32, device="cuda")
         for r in range(W):
-            F.stage_unshard_push(emu.layers[r], dt, arenas, fp8_scales=sdev)
+            F.stage_unshard_push(emu.layers[r], dt, arenas, fp8_scales=sdev, amax_accum=fused if fp8 else None)
         torch.cuda.synchronize()
+        if fp8:   # the delayed-scaling amax fused into the 8 pushes == the oracle's amax
+            amax = w.precompute_fp8_scales(shards)[0]
+            np.testing.assert_array_equal(fused.cpu().numpy().view(np.uint32), amax.view(np.uint32))
         _, fulls = w.unshard(shards, FP8 if fp8 else BF16, scale)
         for d in range(W):
             written = torch.zeros(arenas[d].numel(), dtype=torch.bool, device="cuda")

@@ -37,9 +37,14 @@ def test_unshard_push_emulated(kind, seed, W, fp8):
         offs, total = F.unsharded_layout(emu.layers[0], dt)
         arenas = [torch.full((total + 16,), 0xA5, dtype=torch.uint8, device="cuda") for _ in range(W)]
         sdev = torch.from_numpy(scale).cuda() if fp8 else None
+        fused = torch.zeros(max(len(shapes), 1), dtype=torch.float32, device="cuda")
         for r in range(W):
-            F.stage_unshard_push(emu.layers[r], dt, arenas, fp8_scales=sdev)
+            F.stage_unshard_push(emu.layers[r], dt, arenas, fp8_scales=sdev, amax_accum=fused if fp8 else None)
         torch.cuda.synchronize()
+        if fp8:   # the delayed-scaling amax fused into the push == the oracle's amax (eligible params)
+            amax = w.precompute_fp8_scales(shards)[0]
+            want_f = np.where(np.array(elig, bool), amax, np.float32(0)).astype(np.float32)
+            np.testing.assert_array_equal(fused.cpu().numpy()[:len(shapes)].view(np.uint32), want_f.view(np.uint32))
         _, fulls = w.unshard(shards, FP8 if fp8 else BF16, scale)
         for d in range(W):
             a = arenas[d].cpu().numpy()

@@ -131,11 +131,15 @@ def test_fp8_amax_scale_copy_in_copy_out(kind, seed, W):
         # K3 copy-in given the oracle's scale, then K4 copy-out of the oracle's buffer
         scale_dev = torch.from_numpy(scale).cuda()
         slots = [w.copy_in(s, FP8, scale) for s in shards]
+        fused = torch.zeros(l0.P, dtype=torch.float32, device="cuda")   # amax fused into K3 (delayed)
         for r, l in enumerate(emu.layers):
             slot = torch.zeros(l.S_bytes_fp8, dtype=torch.uint8, device="cuda")
-            F.stage_copy_in(l, torch.float8_e4m3fn, slot, fp8_scales=scale_dev)
+            F.stage_copy_in(l, torch.float8_e4m3fn, slot, fp8_scales=scale_dev, amax_accum=fused)
             torch.cuda.synchronize()
             np.testing.assert_array_equal(slot.cpu().numpy(), slots[r])
+        # max over the ranks' fused accumulators == the oracle's all-reduced amax (eligible params)
+        want_f = np.where(np.array(elig, bool), amax, np.float32(0)).astype(np.float32)
+        np.testing.assert_array_equal(fused.cpu().numpy().view(np.uint32), want_f.view(np.uint32))
         ag = w.all_gather(slots)
         fulls = w.copy_out(ag, FP8)
         outs = [torch.empty(s, dtype=torch.float8_e4m3fn if e else torch.bfloat16, device="cuda")

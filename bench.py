@@ -339,6 +339,11 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
 
+    mem = {k: round(v / 2 ** 30, 3) for k, v in mesh.memory().items()}   # after warm-up: pools at steady size
+    free_b, total_b = torch.cuda.mem_get_info(dev)
+    mem["device_used_GiB"] = round((total_b - free_b) / 2 ** 30, 2)
+    mem["device_total_GiB"] = round(total_b / 2 ** 30, 2)
+    mem["unit"] = "GiB per rank (peer_mapped: address space of W-1 peers' symmetric buffers, not local HBM)"
     timed_step, graph_prof = step, None
     if args.graph:
         # one eager profiled step: the per-step kernel counts / bytes (no timing events exist
@@ -562,7 +567,7 @@ def run_ours(args):
                          "pass": f"serial issue, {roof_steps} steps after the timed region (CUDA events on the launching streams)",
                          "step_hbm_GBps": round(step_hbm, 1), "step_hbm_frac": round(step_hbm / measured_peaks()[0], 4),
                          "step_hbm_frac_of_nominal": round(step_hbm / HBM_NOMINAL_GBS, 4)},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk, "memory": mem,
         }
         if proxy:
             line["compute_proxy"] = proxy

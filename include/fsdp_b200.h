@@ -196,6 +196,12 @@ fsdp_status_t fsdp_mesh_info_hsdp(const fsdp_mesh_t* mesh, int32_t* replicate_si
 fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* mesh);
 fsdp_status_t fsdp_mesh_info(const fsdp_mesh_t* mesh, int32_t* world_size, int32_t* rank,
                              int32_t* cuda_device);
+/* Device memory the mesh holds, in bytes (SURVEY §8(e) sizing at W): out[0] symmetric
+ * buffers this rank allocated (flags, P2P arenas and grad staging / receive slots, zero-copy
+ * grad buffers); out[1] the peers' copies of them mapped into this process over CUDA IPC
+ * (address space only: the peers' HBM); out[2] pooled NCCL-mode / W=1 buffers; out[3] the
+ * layers' fp32 shards and sharded grads (+ non-symmetric grad buffers). */
+fsdp_status_t fsdp_mesh_memory(const fsdp_mesh_t* mesh, int64_t out[4]);
 
 /* Selects the collective algorithm (fsdp_algo_t).  Collective: every rank must make the
  * same call at the same point, with no layer unsharded / reduce-scatter pending.  The

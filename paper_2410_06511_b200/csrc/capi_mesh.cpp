@@ -242,6 +242,29 @@ fsdp_status_t fsdp_mesh_info(const fsdp_mesh_t* m, int32_t* W, int32_t* rank, in
   });
 }
 
+fsdp_status_t fsdp_mesh_memory(const fsdp_mesh_t* m, int64_t out[4]) {
+  return guarded([&] {
+    if (!m || !out) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL argument");
+    int64_t sym = 0, pool = 0, layer = 0;
+    if (m->p2p_ok) sym += (int64_t)m->flags.bytes;
+    for (const auto* pl : {&m->p2p_ag, &m->p2p_rs})
+      for (const SymSlot* s : *pl) sym += (int64_t)s->buf.bytes;
+    for (const auto* pl : {&m->ag_slots, &m->rs_slots})
+      for (const Slot* s : *pl) pool += (int64_t)(s->a.cap + s->b.cap);
+    for (const fsdp_layer* l : m->layers) {
+      layer += 2 * (int64_t)sizeof(float) * std::max<int64_t>(l->L.S, 16);   // fp32 shard + sharded grad
+      if (l->gbuf) {
+        if (l->gbuf_sym) sym += (int64_t)l->gbuf->buf.bytes;
+        else layer += (int64_t)l->gbuf->buf.bytes;
+      }
+    }
+    out[0] = sym;                                       // symmetric buffers this rank allocated
+    out[1] = sym * (int64_t)std::max(m->W - 1, 0);      // the same buffers of W-1 peers, mapped
+    out[2] = pool;                                      // NCCL-mode / W=1 pooled buffers
+    out[3] = layer;                                     // per-layer fp32 shard + grad (+ plain grad buffers)
+  });
+}
+
 fsdp_status_t fsdp_mesh_abort(fsdp_mesh_t* m) {
   return guarded([&] {
     if (!m) fail(FSDP_ERR_INVALID_ARGUMENT, "mesh is NULL");

@@ -214,6 +214,12 @@ class Mesh:
         return {k: {"launches": int(pr.launches[i]), "ms": float(pr.total_ms[i]), "bytes": int(pr.bytes[i])}
                 for i, k in enumerate(capi.PROF_KINDS)}
 
+    def memory(self) -> dict:
+        """Device bytes the mesh holds (fsdp_mesh_memory)."""
+        out = (C.c_int64 * 4)()
+        call("fsdp_mesh_memory", self.handle, out)
+        return {"symmetric": out[0], "peer_mapped": out[1], "pools": out[2], "layers": out[3]}
+
     def destroy(self):
         for l in list(self.layers):
             l.destroy()

@@ -333,7 +333,12 @@ fsdp_status_t fsdp_fp8_scales(const fsdp_layer_t* layer, const float** scales_de
  * no-op for the same param_dtype and FSDP_ERR_STATE for another. */
 fsdp_status_t fsdp_unshard(fsdp_layer_t* layer, fsdp_dtype_t param_dtype,
                            const float* fp8_scales_dev, void* compute);
-/* Makes `compute` wait for the unshard.  State: UNSHARDING -> UNSHARDED. */
+/* Makes `compute` wait for the unshard.  State: UNSHARDING -> UNSHARDED.
+ * Both wait_* calls also report, without synchronizing, what has already failed
+ * asynchronously: a P2P handshake that gave up on a peer (FSDP_ERR_TIMEOUT) or a NCCL async
+ * error (FSDP_ERR_NCCL); the mesh is then unusable (fsdp_mesh_abort).  A failure that has not
+ * happened yet when wait_* is called is reported by a later wait_* or by
+ * fsdp_mesh_synchronize, which drains the streams and reports everything. */
 fsdp_status_t fsdp_wait_unshard(fsdp_layer_t* layer, void* compute);
 /* fsdp_unshard + fsdp_wait_unshard (the name used by BASELINE.json). */
 fsdp_status_t fsdp_all_gather_params(fsdp_layer_t* layer, fsdp_dtype_t param_dtype,

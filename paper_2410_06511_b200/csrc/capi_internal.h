@@ -261,7 +261,8 @@ struct fsdp_mesh {
   int32_t* reg_pos = nullptr;
   uint8_t* reg_hinit = nullptr;
   int hist_len = 0;               // fixed at the first delayed precompute
-  int* d_err = nullptr;
+  int* d_err = nullptr;              // device view of h_err (mapped pinned host memory)
+  volatile int* h_err = nullptr;
   cudaEvent_t ev_pre_call = nullptr, ev_pre_done = nullptr;
   std::vector<fsdp_layer*> layers;
   // precompute cache: layer list -> (amax tiles, finalize index list)
@@ -382,6 +383,7 @@ void launch_rs_copy_in_all(fsdp_layer* l, const void* const* grads, bool grad_bf
                            bool mean, cudaStream_t st);
 int64_t cin_bytes(const fsdp_layer* l, bool fp8);
 int64_t slot_bytes(const fsdp_layer* l, bool fp8);
+void poll_async_errors(fsdp_mesh* m);   // wait_*: report device timeouts / NCCL async errors seen so far
 void do_copy_in(fsdp_layer* l, bool fp8, const float* scales, void* dst, cudaStream_t st,
                 uint32_t* amax_acc = nullptr);
 void validate_grads(const fsdp_layer* l, const void* const* grads, fsdp_dtype_t gd, fsdp_dtype_t rd);

@@ -440,6 +440,7 @@ fsdp_status_t fsdp_wait_unshard(fsdp_layer_t* l, void* compute) {
     check_layer(l);
     if (l->state == UNSHARDED) return;
     if (l->state != UNSHARDING) fail(FSDP_ERR_STATE, "fsdp_wait_unshard without fsdp_unshard");
+    poll_async_errors(l->mesh);
     DeviceGuard g(l->mesh->device);
     CUDA_CHECK(cudaStreamWaitEvent(as_stream(compute), l->ev_done, 0));
     l->state = UNSHARDED;
@@ -747,6 +748,7 @@ fsdp_status_t fsdp_wait_reduce_scatter(fsdp_layer_t* l, void* compute) {
   return guarded([&] {
     check_layer(l);
     if (!l->rs_pending) return;
+    poll_async_errors(l->mesh);
     DeviceGuard g(l->mesh->device);
     CUDA_CHECK(cudaStreamWaitEvent(as_stream(compute), l->ev_rs_done, 0));
     l->rs_pending = false;

@@ -87,8 +87,15 @@ static void mesh_common_init(fsdp_mesh* m) {
   if (const char* e = std::getenv("FSDP_B200_PULL_STAGES")) m->cfg.pull_stages = std::max(2, std::min(4, std::atoi(e)));
   if (const char* e = std::getenv("FSDP_B200_PDL")) m->cfg.pdl = std::atoi(e) != 0;
   m->cfg.grid_cap = sms * (per_sm > 0 ? per_sm : 4);
-  CUDA_CHECK(cudaMalloc(&m->d_err, sizeof(int)));
-  CUDA_CHECK(cudaMemset(m->d_err, 0, sizeof(int)));
+  // device error flag in mapped pinned host memory: kernels store a code (plain stores, no
+  // atomics over PCIe), the host reads it without a copy or sync (wait_* poll it)
+  void* herr = nullptr;
+  CUDA_CHECK(cudaHostAlloc(&herr, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
+  m->h_err = static_cast<volatile int*>(herr);
+  *m->h_err = 0;
+  void* derr = nullptr;
+  CUDA_CHECK(cudaHostGetDevicePointer(&derr, herr, 0));
+  m->d_err = static_cast<int*>(derr);
   m->ev_pre_call = new_event();
   m->ev_pre_done = new_event();
   CUDA_CHECK(cudaMalloc(&m->d_barrier, sizeof(int)));
@@ -218,7 +225,7 @@ fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
     for (auto e : m->ev_pool) cudaEventDestroy(e);
     cudaFree(m->reg_acc); cudaFree(m->reg_amax); cudaFree(m->reg_scale); cudaFree(m->reg_elig);
     cudaFree(m->reg_hist); cudaFree(m->reg_pos); cudaFree(m->reg_hinit);
-    cudaFree(m->d_err);
+    if (m->h_err) cudaFreeHost(const_cast<int*>(m->h_err));
     cudaFree(m->d_barrier);
     cudaFree(m->d_epochs);
     if (m->ev_pre_call) cudaEventDestroy(m->ev_pre_call);
@@ -240,6 +247,27 @@ fsdp_status_t fsdp_mesh_info(const fsdp_mesh_t* m, int32_t* W, int32_t* rank, in
     if (rank) *rank = m->rank;
     if (dev) *dev = m->device;
   });
+}
+
+// SURVEY §8(b) "NCCL async errors and timeouts are reported by wait_*": what has already
+// happened on the device (a P2P handshake that gave up) or in NCCL is reported by the next
+// wait_* call, without a sync; fsdp_mesh_synchronize drains and reports everything.
+void poll_async_errors(fsdp_mesh* m) {
+  const int err = *m->h_err;
+  if ((err & 0xFF) == 2) {
+    m->aborted = true;
+    fail(FSDP_ERR_TIMEOUT, "P2P handshake timed out waiting for shard rank " + std::to_string(err >> 8) +
+                               " (a rank skipped or diverged from the collective call sequence); mesh aborted");
+  }
+  if (comm_ready(m)) {
+    for (ncclComm_t c : {m->comm_ag, m->comm_rs}) {
+      ncclResult_t ar = ncclSuccess;
+      if (c && ncclCommGetAsyncError(c, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
+        m->aborted = true;
+        fail(FSDP_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(ar));
+      }
+    }
+  }
 }
 
 fsdp_status_t fsdp_mesh_memory(const fsdp_mesh_t* m, int64_t out[4]) {
@@ -346,10 +374,9 @@ fsdp_status_t fsdp_mesh_synchronize(fsdp_mesh_t* m, int64_t timeout_ms) {
       }
       std::this_thread::sleep_for(std::chrono::microseconds(50));
     }
-    int err = 0;
-    CUDA_CHECK(cudaMemcpy(&err, m->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    const int err = *m->h_err;
     if (err) {
-      CUDA_CHECK(cudaMemset(m->d_err, 0, sizeof(int)));
+      *m->h_err = 0;
       if ((err & 0xFF) == 2) {   // a P2P handshake gave up waiting for a peer
         m->aborted = true;
         fail(FSDP_ERR_TIMEOUT, "P2P handshake timed out waiting for shard rank " + std::to_string(err >> 8) +

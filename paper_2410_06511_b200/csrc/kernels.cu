@@ -58,6 +58,8 @@ __global__ void __launch_bounds__(kThreads) k_copy_in_fp8(const Tile* __restrict
                                                           uint8_t* __restrict__ slot,
                                                           const float* __restrict__ scales,
                                                           uint32_t* __restrict__ acc) {
+  uint32_t run_m = 0;   // delayed scaling: running max |x| bits of run_p's tiles, committed on change
+  int run_p = -1;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
     const float* src = shard + tl.src;   // 16-element aligned
@@ -66,6 +68,14 @@ __global__ void __launch_bounds__(kThreads) k_copy_in_fp8(const Tile* __restrict
     if (tl.kind == TK_FP8) {
       const float s = scales[tl.param];
       const uint32_t nv = n / 16;
+      if (acc && (int)tl.param != run_p) {   // CTA-uniform
+        if (run_p >= 0) {
+          const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, run_m);
+          if ((threadIdx.x & 31u) == 0 && m) atomicMax(acc + run_p, m);
+        }
+        run_p = (int)tl.param;
+        run_m = 0;
+      }
       uint32_t am = 0;   // delayed scaling: max |x| bits of the cast elements (acc != NULL)
       for (uint32_t v = threadIdx.x; v < nv; v += kThreads) {
         uint4 q[4];
@@ -93,10 +103,7 @@ __global__ void __launch_bounds__(kThreads) k_copy_in_fp8(const Tile* __restrict
         const float x = __fmul_rn(src[e], s);
         dst[e] = (uint8_t)(pack_e4m3x2(x, 0.0f) & 0xFFu);
       }
-      if (acc) {
-        am = __reduce_max_sync(0xFFFFFFFFu, am);
-        if ((threadIdx.x & 31u) == 0 && am) atomicMax(acc + tl.param, am);
-      }
+      run_m = max(run_m, am);
     } else {  // bf16 param inside a float8 unit
       const uint32_t nv = n / 8;
       uint16_t* d16 = reinterpret_cast<uint16_t*>(dst);
@@ -112,6 +119,10 @@ __global__ void __launch_bounds__(kThreads) k_copy_in_fp8(const Tile* __restrict
       for (uint32_t e = nv * 8 + threadIdx.x; e < n; e += kThreads)
         d16[e] = (uint16_t)(pack_bf16x2(src[e], 0.0f) & 0xFFFFu);
     }
+  }
+  if (acc && run_p >= 0) {
+    const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, run_m);
+    if ((threadIdx.x & 31u) == 0 && m) atomicMax(acc + run_p, m);
   }
 }
 
@@ -420,7 +431,7 @@ __global__ void k_fp8_scale(const int32_t* __restrict__ idx, int n, uint32_t* __
   float s = 0.0f;
   if (eligible[j]) {
     if (!isfinite(a)) {
-      atomicExch(err, 1);
+      { *(volatile int*)err = 1; __threadfence_system(); }
     } else {
       const float c = fmaxf(a, 1e-12f);
       s = __double2float_rn(__ddiv_rn(448.0, (double)c));
@@ -442,7 +453,7 @@ __global__ void k_fp8_scale_delayed(const int32_t* __restrict__ idx, int n, uint
   amax_out[j] = a;
   acc[j] = 0u;
   if (!eligible[j]) { scale_out[j] = 0.0f; return; }
-  if (!isfinite(a)) { atomicExch(err, 1); scale_out[j] = 0.0f; return; }
+  if (!isfinite(a)) { { *(volatile int*)err = 1; __threadfence_system(); } scale_out[j] = 0.0f; return; }
   float* h = hist + (size_t)j * hmax;
   if (!init[j]) {                       // history initialised with the first observed amax
     for (int k = 0; k < H; ++k) h[k] = a;
@@ -469,7 +480,7 @@ __global__ void k_fp8_scale_delayed_fused(const int32_t* __restrict__ idx, int n
   amax_out[j] = a;
   acc[j] = 0u;
   if (!eligible[j]) { scale_out[j] = 0.0f; return; }
-  if (!isfinite(a)) { atomicExch(err, 1); scale_out[j] = 0.0f; return; }
+  if (!isfinite(a)) { { *(volatile int*)err = 1; __threadfence_system(); } scale_out[j] = 0.0f; return; }
   float* h = hist + (size_t)j * hmax;
   if (!init[j]) {
     for (int k = 0; k < H; ++k) h[k] = a;

@@ -12,6 +12,7 @@ the CPU oracle's World(W) simulation of all W ranks:
 * bf16 reduce: R11 bound; accumulate mode; layout mismatch -> FSDP_ERR_SHAPE;
 * a prefetch pipeline over several units with random stream delays."""
 import os
+import time
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -229,7 +230,12 @@ def run_fault_injection(W, rank, local):
     dist.barrier()
     if rank != W - 1:
         F.reduce_scatter_grads(layer, grads)
-        F.fsdp_wait_reduce_scatter(layer)
+        time.sleep(4.0)   # the device-side handshake gives up after 2 s
+        try:              # wait_* reports what already failed asynchronously
+            F.fsdp_wait_reduce_scatter(layer)
+            raise AssertionError("wait_reduce_scatter did not report the handshake timeout")
+        except F.FsdpError as e:
+            assert e.status_name == "FSDP_ERR_TIMEOUT", e
         try:
             mesh.synchronize(120000)
             raise AssertionError("the missing rank was not detected")

@@ -349,4 +349,25 @@ void validate_grads(const fsdp_layer* l, const void* const* grads, fsdp_dtype_t 
   if (rd != FSDP_BFLOAT16 && rd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "reduce_dtype must be FLOAT32 or BFLOAT16");
 }
 
+// SURVEY §8(b) "NCCL async errors and timeouts are reported by wait_*": what has already
+// happened on the device (a P2P handshake that gave up) or in NCCL is reported by the next
+// wait_* call, without a sync; fsdp_mesh_synchronize drains and reports everything.
+void poll_async_errors(fsdp_mesh* m) {
+  const int err = *m->h_err;
+  if ((err & 0xFF) == 2) {
+    m->aborted = true;
+    fail(FSDP_ERR_TIMEOUT, "P2P handshake timed out waiting for shard rank " + std::to_string(err >> 8) +
+                               " (a rank skipped or diverged from the collective call sequence); mesh aborted");
+  }
+  if (comm_ready(m)) {
+    for (ncclComm_t c : {m->comm_ag, m->comm_rs}) {
+      ncclResult_t ar = ncclSuccess;
+      if (c && ncclCommGetAsyncError(c, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
+        m->aborted = true;
+        fail(FSDP_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(ar));
+      }
+    }
+  }
+}
+
 }  // namespace fsdpc

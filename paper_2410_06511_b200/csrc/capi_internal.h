@@ -247,6 +247,11 @@ struct fsdp_mesh {
   ncclComm_t comm_ag = nullptr, comm_rs = nullptr;
   ncclComm_t comm_world = nullptr, comm_rep = nullptr;   // HSDP only
   cudaStream_t s_cin = nullptr, s_ag = nullptr, s_cout = nullptr, s_rsc = nullptr, s_rs = nullptr;
+  cudaStream_t s_ce = nullptr;     // copy-engine transfers of the unshard (FSDP_B200_CE)
+  cudaEvent_t ev_ce = nullptr;     // cast of param p done -> its copies may start (reused per param)
+  bool ce = false;                 // P2P transfers by the copy engines (cudaMemcpyAsync over the IPC
+                                   // mappings) instead of SM stores; FSDP_B200_CE=1
+
   fsdpk::LaunchCfg cfg{};
   std::vector<Slot*> ag_slots, rs_slots;
   uint64_t use_seq = 0;
@@ -332,6 +337,7 @@ struct fsdp_layer {
   // unshard ran since the last precompute; t_amax_reg: K1 tiles of this layer alone
   // (registry indices), the stand-in for an armed layer that was not unsharded in a step
   bool amax_armed = false, amax_pushed = false;
+  std::vector<int> push_tile_off_bf16, push_tile_off_fp8;   // first push tile of param p (P+1 entries)
   DevTiles t_amax_reg;
   std::vector<int64_t> stg_off_el;   // full-grad staging: param p at element offset (128-aligned)
   int64_t stg_elems = 0;
@@ -383,7 +389,18 @@ void launch_rs_copy_in_all(fsdp_layer* l, const void* const* grads, bool grad_bf
                            bool mean, cudaStream_t st);
 int64_t cin_bytes(const fsdp_layer* l, bool fp8);
 int64_t slot_bytes(const fsdp_layer* l, bool fp8);
-void poll_async_errors(fsdp_mesh* m);   // wait_*: report device timeouts / NCCL async errors seen so far
+void poll_async_errors(fsdp_mesh* m);
+// Copy-engine unshard (FSDP_B200_CE): cast this rank's rows into arenas.p[rank] one param at
+// a time (push kernel, local arena only) on `st`; after each param's cast the copy engines
+// send its rows to every other rank's arena (cudaMemcpyAsync on m->s_ce, peers in the order
+// rank+1, rank+2, ...); `st` then waits for the copies.
+void ce_unshard(fsdp_layer* l, bool fp8, const float* scales, const fsdpp::PeerPtrs& arenas, cudaStream_t st,
+                uint32_t* amax_acc);
+// Copy-engine store-scatter: this rank's rows of every other rank r's chunk (and of its own
+// when include_self) -> recvs.p[r] at slot `rank` (one cudaMemcpyAsync per rank and param, on
+// `st`, ranks in the order rank+1, rank+2, ...).
+void ce_scatter(fsdp_layer* l, const void* const* grads, int64_t gsz, const fsdpp::PeerPtrs& recvs, cudaStream_t st,
+                bool include_self);   // wait_*: report device timeouts / NCCL async errors seen so far
 void do_copy_in(fsdp_layer* l, bool fp8, const float* scales, void* dst, cudaStream_t st,
                 uint32_t* amax_acc = nullptr);
 void validate_grads(const fsdp_layer* l, const void* const* grads, fsdp_dtype_t gd, fsdp_dtype_t rd);

@@ -59,8 +59,14 @@ fsdp_status_t fsdp_shard(fsdp_mesh_t* m, int32_t n, const fsdp_param_desc_t* des
       l->t_cout_fp8.upload(fsdpl::tiles_copy_out(Ly, true, &l->t_cout_fp8.first));
       l->t_rsin.upload(fsdpl::tiles_rs_copy_in(Ly, &l->t_rsin.first));
       l->stg_off_el = fsdpl::staging_offsets(Ly, &l->stg_elems);
-      l->t_push_bf16.upload(fsdpl::tiles_push(Ly, false));
-      l->t_push_fp8.upload(fsdpl::tiles_push(Ly, true));
+      for (int f = 0; f < 2; ++f) {   // push tables are param-major: first tile of every param
+        const std::vector<Tile> tp = fsdpl::tiles_push(Ly, f == 1);
+        std::vector<int>& off = f ? l->push_tile_off_fp8 : l->push_tile_off_bf16;
+        off.assign(n + 1, 0);
+        for (const Tile& x : tp) off[x.param + 1]++;
+        for (int p = 0; p < n; ++p) off[p + 1] += off[p];
+        (f ? l->t_push_fp8 : l->t_push_bf16).upload(tp);
+      }
       l->t_pull.upload(fsdpl::tiles_pull(Ly, l->stg_off_el));
       l->t_stage_bf16.upload(fsdpl::tiles_stage(Ly, l->stg_off_el, 2));
       l->t_stage_fp32.upload(fsdpl::tiles_stage(Ly, l->stg_off_el, 4));
@@ -118,7 +124,7 @@ fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* l) {
     fsdp_mesh* m = l->mesh;
     if (l->state != SHARDED) fail(FSDP_ERR_STATE, "reshard the layer before destroying it");
     DeviceGuard g(m->device);
-    for (cudaStream_t s : {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs}) cudaStreamSynchronize(s);
+    for (cudaStream_t s : {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs, m->s_ce}) cudaStreamSynchronize(s);
     l->al.release(l->shard);
     l->al.release(l->grad);
     cudaFree(l->d_idx_local);
@@ -345,8 +351,11 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
       {
         const DevTiles& T = fp8 ? l->t_push_fp8 : l->t_push_bf16;
         ProfScope pp(m, FSDP_PROF_UNSHARD_PUSH, m->s_ag, fp8 ? l->push_bytes_fp8 : l->push_bytes_bf16);
-        CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, peer_ptrs(m, ss->buf), m->W, m->rank,
-                                              m->cfg, m->s_ag, amax_acc));
+        if (m->ce)   // cast locally, the copy engines send the rows (FSDP_B200_CE)
+          ce_unshard(l, fp8, scales, peer_ptrs(m, ss->buf), m->s_ag, amax_acc);
+        else
+          CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, peer_ptrs(m, ss->buf), m->W, m->rank,
+                                                m->cfg, m->s_ag, amax_acc));
         pp.done();
       }
       {
@@ -529,7 +538,7 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
     const int64_t bus_bytes = l->stg_elems * dtype_size(gd) * (m->W - 1) / std::max(m->W, 1);
     const bool p2p_store = m->p2p_rs_mode == FSDP_P2P_RS_STORE ||
                            (m->p2p_rs_mode == FSDP_P2P_RS_AUTO &&
-                            !(zc_layer && (m->W == 2 || bus_bytes < (64ll << 20))));
+                            (m->ce || !(zc_layer && (m->W == 2 || bus_bytes < (64ll << 20)))));
     if (m->algo == FSDP_ALGO_P2P && p2p_store) {
       // store-based path: ready handshake (this rank's receive buffer is free) -> scatter
       // (this rank's rows of every rank's chunk, read from the caller's grads, stored into
@@ -562,7 +571,10 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
         const DevTiles& T = own_direct ? (gd == FSDP_BFLOAT16 ? l->t_scatter_peers_bf16 : l->t_scatter_peers_fp32)
                                        : (gd == FSDP_BFLOAT16 ? l->t_scatter_bf16 : l->t_scatter_fp32);
         ProfScope pp(m, FSDP_PROF_RS_SCATTER, m->s_rs, l->scatter_elems * gsz);
-        CUDA_CHECK(fsdpp::launch_rs_scatter(T.d, T.n, pa, peer_ptrs(m, ss->buf), m->cfg, m->s_rs));
+        if (m->ce)   // the copy engines move the rows (FSDP_B200_CE)
+          ce_scatter(l, grads, gsz, peer_ptrs(m, ss->buf), m->s_rs, !own_direct);
+        else
+          CUDA_CHECK(fsdpp::launch_rs_scatter(T.d, T.n, pa, peer_ptrs(m, ss->buf), m->cfg, m->s_rs));
         pp.done();
       }
       {

@@ -67,7 +67,7 @@ fsdp_status_t fsdp_get_unique_id(uint8_t id[FSDP_UNIQUE_ID_BYTES]) {
 static void mesh_common_init(fsdp_mesh* m) {
   int prio_lo = 0, prio_hi = 0;
   CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-  for (cudaStream_t* s : {&m->s_cin, &m->s_ag, &m->s_cout, &m->s_rsc, &m->s_rs})
+  for (cudaStream_t* s : {&m->s_cin, &m->s_ag, &m->s_cout, &m->s_rsc, &m->s_rs, &m->s_ce})
     CUDA_CHECK(cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, prio_hi));
   int sms = 0;
   CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device));
@@ -96,6 +96,7 @@ static void mesh_common_init(fsdp_mesh* m) {
   void* derr = nullptr;
   CUDA_CHECK(cudaHostGetDevicePointer(&derr, herr, 0));
   m->d_err = static_cast<int*>(derr);
+  m->ev_ce = new_event();
   m->ev_pre_call = new_event();
   m->ev_pre_done = new_event();
   CUDA_CHECK(cudaMalloc(&m->d_barrier, sizeof(int)));
@@ -107,6 +108,7 @@ static void mesh_common_init(fsdp_mesh* m) {
 static void p2p_init(fsdp_mesh* m) {
   if (const char* e = std::getenv("FSDP_B200_STORE_OWN")) m->store_own_direct = std::atoi(e) != 0;
   if (const char* e = std::getenv("FSDP_B200_AMAX_FUSE")) m->amax_fuse = std::atoi(e) != 0;
+  if (const char* e = std::getenv("FSDP_B200_CE")) m->ce = std::atoi(e) != 0;
   if (m->local || m->W < 2 || m->W > 8) return;
   const size_t fbytes = sizeof(unsigned long long) * FK_NUM * kFlagSlots * fsdpp::kMaxRanks;
   m->p2p_ok = sym_alloc(m, m->flags, fbytes);
@@ -197,7 +199,7 @@ fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
     if (!m) return;
     if (!m->layers.empty()) fail(FSDP_ERR_STATE, "destroy all layers of the mesh first");
     DeviceGuard g(m->device);
-    for (cudaStream_t s : {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs})
+    for (cudaStream_t s : {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs, m->s_ce})
       if (s) cudaStreamSynchronize(s);
     if (!m->aborted) {
       p2p_teardown(m);
@@ -228,13 +230,14 @@ fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
     if (m->h_err) cudaFreeHost(const_cast<int*>(m->h_err));
     cudaFree(m->d_barrier);
     cudaFree(m->d_epochs);
+    if (m->ev_ce) cudaEventDestroy(m->ev_ce);
     if (m->ev_pre_call) cudaEventDestroy(m->ev_pre_call);
     if (m->ev_pre_done) cudaEventDestroy(m->ev_pre_done);
     if (m->comm_rs) { if (m->aborted) ncclCommAbort(m->comm_rs); else ncclCommDestroy(m->comm_rs); }
     if (m->comm_ag) { if (m->aborted) ncclCommAbort(m->comm_ag); else ncclCommDestroy(m->comm_ag); }
     for (ncclComm_t c : {m->comm_rep, m->comm_world})
       if (c) { if (m->aborted) ncclCommAbort(c); else ncclCommDestroy(c); }
-    for (cudaStream_t s : {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs})
+    for (cudaStream_t s : {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs, m->s_ce})
       if (s) cudaStreamDestroy(s);
     delete m;
   });
@@ -325,7 +328,7 @@ fsdp_status_t fsdp_mesh_synchronize(fsdp_mesh_t* m, int64_t timeout_ms) {
     check_mesh(m);
     DeviceGuard g(m->device);
     const auto t0 = std::chrono::steady_clock::now();
-    cudaStream_t ss[] = {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs};
+    cudaStream_t ss[] = {m->s_cin, m->s_ag, m->s_cout, m->s_rsc, m->s_rs, m->s_ce};
     for (;;) {
       bool idle = true;
       for (cudaStream_t s : ss) {

@@ -139,8 +139,12 @@ fsdp_status_t fsdp_stage_unshard_push(const fsdp_layer_t* lc, fsdp_dtype_t dt, c
     DeviceGuard g(m->device);
     const DevTiles& T = fp8 ? l->t_push_fp8 : l->t_push_bf16;
     ProfScope ps(m, FSDP_PROF_UNSHARD_PUSH, as_stream(stream), fp8 ? l->push_bytes_fp8 : l->push_bytes_bf16);
-    CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, pp, m->W, m->rank, m->cfg, as_stream(stream),
-                                          fp8 ? reinterpret_cast<uint32_t*>(amax_accum) : nullptr));
+    uint32_t* acc = fp8 ? reinterpret_cast<uint32_t*>(amax_accum) : nullptr;
+    if (m->ce)
+      ce_unshard(l, fp8, scales, pp, as_stream(stream), acc);
+    else
+      CUDA_CHECK(fsdpp::launch_unshard_push(T.d, T.n, l->shard, scales, pp, m->W, m->rank, m->cfg, as_stream(stream),
+                                            acc));
     ps.done();
   });
 }
@@ -213,7 +217,10 @@ fsdp_status_t fsdp_stage_rs_scatter(const fsdp_layer_t* lc, const void* const* g
                                      : (gd == FSDP_BFLOAT16 ? l->t_scatter_peers_bf16 : l->t_scatter_peers_fp32);
     DeviceGuard g(m->device);
     ProfScope ps(m, FSDP_PROF_RS_SCATTER, as_stream(stream), l->scatter_elems * dtype_size(gd));
-    CUDA_CHECK(fsdpp::launch_rs_scatter(T.d, T.n, pa, pp, m->cfg, as_stream(stream)));
+    if (m->ce)
+      ce_scatter(l, grads, dtype_size(gd), pp, as_stream(stream), include_self != 0);
+    else
+      CUDA_CHECK(fsdpp::launch_rs_scatter(T.d, T.n, pa, pp, m->cfg, as_stream(stream)));
     ps.done();
   });
 }

@@ -370,4 +370,51 @@ void poll_async_errors(fsdp_mesh* m) {
   }
 }
 
+void ce_unshard(fsdp_layer* l, bool fp8, const float* scales, const fsdpp::PeerPtrs& arenas, cudaStream_t st,
+                uint32_t* amax_acc) {
+  fsdp_mesh* m = l->mesh;
+  const fsdpl::Layout& L = l->L;
+  const DevTiles& T = fp8 ? l->t_push_fp8 : l->t_push_bf16;
+  const std::vector<int>& toff = fp8 ? l->push_tile_off_fp8 : l->push_tile_off_bf16;
+  const std::vector<int64_t>& uoff = fp8 ? L.uoff_fp8 : L.uoff_bf16;
+  fsdpp::PeerPtrs loc{};
+  loc.p[0] = arenas.p[L.rank];
+  fsdpk::LaunchCfg cfg = m->cfg;
+  cfg.pdl = false;
+  for (int p = 0; p < l->P; ++p) {
+    const int nt = toff[p + 1] - toff[p];
+    if (nt == 0) continue;
+    CUDA_CHECK(fsdpp::launch_unshard_push(T.d + toff[p], nt, l->shard, scales, loc, 1, 0, cfg, st, amax_acc));
+    CUDA_CHECK(cudaEventRecord(m->ev_ce, st));
+    CUDA_CHECK(cudaStreamWaitEvent(m->s_ce, m->ev_ce, 0));
+    const auto& mt = L.metas[p];
+    const int64_t es = (fp8 && L.fp8[p]) ? 1 : 2;
+    const int64_t off = uoff[p] + mt.row_begin * mt.rest * es;
+    const size_t bytes = (size_t)(mt.row_count * mt.rest * es);
+    for (int k = 1; k < L.W; ++k) {
+      const int q = (L.rank + k) % L.W;
+      CUDA_CHECK(cudaMemcpyAsync(arenas.p[q] + off, arenas.p[L.rank] + off, bytes, cudaMemcpyDeviceToDevice, m->s_ce));
+    }
+  }
+  CUDA_CHECK(cudaEventRecord(m->ev_ce, m->s_ce));
+  CUDA_CHECK(cudaStreamWaitEvent(st, m->ev_ce, 0));
+}
+
+void ce_scatter(fsdp_layer* l, const void* const* grads, int64_t gsz, const fsdpp::PeerPtrs& recvs, cudaStream_t st,
+                bool include_self) {
+  const fsdpl::Layout& L = l->L;
+  for (int k = include_self ? 0 : 1; k < L.W; ++k) {
+    const int r = (L.rank + k) % L.W;
+    for (int p = 0; p < l->P; ++p) {
+      const auto& mt = L.metas[p];
+      const int64_t b = std::min<int64_t>((int64_t)r * mt.chunk_rows, mt.dim0);
+      const int64_t e = std::min<int64_t>((int64_t)(r + 1) * mt.chunk_rows, mt.dim0);
+      if (e <= b || mt.rest == 0) continue;
+      const uint8_t* src = static_cast<const uint8_t*>(grads[p]) + (size_t)(b * mt.rest * gsz);
+      uint8_t* dst = recvs.p[r] + (size_t)(((int64_t)L.rank * L.S + mt.elem_offset) * gsz);
+      CUDA_CHECK(cudaMemcpyAsync(dst, src, (size_t)((e - b) * mt.rest * gsz), cudaMemcpyDeviceToDevice, st));
+    }
+  }
+}
+
 }  // namespace fsdpc

@@ -50,7 +50,7 @@ def main():
     ap.add_argument("--W", type=int, default=2)
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--model", default="llama3.1-8b")
-    ap.add_argument("--kernels", default="push,scatter,pull")
+    ap.add_argument("--kernels", default="push,scatter,pull,ce")
     args = ap.parse_args()
     W = args.W
     assert torch.cuda.device_count() >= W, f"needs {W} GPUs"
@@ -106,6 +106,33 @@ def main():
         timed("k_unshard_push_bulk",
               lambda r, s: F.stage_unshard_push(layers[r], torch.bfloat16, arenas, stream=s),
               [(W - 1) * 2 * c for c in own])
+        del arenas
+    if "ce" in kinds:
+        # copy-engine variant of the push's transfer (rows already cast): per peer and param one
+        # cudaMemcpyPeerAsync of this rank's rows into the peer's arena, on `nce` streams per rank
+        from cuda.bindings import runtime as rt
+        offs, total = F.unsharded_layout(layers[0], torch.bfloat16)
+        arenas = [torch.empty(total, dtype=torch.uint8, device=f"cuda:{d}") for d in range(W)]
+        for nce in (1, 2, 4):
+            ce_st = [[torch.cuda.Stream(device=r) for _ in range(nce)] for r in range(W)]
+
+            def ce_push(r, s, nce=nce, ce_st=ce_st):
+                jobs = []
+                for k in range(1, W):
+                    q = (r + k) % W
+                    for p, m in enumerate(layers[r].metas):
+                        n = m["row_count"] * m["rest"] * 2
+                        if n:
+                            off = offs[p] + m["row_begin"] * m["rest"] * 2
+                            jobs.append((arenas[q].data_ptr() + off, q, arenas[r].data_ptr() + off, r, n))
+                for st in ce_st[r]:
+                    st.wait_stream(s)
+                for i, (d, dq, src, sr, n) in enumerate(jobs):
+                    err = rt.cudaMemcpyPeerAsync(d, dq, src, sr, n, ce_st[r][i % nce].cuda_stream)[0]
+                    assert int(err) == 0, err
+                for st in ce_st[r]:
+                    s.wait_stream(st)
+            timed(f"ce_push_{nce}streams", ce_push, [(W - 1) * 2 * c for c in own])
         del arenas
     grads = []
     for q in range(W):

@@ -234,7 +234,9 @@ fsdp_status_t fsdp_mesh_get_p2p_rs(const fsdp_mesh_t* mesh, int32_t* mode);
  * asynchronous errors.  Returns FSDP_ERR_NONFINITE if a precompute saw a non-finite
  * amax since the last call (flag is then cleared), FSDP_ERR_NCCL on a NCCL async
  * error, FSDP_ERR_TIMEOUT after timeout_ms (<= 0: no timeout); after NCCL/TIMEOUT the
- * communicators are aborted and the mesh is unusable. */
+ * communicators are aborted and the mesh is unusable.  The abort is sticky: every later
+ * call on the mesh (this one included) returns the FIRST failure's status and message,
+ * whichever call (wait_* or this one) reported it first. */
 fsdp_status_t fsdp_mesh_synchronize(fsdp_mesh_t* mesh, int64_t timeout_ms);
 /* Marks the mesh unusable without any collective step (aborts its NCCL communicators);
  * layers and the mesh can then be destroyed rank-locally.  Use after FSDP_ERR_TIMEOUT /

@@ -285,6 +285,8 @@ struct fsdp_mesh {
   std::vector<cudaEvent_t> ev_pool;
   fsdp_profile_t prof_acc{};
   bool aborted = false;
+  fsdp_status_t abort_status = FSDP_ERR_STATE;   // why (sticky: every later call reports it)
+  std::string abort_msg = "mesh was aborted by fsdp_mesh_abort";
   // P2P (fused peer-memory) path
   int algo = FSDP_ALGO_NCCL;
   int p2p_rs_mode = FSDP_P2P_RS_AUTO;        // how the P2P reduce-scatter moves data
@@ -390,6 +392,8 @@ void launch_rs_copy_in_all(fsdp_layer* l, const void* const* grads, bool grad_bf
 int64_t cin_bytes(const fsdp_layer* l, bool fp8);
 int64_t slot_bytes(const fsdp_layer* l, bool fp8);
 void poll_async_errors(fsdp_mesh* m);
+// Marks the mesh aborted with a sticky reason and throws it (later calls re-report it).
+[[noreturn]] void abort_mesh(fsdp_mesh* m, fsdp_status_t st, const std::string& msg);
 // Copy-engine unshard (FSDP_B200_CE): cast this rank's rows into arenas.p[rank] one param at
 // a time (push kernel, local arena only) on `st`; after each param's cast the copy engines
 // send its rows to every other rank's arena (cudaMemcpyAsync on m->s_ce, peers in the order

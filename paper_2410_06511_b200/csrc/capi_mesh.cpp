@@ -340,30 +340,24 @@ fsdp_status_t fsdp_mesh_synchronize(fsdp_mesh_t* m, int64_t timeout_ms) {
         for (ncclComm_t c : {m->comm_ag, m->comm_rs}) {
           ncclResult_t ar = ncclSuccess;
           NCCL_CHECK(ncclCommGetAsyncError(c, &ar));
-          if (ar != ncclSuccess) {
-            m->aborted = true;
-            fail(FSDP_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(ar));
-          }
+          if (ar != ncclSuccess) abort_mesh(m, FSDP_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(ar));
         }
       }
       if (idle) break;
       if (timeout_ms > 0 && std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(timeout_ms)) {
-        m->aborted = true;
         if (m->comm_ag) ncclCommAbort(m->comm_ag);
         if (m->comm_rs) ncclCommAbort(m->comm_rs);
         m->comm_ag = m->comm_rs = nullptr;
-        fail(FSDP_ERR_TIMEOUT, "mesh streams did not drain before the timeout; communicators aborted");
+        abort_mesh(m, FSDP_ERR_TIMEOUT, "mesh streams did not drain before the timeout; communicators aborted");
       }
       std::this_thread::sleep_for(std::chrono::microseconds(50));
     }
     const int err = *m->h_err;
     if (err) {
       *m->h_err = 0;
-      if ((err & 0xFF) == 2) {   // a P2P handshake gave up waiting for a peer
-        m->aborted = true;
-        fail(FSDP_ERR_TIMEOUT, "P2P handshake timed out waiting for shard rank " + std::to_string(err >> 8) +
-                                   " (a rank skipped or diverged from the collective call sequence); mesh aborted");
-      }
+      if ((err & 0xFF) == 2)   // a P2P handshake gave up waiting for a peer
+        abort_mesh(m, FSDP_ERR_TIMEOUT, "P2P handshake timed out waiting for shard rank " + std::to_string(err >> 8) +
+                                            " (a rank skipped or diverged from the collective call sequence); mesh aborted");
       fail(FSDP_ERR_NONFINITE, "non-finite fp8 amax seen by fsdp_precompute_fp8_scales (SPEC.md:38)");
     }
   });

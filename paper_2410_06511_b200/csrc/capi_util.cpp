@@ -93,7 +93,16 @@ void release_sym_slot(SymSlot* s, cudaStream_t last_user, const Capture& cap) { 
 
 void check_mesh(const fsdp_mesh* m) {
   if (!m) fail(FSDP_ERR_INVALID_ARGUMENT, "mesh is NULL");
-  if (m->aborted) fail(FSDP_ERR_STATE, "mesh was aborted after a NCCL error/timeout");
+  if (m->aborted) fail(m->abort_status, "mesh aborted earlier: " + m->abort_msg);
+}
+
+void abort_mesh(fsdp_mesh* m, fsdp_status_t st, const std::string& msg) {
+  if (!m->aborted) {   // the first reason sticks
+    m->aborted = true;
+    m->abort_status = st;
+    m->abort_msg = msg;
+  }
+  fail(st, msg);
 }
 void check_layer(const fsdp_layer* l) {
   if (!l) fail(FSDP_ERR_INVALID_ARGUMENT, "layer is NULL");
@@ -354,18 +363,14 @@ void validate_grads(const fsdp_layer* l, const void* const* grads, fsdp_dtype_t 
 // wait_* call, without a sync; fsdp_mesh_synchronize drains and reports everything.
 void poll_async_errors(fsdp_mesh* m) {
   const int err = *m->h_err;
-  if ((err & 0xFF) == 2) {
-    m->aborted = true;
-    fail(FSDP_ERR_TIMEOUT, "P2P handshake timed out waiting for shard rank " + std::to_string(err >> 8) +
-                               " (a rank skipped or diverged from the collective call sequence); mesh aborted");
-  }
+  if ((err & 0xFF) == 2)
+    abort_mesh(m, FSDP_ERR_TIMEOUT, "P2P handshake timed out waiting for shard rank " + std::to_string(err >> 8) +
+                                        " (a rank skipped or diverged from the collective call sequence); mesh aborted");
   if (comm_ready(m)) {
     for (ncclComm_t c : {m->comm_ag, m->comm_rs}) {
       ncclResult_t ar = ncclSuccess;
-      if (c && ncclCommGetAsyncError(c, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
-        m->aborted = true;
-        fail(FSDP_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(ar));
-      }
+      if (c && ncclCommGetAsyncError(c, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress)
+        abort_mesh(m, FSDP_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(ar));
     }
   }
 }

@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(kThreads) k_copy_in_bf16(const float4* __restr
 }
 
 // ------------------------------------------------------------------- K3 copy-in fp8
+template <bool kAmax>   // compile-time: the amax-free instance keeps its 32 registers
 __global__ void __launch_bounds__(kThreads) k_copy_in_fp8(const Tile* __restrict__ tiles, int ntiles,
                                                           const float* __restrict__ shard,
                                                           uint8_t* __restrict__ slot,
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(kThreads) k_copy_in_fp8(const Tile* __restrict
     if (tl.kind == TK_FP8) {
       const float s = scales[tl.param];
       const uint32_t nv = n / 16;
-      if (acc && (int)tl.param != run_p) {   // CTA-uniform
+      if (kAmax && (int)tl.param != run_p) {   // CTA-uniform
         if (run_p >= 0) {
           const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, run_m);
           if ((threadIdx.x & 31u) == 0 && m) atomicMax(acc + run_p, m);
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kThreads) k_copy_in_fp8(const Tile* __restrict
         uint4 q[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) q[j] = ld_stream(src + 16 * v + 4 * j);
-        if (acc) {
+        if constexpr (kAmax) {
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             am = max(am, max(max(q[j].x & 0x7FFFFFFFu, q[j].y & 0x7FFFFFFFu),
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(kThreads) k_copy_in_fp8(const Tile* __restrict
         st_v4(dst + 16 * v, make_uint4(w[0], w[1], w[2], w[3]));
       }
       for (uint32_t e = nv * 16 + threadIdx.x; e < n; e += kThreads) {
-        if (acc) am = max(am, __float_as_uint(src[e]) & 0x7FFFFFFFu);
+        if constexpr (kAmax) am = max(am, __float_as_uint(src[e]) & 0x7FFFFFFFu);
         const float x = __fmul_rn(src[e], s);
         dst[e] = (uint8_t)(pack_e4m3x2(x, 0.0f) & 0xFFu);
       }
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(kThreads) k_copy_in_fp8(const Tile* __restrict
         d16[e] = (uint16_t)(pack_bf16x2(src[e], 0.0f) & 0xFFFFu);
     }
   }
-  if (acc && run_p >= 0) {
+  if (kAmax && run_p >= 0) {
     const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, run_m);
     if ((threadIdx.x & 31u) == 0 && m) atomicMax(acc + run_p, m);
   }
@@ -513,8 +514,8 @@ cudaError_t launch_copy_in_bf16(const float* shard, void* slot, int64_t S, Launc
 cudaError_t launch_copy_in_fp8(const Tile* tiles, int ntiles, const float* shard, void* slot,
                                const float* scales, LaunchCfg cfg, cudaStream_t st, uint32_t* amax_acc) {
   if (ntiles == 0) return cudaSuccess;
-  return launch_persistent(k_copy_in_fp8, grid_for(ntiles, cfg), 0, st, tiles, ntiles, shard, (uint8_t*)slot,
-                           scales, amax_acc);
+  return launch_persistent(amax_acc ? k_copy_in_fp8<true> : k_copy_in_fp8<false>, grid_for(ntiles, cfg), 0, st,
+                           tiles, ntiles, shard, (uint8_t*)slot, scales, amax_acc);
 }
 
 cudaError_t launch_copy_out(const Tile* tiles, int ntiles, const void* ag, const PtrArray& outs,

@@ -76,29 +76,22 @@ __global__ void k_signal_wait(FlagPtrs remote, unsigned long long* local, int W,
 // uint32; NaN patterns propagate), the warp reduces it and lane 0 folds it into
 // acc[param] with atomicMax — the same uint-bit max as K1, so the result is bit-identical.
 __device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
-__device__ __forceinline__ void amax_commit(uint32_t* acc, uint32_t param, uint32_t m) {
+// One atomic per CTA per tile: warp max -> shared -> warp 0 max -> thread 0 atomicMax
+// (~13K atomics per 8B block instead of ~106K per-warp ones, which serialised at L2 on the
+// ~7 addresses of a block and cost ~80 us).  A running per-param max committed only when the
+// param changes needed 24 more registers (64) and cut the push's occupancy.  CTA-uniform
+// call; red[] is reused after the trailing barrier.
+__device__ __forceinline__ void amax_commit_cta(uint32_t* acc, uint32_t param, uint32_t m, uint32_t* red) {
   m = __reduce_max_sync(0xFFFFFFFFu, m);
-  if ((threadIdx.x & 31u) == 0 && m) atomicMax(acc + param, m);
+  if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t r = threadIdx.x < kThreads / 32 ? red[threadIdx.x] : 0u;
+    r = __reduce_max_sync(0xFFFFFFFFu, r);
+    if (threadIdx.x == 0 && r) atomicMax(acc + param, r);
+  }
+  __syncthreads();
 }
-// A CTA walks its tiles in param order (round robin over a param-ordered table), so the
-// running max is committed only when the param changes and once at the end: ~2 commits per
-// CTA per kernel instead of one per tile (per-tile atomics on ~7 addresses serialised at L2
-// and cost ~80 us per 8B block).  CTA-uniform calls.
-struct AmaxRun {
-  uint32_t m = 0;
-  int param = -1;
-  __device__ __forceinline__ void next(uint32_t* acc, uint32_t p) {
-    if ((int)p != param) {
-      if (param >= 0) amax_commit(acc, (uint32_t)param, m);
-      param = (int)p;
-      m = 0;
-    }
-  }
-  __device__ __forceinline__ void flush(uint32_t* acc) {
-    if (param >= 0) amax_commit(acc, (uint32_t)param, m);
-  }
-};
-
 // ------------------------------------------------------------------- unshard push
 template <int V>   // floats per 16-byte output vector: 8 (bf16) or 16 (e4m3)
 __device__ __forceinline__ void load_floats(const float* p, uint32_t ph, float (&x)[V]) {
@@ -113,6 +106,45 @@ __device__ __forceinline__ void load_floats(const float* p, uint32_t ph, float (
       w[4 * i + 2] = __uint_as_float(q.z); w[4 * i + 3] = __uint_as_float(q.w);
     }
   }
+  switch (ph) {
+    case 0:
+#pragma unroll
+      for (int i = 0; i < V; ++i) x[i] = w[i];
+      break;
+    case 1:
+#pragma unroll
+      for (int i = 0; i < V; ++i) x[i] = w[i + 1];
+      break;
+    case 2:
+#pragma unroll
+      for (int i = 0; i < V; ++i) x[i] = w[i + 2];
+      break;
+    default:
+#pragma unroll
+      for (int i = 0; i < V; ++i) x[i] = w[i + 3];
+      break;
+  }
+}
+
+// load_floats + max |x| bits of the V selected words, taken on the loaded words before the
+// phase shift (a per-word mask instead of a max after it: that variant needed 18 more registers)
+template <int V>
+__device__ __forceinline__ void load_floats_amax(const float* p, uint32_t ph, float (&x)[V], uint32_t& am) {
+  constexpr int NQ = V / 4 + 1;
+  float w[NQ * 4];
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) {
+    if (i < V / 4 || ph != 0) {
+      const uint4 q = ld_stream(p + 4 * i);
+      w[4 * i] = __uint_as_float(q.x); w[4 * i + 1] = __uint_as_float(q.y);
+      w[4 * i + 2] = __uint_as_float(q.z); w[4 * i + 3] = __uint_as_float(q.w);
+    } else {
+      w[4 * i] = w[4 * i + 1] = w[4 * i + 2] = w[4 * i + 3] = 0.0f;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NQ * 4; ++i)
+    if ((uint32_t)i >= ph && (uint32_t)i < ph + V) am = max(am, __float_as_uint(w[i]) & 0x7FFFFFFFu);
   switch (ph) {
     case 0:
 #pragma unroll
@@ -167,11 +199,12 @@ __device__ __forceinline__ void push_tile(const Tile& tl, const float* __restric
   uint32_t v = threadIdx.x;
   for (; v + kThreads < nb; v += 2 * kThreads) {
     float x0[V], x1[V];
-    load_floats<V>(abase + V * v, ph, x0);
-    load_floats<V>(abase + V * (v + kThreads), ph, x1);
     if constexpr (kAmax) {
-#pragma unroll
-      for (uint32_t i = 0; i < V; ++i) am = max(am, max(abs_bits(x0[i]), abs_bits(x1[i])));
+      load_floats_amax<V>(abase + V * v, ph, x0, am);
+      load_floats_amax<V>(abase + V * (v + kThreads), ph, x1, am);
+    } else {
+      load_floats<V>(abase + V * v, ph, x0);
+      load_floats<V>(abase + V * (v + kThreads), ph, x1);
     }
     uint4 o0, o1;
     if constexpr (kFp8) { o0 = cvt_e4m3x16(x0, s); o1 = cvt_e4m3x16(x1, s); }
@@ -189,11 +222,8 @@ __device__ __forceinline__ void push_tile(const Tile& tl, const float* __restric
   }
   for (; v < nb; v += kThreads) {
     float x[V];
-    load_floats<V>(abase + V * v, ph, x);
-    if constexpr (kAmax) {
-#pragma unroll
-      for (uint32_t i = 0; i < V; ++i) am = max(am, abs_bits(x[i]));
-    }
+    if constexpr (kAmax) load_floats_amax<V>(abase + V * v, ph, x, am);
+    else load_floats<V>(abase + V * v, ph, x);
     uint4 o;
     if constexpr (kFp8) o = cvt_e4m3x16(x, s);
     else o = cvt_bf16x8(x);
@@ -229,25 +259,29 @@ __device__ __forceinline__ void push_tile(const Tile& tl, const float* __restric
   if constexpr (kAmax) *amp = max(*amp, am);
 }
 
+// kAmax is a template parameter, not a runtime branch: with both fp8 paths in one kernel the
+// register count doubled (37 -> 79 bulk, 56 -> 106 register push), occupancy fell and the bf16
+// W=1 step went 15.2 -> 18.3 ms (profiles/round2/v2).  The amax-free instance is the old kernel.
+template <bool kAmax>
 __global__ void __launch_bounds__(kThreads) k_unshard_push(const Tile* __restrict__ tiles, int ntiles,
                                                            const float* __restrict__ shard,
                                                            const float* __restrict__ scales, PeerPtrs arena,
                                                            int W, int rank, uint32_t* __restrict__ acc) {
+  __shared__ uint32_t red[kThreads / 32];
   pdl_wait();   // the ready handshake before it has completed
-  AmaxRun run;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
     if (tl.kind == fsdpk::TK_FP8) {
-      if (acc) {
-        run.next(acc, tl.param);
-        push_tile<true, true>(tl, shard, scales[tl.param], arena, W, rank, &run.m);
+      if constexpr (kAmax) {
+        uint32_t mm = 0;
+        push_tile<true, true>(tl, shard, scales[tl.param], arena, W, rank, &mm);
+        amax_commit_cta(acc, tl.param, mm, red);
       } else {
         push_tile<true>(tl, shard, scales[tl.param], arena, W, rank);
       }
     }
     else push_tile<false>(tl, shard, 0.0f, arena, W, rank);
   }
-  if (acc) run.flush(acc);
   __threadfence_system();
 }
 
@@ -616,11 +650,8 @@ __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __re
     const uint32_t v = c * CV + threadIdx.x;
     if (v < nb) {
       float x[V];
-      load_floats<V>(abase + V * v, ph, x);
-      if constexpr (kAmax) {
-#pragma unroll
-        for (uint32_t i = 0; i < V; ++i) am = max(am, abs_bits(x[i]));
-      }
+      if constexpr (kAmax) load_floats_amax<V>(abase + V * v, ph, x, am);
+      else load_floats<V>(abase + V * v, ph, x);
       uint4 o;
       if constexpr (kFp8) o = cvt_e4m3x16(x, s);
       else o = cvt_bf16x8(x);
@@ -663,27 +694,28 @@ __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __re
   if constexpr (kAmax) *amp = max(*amp, am);
 }
 
+template <bool kAmax>
 __global__ void __launch_bounds__(kThreads) k_unshard_push_bulk(const Tile* __restrict__ tiles, int ntiles,
                                                                 const float* __restrict__ shard,
                                                                 const float* __restrict__ scales, PeerPtrs arena,
                                                                 int W, uint32_t* __restrict__ acc) {
   __shared__ __align__(128) uint8_t stage_buf[2 * kBulkChunk];
+  __shared__ uint32_t red[kThreads / 32];
   pdl_wait();
   uint32_t it = 0;
-  AmaxRun run;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
     if (tl.kind == fsdpk::TK_FP8) {
-      if (acc) {
-        run.next(acc, tl.param);
-        push_tile_bulk<true, true>(tl, shard, scales[tl.param], arena, W, stage_buf, it, &run.m);
+      if constexpr (kAmax) {
+        uint32_t mm = 0;
+        push_tile_bulk<true, true>(tl, shard, scales[tl.param], arena, W, stage_buf, it, &mm);
+        amax_commit_cta(acc, tl.param, mm, red);
       } else {
         push_tile_bulk<true>(tl, shard, scales[tl.param], arena, W, stage_buf, it);
       }
     }
     else push_tile_bulk<false>(tl, shard, 0.0f, arena, W, stage_buf, it);
   }
-  if (acc) run.flush(acc);
   if (threadIdx.x == 0) bulk_wait0();                 // every bulk store has completed
   __syncthreads();
   __threadfence_system();
@@ -854,8 +886,10 @@ cudaError_t launch_unshard_push(const Tile* tiles, int ntiles, const float* shar
   for (int i = 0; i < W; ++i) rot.p[i] = arena.p[(rank + 1 + i) % W];
   const int g = grid_for(ntiles, cfg, fsdpk::kCtasPush);
   if (cfg.variant & 4)   // TMA bulk push
-    return launch_p(cfg.pdl, k_unshard_push_bulk, g, 0, st, tiles, ntiles, shard, scales, rot, W, amax_acc);
-  return launch_p(cfg.pdl, k_unshard_push, g, 0, st, tiles, ntiles, shard, scales, rot, W, rank, amax_acc);
+    return amax_acc ? launch_p(cfg.pdl, k_unshard_push_bulk<true>, g, 0, st, tiles, ntiles, shard, scales, rot, W, amax_acc)
+                    : launch_p(cfg.pdl, k_unshard_push_bulk<false>, g, 0, st, tiles, ntiles, shard, scales, rot, W, amax_acc);
+  return amax_acc ? launch_p(cfg.pdl, k_unshard_push<true>, g, 0, st, tiles, ntiles, shard, scales, rot, W, rank, amax_acc)
+                  : launch_p(cfg.pdl, k_unshard_push<false>, g, 0, st, tiles, ntiles, shard, scales, rot, W, rank, amax_acc);
 }
 
 cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool grad_bf16, int divisor, float* grad, bool mean,

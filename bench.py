@@ -43,7 +43,7 @@ NVLINK_MEASURED_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.
 HBM_NOMINAL_GBS = 8000.0     # "~8 TB/s" (BASELINE.json north_star)
 
 
-def wire_report(wire_rank, ms, ms_iso, W, R):
+def wire_report(wire_rank, ms, ms_iso, W, R, hsdp_wp=False):
     """Physical NVLink bytes per rank per direction per step / step time, vs 900 and 770."""
     if not wire_rank:
         return None
@@ -55,7 +55,9 @@ def wire_report(wire_rank, ms, ms_iso, W, R):
             "isolated_GBps_per_direction": round(gi, 1), "isolated_frac_of_900": round(gi / NVLINK_GBS, 4),
             "isolated_frac_of_770": round(gi / NVLINK_MEASURED_GBS, 4),
             "model": "P2P: (W-1) x own cast rows (push) + (W-1) x own bf16 grad rows (reduce-scatter); "
-                     "NCCL ring: (W-1) x slot + (W-1) x 4S" + ("; + fp32 replica all-reduce" if R > 1 else "")}
+                     "NCCL ring: (W-1) x slot + (W-1) x 4S" + (
+                         "; HSDP world pull: (R W - 1) x own bf16 grad rows instead of the shard-group RS"
+                         if hsdp_wp else ("; + fp32 replica all-reduce" if R > 1 else ""))}
 
 
 def parse():
@@ -186,6 +188,10 @@ def run_ours(args):
     algo = mesh.algo if N > 1 else "local (W=1: identity collectives)"
     if N > 1 and mesh.algo == "p2p":
         algo += f" (reduce-scatter: {mesh.p2p_rs})"
+    hsdp_wp = N > 1 and mesh.replicate_size > 1 and mesh.hsdp_rs == "world_pull"
+    if N > 1 and mesh.replicate_size > 1:
+        algo += f"; HSDP {mesh.replicate_size}x{mesh.shard_size} reduce-scatter: " + \
+            ("world pull (one kernel over all ranks, nested order)" if hsdp_wp else "shard-group RS + NCCL all-reduce")
     wl = WORKLOADS[args.workload]
     units = unit_lists(wl["model"])
     if wl["cycle"]:   # 70B: cycle `cycle` distinct block instances (memory), SURVEY.md §8(d) row 4
@@ -195,8 +201,8 @@ def run_ours(args):
     # ---- setup: shard (synthetic seeded params written straight into the shards)
     layers, grads = [], []
     gen = torch.Generator(device=dev).manual_seed(241006511 + rank)
-    lib_grads = args.grads == "library" or (args.grads == "auto" and N > 1 and mesh.algo == "p2p"
-                                             and mesh.p2p_rs != "store")   # store mode reads any grads
+    lib_grads = args.grads == "library" or (args.grads == "auto" and N > 1 and (
+        hsdp_wp or (mesh.algo == "p2p" and mesh.p2p_rs != "store")))   # store mode reads any grads
     for ui, (shapes, elig) in enumerate(units):
         l = F.fsdp_shard(mesh, None, elig, shapes=shapes)
         flat = l.sharded_flat()
@@ -310,7 +316,8 @@ def run_ours(args):
     # rank's cast rows into W-1 peers; the reduce-scatter moves this rank's bf16 grad rows of
     # every peer's chunk (store) / every peer's rows of this rank's chunk (pull), (W-1) x own
     # rows x 2 B either way.  NCCL ring: (W-1) x slot bytes (AG) + (W-1) x 4S (fp32 RS).
-    # HSDP adds the fp32 replica all-reduce (NCCL ring, 2 (R-1)/R x 4S).
+    # HSDP adds the fp32 replica all-reduce (NCCL ring, 2 (R-1)/R x 4S); the HSDP world pull
+    # instead reads this rank's bf16 rows from all R W - 1 other ranks, (R W - 1) x own x 2 B.
     R = mesh.replicate_size if N > 1 else 1
 
     def wire_unit(l, k):
@@ -319,11 +326,17 @@ def run_ours(args):
         own = [m["row_count"] * m["rest"] for m in l.metas]
         if N > 1 and mesh.algo == "p2p":
             es = [1 if (wl["fp8"] and e) else 2 for e in l.fp8_eligible]
-            b = k * (W - 1) * sum(o * s for o, s in zip(own, es)) + (W - 1) * 2 * sum(own)
+            b = k * (W - 1) * sum(o * s for o, s in zip(own, es))
         else:
             sb = l.S_bytes_fp8 if wl["fp8"] else 2 * l.S
-            b = k * (W - 1) * sb + (W - 1) * 4 * l.S
-        if R > 1:
+            b = k * (W - 1) * sb
+        if hsdp_wp:
+            b += (R * W - 1) * 2 * sum(own)
+        elif N > 1 and mesh.algo == "p2p":
+            b += (W - 1) * 2 * sum(own)
+        else:
+            b += (W - 1) * 4 * l.S
+        if R > 1 and not hsdp_wp:
             b += 2 * (R - 1) * 4 * l.S // R
         return b
     wire_rank = sum(wire_unit(l, k) for k, l in zip(n_unshard, layers))
@@ -512,6 +525,22 @@ def run_ours(args):
             traffic = json.load(open(tfile)).get(f"{args.workload}/w{N}", {}).get(dom)
         except Exception:
             traffic = None
+    traffic_src = "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch (profiles/ncu_traffic.json)" \
+        if traffic is not None else None
+    if traffic is None and bound == "nvlink":
+        # NVLink wire bytes: ncu nvltx / nvlrx user-payload bytes per launch of the same kernel
+        # on the 8B block at this W, as a ratio to its algorithmic bytes (profiles/round2)
+        try:
+            wire = json.load(open(os.path.join(ROOT, "profiles", "round2", "nvlink_wire.json")))
+            kname = {"unshard_push": "k_unshard_push_bulk", "rs_pull": "k_rs_pull_bulk",
+                     "rs_scatter": "k_rs_scatter"}[dom]
+            ent = wire[f"W{W}"][kname]
+            traffic = int(round(per_launch_bytes * ent["ratio"]))
+            traffic_src = (f"NVLink wire bytes: ncu {'nvlrx' if dom == 'rs_pull' else 'nvltx'}__bytes_data_user.sum / "
+                           f"algorithmic = {ent['ratio']} for {kname} at W={W} (profiles/round2/nvlink_wire.json) "
+                           "x this line's algorithmic bytes per launch")
+        except (OSError, KeyError, ValueError):
+            traffic = None
     gpu_launches = sum(prof_step[k]["launches"] for k in ours)
     # whole-step HBM efficiency of our kernels in the timed step (sum of their algorithmic
     # HBM bytes / step time), meaningful where no NVLink kernel runs (W = 1)
@@ -550,7 +579,7 @@ def run_ours(args):
                          "busbw_frac_nvlink_900": round(busbw_rank / NVLINK_GBS, 4),
                          "busbw_note": "metric units: counts the paper's fp32 reduce-scatter bytes; the P2P "
                                        "path sends bf16 grads (DESIGN.md R14), so see `wire` for the link rate"},
-            "wire": wire_report(wire_rank, ms_max, ms_iso, W, R),
+            "wire": wire_report(wire_rank, ms_max, ms_iso, W, R, hsdp_wp),
             "isolated": {"ms_per_step": round(ms_iso, 4), "steps": roof_steps,
                          "value": round(N * bytes_rank / (ms_iso * 1e-3) / 1e9, 2),
                          "what": "same step with every unit's unshard and reduce-scatter issued serially (no "
@@ -560,7 +589,7 @@ def run_ours(args):
             "kernels_serial": kernels_serial,
             "roofline": {"bound": bound, "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
-                         "bytes_per_launch": int(per_launch_bytes), "traffic": traffic,
+                         "bytes_per_launch": int(per_launch_bytes), "traffic": traffic, "traffic_source": traffic_src,
                          "sm_mechanism_ceiling": mech,
                          "frac_of_nominal": round(achieved / (NVLINK_GBS if bound == "nvlink" else HBM_NOMINAL_GBS), 4),
                          "nominal_peak": NVLINK_GBS if bound == "nvlink" else HBM_NOMINAL_GBS,

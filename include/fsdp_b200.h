@@ -183,13 +183,23 @@ fsdp_status_t fsdp_mesh_init_local(int32_t world_size, int32_t rank, int32_t cud
  * world_size (mean over all ranks), reduce-scatters within the shard group
  * and all-reduces (sum, fp32, NCCL) across the replica group ("the addition of backward
  * gradient allreduce across replica groups").  Collective over all world_size
- * ranks; shard_size must divide world_size; shard_size == world_size is plain FSDP. */
+ * ranks; shard_size must divide world_size; shard_size == world_size is plain FSDP.
+ * One NVSwitch domain (world_size <= 8, every rank maps every rank's memory, checked
+ * collectively here): the reduce-scatter is ONE pull over the world instead — each rank
+ * reads its shard rows of all world_size ranks' grads and sums them in the same nested
+ * order (shard ranks ascending within a replica, then the replica partials ascending, fp32:
+ * the oracle's HsdpWorld 'order', bit for bit) with no serial replica all-reduce, and
+ * fsdp_full_grad_buffer maps its zero-copy grad buffers over the whole world.
+ * FSDP_B200_HSDP_P2P=0 (at init) or fsdp_mesh_set_algo(FSDP_ALGO_NCCL) keeps the
+ * reduce-scatter + NCCL all-reduce pair; fsdp_mesh_get_hsdp_rs tells which runs. */
 fsdp_status_t fsdp_mesh_init_hsdp(const uint8_t id[FSDP_UNIQUE_ID_BYTES], int32_t world_size,
                                   int32_t rank, int32_t shard_size, int32_t cuda_device,
                                   fsdp_mesh_t** out);
 /* replicate_size and this rank's replica index (1 and 0 for a 1-D mesh). */
 fsdp_status_t fsdp_mesh_info_hsdp(const fsdp_mesh_t* mesh, int32_t* replicate_size,
                                   int32_t* replica_index);
+/* *world_pull = 1 when the HSDP reduce-scatter runs as the one-domain world pull above. */
+fsdp_status_t fsdp_mesh_get_hsdp_rs(const fsdp_mesh_t* mesh, int32_t* world_pull);
 
 /* Destroys the mesh (synchronizes its streams, frees its pools, destroys the comms).
  * All layers of the mesh must have been destroyed. */
@@ -207,7 +217,9 @@ fsdp_status_t fsdp_mesh_memory(const fsdp_mesh_t* mesh, int64_t out[4]);
  * same call at the same point, with no layer unsharded / reduce-scatter pending.  The
  * default after fsdp_mesh_init is FSDP_ALGO_P2P when W > 1, W <= 8 and every rank could
  * map its peers' buffers (environment FSDP_B200_ALGO=nccl|p2p overrides), else NCCL.
- * FSDP_ERR_UNAVAILABLE if P2P is requested but not possible. */
+ * FSDP_ERR_UNAVAILABLE if P2P is requested but not possible.  On an HSDP mesh the choice
+ * also selects the reduce-scatter (P2P: the world pull when available); with shard_size 1
+ * P2P only switches that on (the unshard is local). */
 fsdp_status_t fsdp_mesh_set_algo(fsdp_mesh_t* mesh, int32_t algo);
 fsdp_status_t fsdp_mesh_get_algo(const fsdp_mesh_t* mesh, int32_t* algo);
 
@@ -319,7 +331,10 @@ fsdp_status_t fsdp_precompute_fp8_scales_delayed(fsdp_mesh_t* mesh, fsdp_layer_t
  * environment FSDP_B200_REGISTRY_CAP) and is never reallocated, so views taken here and
  * kernel arguments captured in CUDA graphs never dangle; fsdp_shard returns
  * FSDP_ERR_UNAVAILABLE when the registry is full.  Entries are assigned in fsdp_shard order
- * and recycled only once every layer of the mesh has been destroyed. */
+ * and recycled only once every layer of the mesh has been destroyed.
+ * Deliberate extension of SURVEY §8(b)'s `fsdp_fp8_scales(layer, scales)`: amax_dev (may
+ * be NULL) also exposes the all-reduced amax the scales were taken from, so callers and
+ * tests can check the scale formula without recomputing the amax. */
 fsdp_status_t fsdp_fp8_scales(const fsdp_layer_t* layer, const float** scales_dev,
                               const float** amax_dev);
 
@@ -378,7 +393,10 @@ fsdp_status_t fsdp_wait_reduce_scatter(fsdp_layer_t* layer, void* compute);
  * for another grad_dtype. */
 fsdp_status_t fsdp_full_grad_buffer(fsdp_layer_t* layer, fsdp_dtype_t grad_dtype, int32_t p, void** dev);
 /* fp32 sharded grad of param p: (*dev)[0 .. row_count*rest) (views into the layer's
- * grad buffer, same flat layout as the shard). */
+ * grad buffer, same flat layout as the shard).  Deliberate narrowing of SURVEY §8(b)'s
+ * `(void** dev, fsdp_dtype_t* dt)`: the sharded grad is always fp32 here (reduce_dtype
+ * BFLOAT16 only changes the reduction's rounding, R11, and the result is widened into the
+ * fp32 grad), so the pointer is typed and no dtype is returned. */
 fsdp_status_t fsdp_sharded_grad(const fsdp_layer_t* layer, int32_t p, float** dev);
 fsdp_status_t fsdp_sharded_grad_flat(const fsdp_layer_t* layer, float** dev);
 fsdp_status_t fsdp_zero_grad(fsdp_layer_t* layer, void* stream);
@@ -438,6 +456,16 @@ fsdp_status_t fsdp_stage_grads_to_staging(const fsdp_layer_t* layer, const void*
 fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* layer, const void* const* stagings_dev,
                                  fsdp_dtype_t grad_dtype, fsdp_dtype_t reduce_dtype, int32_t mean,
                                  int32_t accumulate, void* stream);
+/* HSDP world pull (header of fsdp_mesh_init_hsdp): for this rank's rows (shard rank
+ * = the layer's rank, W = its shard group), grad (+)= sum over replicas r = 0..replicate-1
+ * ascending of ( sum over shard ranks q = 0..W-1 ascending of fp32(stagings_dev[r*W+q]) /
+ * (replicate*W) ), both sums fp32 (the oracle's HsdpWorld 'order').  stagings_dev: one
+ * staging per global rank g = r*W + q, laid out as fsdp_grad_staging_layout, 16-byte
+ * aligned.  replicate * W <= 8; replicate must equal the mesh's replicate size unless the
+ * mesh is 1-D (a local mesh emulating one shard rank). */
+fsdp_status_t fsdp_stage_rs_pull_hsdp(fsdp_layer_t* layer, const void* const* stagings_dev, int32_t replicate,
+                                      fsdp_dtype_t grad_dtype, fsdp_dtype_t reduce_dtype, int32_t mean,
+                                      int32_t accumulate, void* stream);
 /* Store-based reduce-scatter (FSDP_P2P_RS_STORE), sender: for every rank r, this rank's
  * full-grad rows of r's Shard(0) chunk of each param are copied into r's receive buffer
  * recv_dev[r] at slot `rank`: recv_r[(rank * S + off_p) + j] (grad_dtype elements; a receive

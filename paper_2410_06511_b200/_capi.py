@@ -106,6 +106,8 @@ SIGNATURES = {
     "fsdp_grad_staging_layout": [_VP, C.POINTER(_I64), C.POINTER(_I64)],
     "fsdp_stage_grads_to_staging": [_VP, _PP, _I32, _VP, _VP],
     "fsdp_stage_rs_pull": [_VP, _PP, _I32, _I32, _I32, _I32, _VP],
+    "fsdp_stage_rs_pull_hsdp": [_VP, _PP, _I32, _I32, _I32, _I32, _I32, _VP],
+    "fsdp_mesh_get_hsdp_rs": [_VP, C.POINTER(_I32)],
     "fsdp_mesh_memory": [_VP, C.POINTER(_I64)],
     "fsdp_stage_rs_scatter": [_VP, _PP, _I32, _PP, _I32, _VP],
     "fsdp_stage_rs_recv_reduce": [_VP, _VP, _PP, _I32, _I32, _I32, _I32, _VP],

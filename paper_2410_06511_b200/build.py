@@ -35,31 +35,56 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(INCLUDE, "fsdp_b200.h"), __file__]
+    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+        [os.path.join(INCLUDE, "fsdp_b200.h"), __file__]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compiles every source to an object in parallel (one nvcc per file), then links."""
     if not force and not _stale():
         return LIB
     inc, lib = nccl_dirs()
     import time
+    from concurrent.futures import ThreadPoolExecutor
     t_start = time.time()   # the library is stamped with this: sources edited during the build stay newer
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC",
-           "-prec-div=true", "-prec-sqrt=true", "-ftz=false", "-Xptxas", "-v",
-           *os.environ.get("FSDP_B200_NVCC_EXTRA", "").split(),   # experiments only (e.g. -D...)
-           "-I", INCLUDE, "-I", CSRC, "-I", inc, *sources(),
-           "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}", "-o", tmp]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = os.path.join(HERE, ".obj")
+    os.makedirs(objdir, exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-prec-div=true", "-prec-sqrt=true", "-ftz=false", "-Xptxas", "-v",
+             *os.environ.get("FSDP_B200_NVCC_EXTRA", "").split(),   # experiments only (e.g. -D...)
+             "-I", INCLUDE, "-I", CSRC, "-I", inc]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *flags, "-c", src, "-o", obj]
+        return obj, cmd, subprocess.run(cmd, capture_output=True, text=True)
+
+    srcs = sources()
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, srcs))
+    link = [NVCC, *ARCH, "--shared", "-Xcompiler", "-fPIC", *[o for o, _, _ in results],
+            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}", "-o", tmp]
+    res_link = None
+    if all(r.returncode == 0 for _, _, r in results):
+        res_link = subprocess.run(link, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
+        for _, cmd, r in results:
+            f.write(" ".join(cmd) + "\n\n" + r.stdout + r.stderr + "\n")
+        if res_link is not None:
+            f.write(" ".join(link) + "\n\n" + res_link.stdout + res_link.stderr)
+    if res_link is None or res_link.returncode != 0:
+        for _, _, r in results:
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+        if res_link is not None:
+            sys.stderr.write(res_link.stdout + res_link.stderr)
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
-        sys.stdout.write(res.stderr)
+        for _, _, r in results:
+            sys.stdout.write(r.stderr)
     os.replace(tmp, LIB)
     os.utime(LIB, (t_start, t_start))
     return LIB

@@ -209,7 +209,12 @@ struct SymBuf {
   void* local = nullptr;
   size_t bytes = 0;
   std::vector<void*> peers;   // peers[r] = rank r's buffer in this process (peers[rank] = local)
+  int grp = 0;                // the group it is symmetric over: GRP_SHARD or GRP_WORLD (HSDP)
 };
+
+// Groups a symmetric buffer / handshake spans: the Shard(0) group (FSDP, and the HSDP
+// unshard), or the whole world (the HSDP reduce-scatter pull on one NVSwitch domain).
+enum GroupKind { GRP_SHARD = 0, GRP_WORLD = 1 };
 
 // A pooled symmetric slot of the P2P path (unsharded arena, or grad staging).  Slots are
 // chosen deterministically (same choice on every rank) and each use bumps the epoch the
@@ -295,6 +300,15 @@ struct fsdp_mesh {
   bool store_own_direct = true;              // store RS: own rows read from the caller's grads (FSDP_B200_STORE_OWN=0: own slot)
   bool p2p_ok = false;
   SymBuf flags;                              // uint64 [FK_NUM][kFlagSlots][kMaxRanks]
+  // HSDP on one NVSwitch domain (R > 1, R * W <= 8, every rank maps every rank): the
+  // reduce-scatter pulls this rank's shard rows from all R * W ranks and sums them in the
+  // oracle's nested order (shard ranks, then replicas) — no separate replica all-reduce.
+  // World-group symmetric memory: its own flags, epochs, staging pool.
+  bool hsdp_p2p = false;                     // capability (collective check at init)
+  bool hsdp_rs_p2p = false;                  // in use (FSDP_B200_HSDP_P2P=0 / set_algo(NCCL): off)
+  SymBuf wflags;
+  std::vector<SymSlot*> p2p_wrs;             // world grad staging
+  unsigned long long* d_wepochs = nullptr;
   std::vector<SymSlot*> p2p_ag, p2p_rs;      // unsharded arenas, grad staging
   uint64_t rs_rr = 0;                        // round robin over staging slots
   int gbuf_seq = 0;                          // flag slots of layer grad buffers: kPoolSlots + seq
@@ -374,15 +388,22 @@ int registry_reserve(fsdp_mesh* m, int n);
 void registry_ensure_hist(fsdp_mesh* m);
 void clear_presets(fsdp_mesh* m);
 int64_t dtype_size(fsdp_dtype_t d);
-void mesh_barrier(fsdp_mesh* m);
-bool mesh_all_ok(fsdp_mesh* m, bool ok);
+// a group: its communicator, size and this rank's index in it
+struct Group {
+  ncclComm_t comm;
+  int W, rank;
+};
+Group group_of(const fsdp_mesh* m, int grp);
+void mesh_barrier(fsdp_mesh* m, int grp = GRP_SHARD);
+bool mesh_all_ok(fsdp_mesh* m, bool ok, int grp = GRP_SHARD);
 void sym_free_local(fsdp_mesh* m, SymBuf& b);
-void sym_free(fsdp_mesh* m, SymBuf& b);
-bool sym_alloc(fsdp_mesh* m, SymBuf& b, size_t bytes);
-fsdpp::FlagPtrs flag_remote(fsdp_mesh* m, int kind, int slot);
-unsigned long long* flag_local(fsdp_mesh* m, int kind, int slot);
-unsigned long long* epoch_ctr(fsdp_mesh* m, int kind, int slot);
-SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t bytes, int prefer, const Capture& cap);
+void sym_free(fsdp_mesh* m, SymBuf& b);   // collective over b.grp
+bool sym_alloc(fsdp_mesh* m, SymBuf& b, size_t bytes, int grp = GRP_SHARD);
+fsdpp::FlagPtrs flag_remote(fsdp_mesh* m, int kind, int slot, int grp = GRP_SHARD);
+unsigned long long* flag_local(fsdp_mesh* m, int kind, int slot, int grp = GRP_SHARD);
+unsigned long long* epoch_ctr(fsdp_mesh* m, int kind, int slot, int grp = GRP_SHARD);
+SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t bytes, int prefer, const Capture& cap,
+                          int grp = GRP_SHARD);
 void release_sym_slot(SymSlot* s, cudaStream_t last_user, const Capture& cap);
 fsdpp::PeerPtrs peer_ptrs(const fsdp_mesh* m, const SymBuf& b);
 void p2p_teardown(fsdp_mesh* m);

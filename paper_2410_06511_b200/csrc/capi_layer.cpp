@@ -534,7 +534,71 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
     // AUTO: with zero-copy buffers the pull needs no staging and one kernel less, so it wins
     // at W = 2 and for small units (the store's ~5% link-rate edge is worth less than its
     // extra kernel below ~64 MB of bus bytes, profiles/r16 alpha-B fits); else store
-    const bool zc_layer = l->gbuf && l->gbuf_sym;
+    if (hsdp && m->hsdp_rs_p2p) {
+      // HSDP on one NVSwitch domain (header: fsdp_mesh_init_hsdp): ONE pull over the
+      // world.  Every rank stages its full grads (zero copy when they live in the layer's
+      // world-symmetric grad buffer); after the world ready handshake this rank reads its
+      // shard rows from all R x W ranks, divides each by R W and sums them shard ranks first,
+      // then replicas (global rank order, R15) into its fp32 grad — the shard-group
+      // reduce-scatter and the replica all-reduce in one kernel, bit-exact to HsdpWorld
+      // 'order'.  Accumulation is the kernel's (g + sum), as the NCCL pair's temp + add.
+      const Group G = group_of(m, GRP_WORLD);
+      const int64_t gsz = dtype_size(gd);
+      const bool use_gbuf = l->gbuf && l->gbuf_sym && l->gbuf->buf.grp == GRP_WORLD && gd == l->gbuf_dtype;
+      bool zc = use_gbuf;
+      for (int p = 0; zc && p < l->P; ++p)
+        zc = l->L.numel[p] == 0 || grads[p] == (const void*)((uint8_t*)l->gbuf->buf.local + l->stg_off_el[p] * gsz);
+      SymSlot* ss = use_gbuf ? l->gbuf
+                             : acquire_sym_slot(m, m->p2p_wrs, (size_t)(l->stg_elems * gsz), (int)(m->rs_rr++ % 2), cap,
+                                                GRP_WORLD);
+      CUDA_CHECK(cudaEventRecord(l->ev_rcall, cs));
+      if (zc) {
+        CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, l->ev_rcall, 0));
+      } else {
+        CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, l->ev_rcall, 0));
+        wait_released(m->s_rsc, ss, cap);
+        {
+          const DevTiles& T = gd == FSDP_BFLOAT16 ? l->t_stage_bf16 : l->t_stage_fp32;
+          fsdpk::PtrArray pa{};
+          for (int p = 0; p < l->P; ++p) pa.p[p] = grads[p];
+          ProfScope pst(m, FSDP_PROF_STAGE_GRADS, m->s_rsc, 2 * l->grad_numel_total * gsz);
+          CUDA_CHECK(fsdpp::launch_gather_copy(T.d, T.n, pa, ss->buf.local, m->cfg, m->s_rsc));
+          pst.done();
+        }
+        CUDA_CHECK(cudaEventRecord(l->ev_k5, m->s_rsc));
+        CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, l->ev_k5, 0));
+      }
+      {
+        ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_rs, 0);
+        CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_READY, ss->index, GRP_WORLD),
+                                             flag_local(m, FK_RS_READY, ss->index, GRP_WORLD), G.W, G.rank,
+                                             epoch_ctr(m, FK_RS_READY, ss->index, GRP_WORLD), m->p2p_timeout_ns,
+                                             m->d_err, m->s_rs));
+        ph.done();
+      }
+      {
+        ProfScope pp(m, FSDP_PROF_RS_PULL, m->s_rs, (int64_t)(G.W - 1) * l->pull_elems * gsz);
+        fsdpk::LaunchCfg pcfg = m->cfg;
+        if (!zc) pcfg.variant &= ~2;   // bulk pull only without a concurrent staging copy (profiles/r06)
+        CUDA_CHECK(fsdpp::launch_rs_pull_nested(l->t_pull.d, l->t_pull.n, peer_ptrs(m, ss->buf), gd == FSDP_BFLOAT16,
+                                                divisor, l->grad, mean != 0, accumulate != 0, obf, G.W, m->W, pcfg,
+                                                m->s_rs));
+        pp.done();
+      }
+      {
+        ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_rs, 0);
+        CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_DONE, ss->index, GRP_WORLD),
+                                             flag_local(m, FK_RS_DONE, ss->index, GRP_WORLD), G.W, G.rank,
+                                             epoch_ctr(m, FK_RS_DONE, ss->index, GRP_WORLD), m->p2p_timeout_ns,
+                                             m->d_err, m->s_rs, m->cfg.pdl));
+        ph.done();
+      }
+      release_sym_slot(ss, m->s_rs, cap);
+      CUDA_CHECK(cudaEventRecord(l->ev_rs_done, m->s_rs));
+      l->rs_pending = true;
+      return;
+    }
+    const bool zc_layer = l->gbuf && l->gbuf_sym && l->gbuf->buf.grp == GRP_SHARD;
     const int64_t bus_bytes = l->stg_elems * dtype_size(gd) * (m->W - 1) / std::max(m->W, 1);
     const bool p2p_store = m->p2p_rs_mode == FSDP_P2P_RS_STORE ||
                            (m->p2p_rs_mode == FSDP_P2P_RS_AUTO &&
@@ -630,7 +694,7 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       // it depends only on collective state: a layer with a symmetric grad buffer of this
       // dtype always reduce-scatters through it — grads given elsewhere are staged INTO it
       // (a rank-local copy) — and a layer without one always uses the pooled staging.
-      const bool use_gbuf = l->gbuf && l->gbuf_sym && gd == l->gbuf_dtype;
+      const bool use_gbuf = l->gbuf && l->gbuf_sym && l->gbuf->buf.grp == GRP_SHARD && gd == l->gbuf_dtype;
       bool zc = use_gbuf;
       for (int p = 0; zc && p < l->P; ++p)
         zc = l->L.numel[p] == 0 || grads[p] == (const void*)((uint8_t*)l->gbuf->buf.local + l->stg_off_el[p] * gsz);
@@ -804,10 +868,12 @@ fsdp_status_t fsdp_full_grad_buffer(fsdp_layer_t* l, fsdp_dtype_t gd, int32_t p,
       auto* s = new SymSlot();
       s->free_ev = new_event();
       const size_t bytes = (size_t)std::max<int64_t>(l->stg_elems, 128) * gsz;
-      if (m->p2p_ok) {   // collective: every rank maps every peer's buffer
+      if (m->p2p_ok || m->hsdp_rs_p2p) {   // collective: every rank of the group maps every peer's buffer
         if (kPoolSlots + m->gbuf_seq >= kFlagSlots) fail(FSDP_ERR_UNAVAILABLE, "too many layer grad buffers");
         s->index = kPoolSlots + m->gbuf_seq++;
-        if (!sym_alloc(m, s->buf, bytes)) {
+        // HSDP world pull: the buffer is symmetric over the whole world (its reduce-scatter
+        // reads it from every replica); else over the shard group
+        if (!sym_alloc(m, s->buf, bytes, m->hsdp_rs_p2p ? GRP_WORLD : GRP_SHARD)) {
           cudaEventDestroy(s->free_ev);
           delete s;
           fail(FSDP_ERR_OUT_OF_MEMORY, "symmetric grad buffer allocation/mapping failed");

@@ -109,13 +109,28 @@ static void p2p_init(fsdp_mesh* m) {
   if (const char* e = std::getenv("FSDP_B200_STORE_OWN")) m->store_own_direct = std::atoi(e) != 0;
   if (const char* e = std::getenv("FSDP_B200_AMAX_FUSE")) m->amax_fuse = std::atoi(e) != 0;
   if (const char* e = std::getenv("FSDP_B200_CE")) m->ce = std::atoi(e) != 0;
-  if (m->local || m->W < 2 || m->W > 8) return;
+  if (m->local) return;
   const size_t fbytes = sizeof(unsigned long long) * FK_NUM * kFlagSlots * fsdpp::kMaxRanks;
-  m->p2p_ok = sym_alloc(m, m->flags, fbytes);
-  CUDA_CHECK(cudaMalloc(&m->d_epochs, sizeof(unsigned long long) * FK_NUM * kFlagSlots));
-  CUDA_CHECK(cudaMemset(m->d_epochs, 0, sizeof(unsigned long long) * FK_NUM * kFlagSlots));
+  const size_t ebytes = sizeof(unsigned long long) * FK_NUM * kFlagSlots;
   const char* env = std::getenv("FSDP_B200_ALGO");
   const bool want_nccl = env && std::string(env) == "nccl";
+  // HSDP on one NVSwitch domain: world-group symmetric memory for the reduce-scatter pull
+  // (collective over the world; the same decision on every rank: R, W and the environment)
+  if (m->R > 1 && m->W * m->R <= 8 && m->comm_world) {
+    const char* h = std::getenv("FSDP_B200_HSDP_P2P");
+    if (!(h && std::atoi(h) == 0)) {
+      m->hsdp_p2p = sym_alloc(m, m->wflags, fbytes, GRP_WORLD);
+      if (m->hsdp_p2p) {
+        CUDA_CHECK(cudaMalloc(&m->d_wepochs, ebytes));
+        CUDA_CHECK(cudaMemset(m->d_wepochs, 0, ebytes));
+      }
+      m->hsdp_rs_p2p = m->hsdp_p2p && !want_nccl;
+    }
+  }
+  if (m->W < 2 || m->W > 8) return;
+  m->p2p_ok = sym_alloc(m, m->flags, fbytes);
+  CUDA_CHECK(cudaMalloc(&m->d_epochs, ebytes));
+  CUDA_CHECK(cudaMemset(m->d_epochs, 0, ebytes));
   m->algo = (m->p2p_ok && !want_nccl) ? FSDP_ALGO_P2P : FSDP_ALGO_NCCL;
   if (const char* t = std::getenv("FSDP_B200_P2P_TIMEOUT_MS"))
     m->p2p_timeout_ns = (unsigned long long)std::max(1L, std::atol(t)) * 1000000ull;
@@ -194,6 +209,13 @@ fsdp_status_t fsdp_mesh_info_hsdp(const fsdp_mesh_t* m, int32_t* R, int32_t* rep
   });
 }
 
+fsdp_status_t fsdp_mesh_get_hsdp_rs(const fsdp_mesh_t* m, int32_t* world_pull) {
+  return guarded([&] {
+    if (!m || !world_pull) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL argument");
+    *world_pull = m->hsdp_rs_p2p ? 1 : 0;
+  });
+}
+
 fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
   return guarded([&] {
     if (!m) return;
@@ -214,6 +236,14 @@ fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
         pool->clear();
       }
       sym_free_local(m, m->flags);
+      for (SymSlot* s : m->p2p_wrs) {
+        sym_free_local(m, s->buf);
+        if (s->free_ev) cudaEventDestroy(s->free_ev);
+        if (s->cap_ev) cudaEventDestroy(s->cap_ev);
+        delete s;
+      }
+      m->p2p_wrs.clear();
+      sym_free_local(m, m->wflags);
     }
     for (auto* pool : {&m->ag_slots, &m->rs_slots})
       for (Slot* s : *pool) {
@@ -230,6 +260,7 @@ fsdp_status_t fsdp_mesh_destroy(fsdp_mesh_t* m) {
     if (m->h_err) cudaFreeHost(const_cast<int*>(m->h_err));
     cudaFree(m->d_barrier);
     cudaFree(m->d_epochs);
+    cudaFree(m->d_wepochs);
     if (m->ev_ce) cudaEventDestroy(m->ev_ce);
     if (m->ev_pre_call) cudaEventDestroy(m->ev_pre_call);
     if (m->ev_pre_done) cudaEventDestroy(m->ev_pre_done);
@@ -255,21 +286,26 @@ fsdp_status_t fsdp_mesh_info(const fsdp_mesh_t* m, int32_t* W, int32_t* rank, in
 fsdp_status_t fsdp_mesh_memory(const fsdp_mesh_t* m, int64_t out[4]) {
   return guarded([&] {
     if (!m || !out) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL argument");
-    int64_t sym = 0, pool = 0, layer = 0;
-    if (m->p2p_ok) sym += (int64_t)m->flags.bytes;
-    for (const auto* pl : {&m->p2p_ag, &m->p2p_rs})
-      for (const SymSlot* s : *pl) sym += (int64_t)s->buf.bytes;
+    int64_t sym = 0, pool = 0, layer = 0, peer = 0;
+    auto add_sym = [&](const SymBuf& b) {   // local bytes + the group's W-1 peer mappings
+      sym += (int64_t)b.bytes;
+      peer += (int64_t)b.bytes * std::max<int64_t>((int64_t)b.peers.size() - 1, 0);
+    };
+    if (m->p2p_ok) add_sym(m->flags);
+    if (m->hsdp_p2p) add_sym(m->wflags);
+    for (const auto* pl : {&m->p2p_ag, &m->p2p_rs, &m->p2p_wrs})
+      for (const SymSlot* s : *pl) add_sym(s->buf);
     for (const auto* pl : {&m->ag_slots, &m->rs_slots})
       for (const Slot* s : *pl) pool += (int64_t)(s->a.cap + s->b.cap);
     for (const fsdp_layer* l : m->layers) {
       layer += 2 * (int64_t)sizeof(float) * std::max<int64_t>(l->L.S, 16);   // fp32 shard + sharded grad
       if (l->gbuf) {
-        if (l->gbuf_sym) sym += (int64_t)l->gbuf->buf.bytes;
+        if (l->gbuf_sym) add_sym(l->gbuf->buf);
         else layer += (int64_t)l->gbuf->buf.bytes;
       }
     }
     out[0] = sym;                                       // symmetric buffers this rank allocated
-    out[1] = sym * (int64_t)std::max(m->W - 1, 0);      // the same buffers of W-1 peers, mapped
+    out[1] = peer;                                      // the same buffers of the group's peers, mapped
     out[2] = pool;                                      // NCCL-mode / W=1 pooled buffers
     out[3] = layer;                                     // per-layer fp32 shard + grad (+ plain grad buffers)
   });
@@ -293,8 +329,10 @@ fsdp_status_t fsdp_mesh_set_algo(fsdp_mesh_t* m, int32_t algo) {
     if (algo != FSDP_ALGO_NCCL && algo != FSDP_ALGO_P2P) fail(FSDP_ERR_INVALID_ARGUMENT, "unknown algo");
     for (auto* l : m->layers)
       if (l->state != SHARDED || l->rs_pending) fail(FSDP_ERR_STATE, "a layer is unsharded or has a pending reduce-scatter");
-    if (algo == FSDP_ALGO_P2P && !m->p2p_ok) fail(FSDP_ERR_UNAVAILABLE, "P2P needs 2 <= W <= 8 ranks whose GPUs can map each other's memory");
-    m->algo = algo;
+    if (algo == FSDP_ALGO_P2P && !m->p2p_ok && !m->hsdp_p2p)
+      fail(FSDP_ERR_UNAVAILABLE, "P2P needs 2 <= W <= 8 ranks whose GPUs can map each other's memory");
+    if (algo == FSDP_ALGO_NCCL || m->p2p_ok) m->algo = algo;   // W = 1 HSDP: the unshard stays local
+    m->hsdp_rs_p2p = algo == FSDP_ALGO_P2P && m->hsdp_p2p;
   });
 }
 

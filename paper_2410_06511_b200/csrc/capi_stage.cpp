@@ -197,6 +197,32 @@ fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* l, const void* const* stagings, f
   });
 }
 
+fsdp_status_t fsdp_stage_rs_pull_hsdp(fsdp_layer_t* l, const void* const* stagings, int32_t replicate, fsdp_dtype_t gd,
+                                      fsdp_dtype_t rd, int32_t mean, int32_t accumulate, void* stream) {
+  return guarded([&] {
+    check_layer(l);
+    fsdp_mesh* m = l->mesh;
+    if (replicate < 1) fail(FSDP_ERR_INVALID_ARGUMENT, "replicate must be >= 1");
+    if (m->R != 1 && m->R != replicate) fail(FSDP_ERR_INVALID_ARGUMENT, "replicate differs from the mesh's replicate size");
+    const int Wt = m->W * replicate;
+    if (Wt > 8) fail(FSDP_ERR_UNAVAILABLE, "the world pull supports replicate * W <= 8");
+    if (!stagings) fail(FSDP_ERR_INVALID_ARGUMENT, "stagings is NULL");
+    if (gd != FSDP_BFLOAT16 && gd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "grad_dtype must be BFLOAT16 or FLOAT32");
+    if (rd != FSDP_BFLOAT16 && rd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "reduce_dtype must be FLOAT32 or BFLOAT16");
+    fsdpp::PeerPtrs pp{};
+    for (int r = 0; r < Wt; ++r) {
+      if (!stagings[r]) fail(FSDP_ERR_INVALID_ARGUMENT, "stagings[g] is NULL");
+      check_align16(stagings[r], "stagings[g]");
+      pp.p[r] = (uint8_t*)stagings[r];
+    }
+    DeviceGuard g(m->device);
+    ProfScope ps(m, FSDP_PROF_RS_PULL, as_stream(stream), (int64_t)(Wt - 1) * l->pull_elems * dtype_size(gd));
+    CUDA_CHECK(fsdpp::launch_rs_pull_nested(l->t_pull.d, l->t_pull.n, pp, gd == FSDP_BFLOAT16, Wt, l->grad, mean != 0,
+                                            accumulate != 0, rd == FSDP_BFLOAT16, Wt, m->W, m->cfg, as_stream(stream)));
+    ps.done();
+  });
+}
+
 fsdp_status_t fsdp_stage_rs_scatter(const fsdp_layer_t* lc, const void* const* grads, fsdp_dtype_t gd,
                                     void* const* recv, int32_t include_self, void* stream) {
   return guarded([&] {

@@ -173,16 +173,23 @@ int64_t dtype_size(fsdp_dtype_t d) { return d == FSDP_FLOAT32 ? 4 : (d == FSDP_B
 
 // ---- symmetric memory over CUDA IPC (collective helpers; every rank calls them in the
 // same order, which the deterministic FSDP call sequence guarantees)
-void mesh_barrier(fsdp_mesh* m) {
-  NCCL_CHECK(ncclAllReduce(m->d_barrier, m->d_barrier, 1, ncclInt32, ncclSum, m->comm_ag, m->s_ag));
+Group group_of(const fsdp_mesh* m, int grp) {
+  if (grp == GRP_WORLD) return Group{m->comm_world, m->W * m->R, m->rep * m->W + m->rank};
+  return Group{m->comm_ag, m->W, m->rank};
+}
+
+void mesh_barrier(fsdp_mesh* m, int grp) {
+  const Group g = group_of(m, grp);
+  NCCL_CHECK(ncclAllReduce(m->d_barrier, m->d_barrier, 1, ncclInt32, ncclSum, g.comm, m->s_ag));
   CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
 }
 
-// all ranks agree that `ok` holds everywhere
-bool mesh_all_ok(fsdp_mesh* m, bool ok) {
+// all ranks of the group agree that `ok` holds everywhere
+bool mesh_all_ok(fsdp_mesh* m, bool ok, int grp) {
+  const Group g = group_of(m, grp);
   int v = ok ? 1 : 0;
   CUDA_CHECK(cudaMemcpy(m->d_barrier, &v, sizeof(int), cudaMemcpyHostToDevice));
-  NCCL_CHECK(ncclAllReduce(m->d_barrier, m->d_barrier, 1, ncclInt32, ncclMin, m->comm_ag, m->s_ag));
+  NCCL_CHECK(ncclAllReduce(m->d_barrier, m->d_barrier, 1, ncclInt32, ncclMin, g.comm, m->s_ag));
   CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
   CUDA_CHECK(cudaMemcpy(&v, m->d_barrier, sizeof(int), cudaMemcpyDeviceToHost));
   return v == 1;
@@ -190,74 +197,82 @@ bool mesh_all_ok(fsdp_mesh* m, bool ok) {
 
 // Rank-local (aborted mesh): unmap the peers' copies and free the local one, no barrier.
 void sym_free_local(fsdp_mesh* m, SymBuf& b) {
-  for (int r = 0; r < m->W; ++r)
-    if (r != m->rank && r < (int)b.peers.size() && b.peers[r]) cudaIpcCloseMemHandle(b.peers[r]);
+  const Group g = group_of(m, b.grp);
+  for (int r = 0; r < g.W; ++r)
+    if (r != g.rank && r < (int)b.peers.size() && b.peers[r]) cudaIpcCloseMemHandle(b.peers[r]);
   if (b.local) cudaFree(b.local);
   cudaGetLastError();
   b = SymBuf();
 }
 
-// Collective: unmap the peers' copies, wait until every rank did, then free the local one.
+// Collective over b's group: unmap the peers' copies, wait until every rank did, then free
+// the local one.
 void sym_free(fsdp_mesh* m, SymBuf& b) {
-  for (int r = 0; r < m->W; ++r)
-    if (r != m->rank && r < (int)b.peers.size() && b.peers[r]) cudaIpcCloseMemHandle(b.peers[r]);
+  const Group g = group_of(m, b.grp);
+  for (int r = 0; r < g.W; ++r)
+    if (r != g.rank && r < (int)b.peers.size() && b.peers[r]) cudaIpcCloseMemHandle(b.peers[r]);
   cudaGetLastError();
-  mesh_barrier(m);
+  mesh_barrier(m, b.grp);
   if (b.local) cudaFree(b.local);
   b = SymBuf();
 }
 
-// Returns false (on every rank) if any rank failed to allocate or map.
-bool sym_alloc(fsdp_mesh* m, SymBuf& b, size_t bytes) {
+// Returns false (on every rank of the group) if any rank failed to allocate or map.
+bool sym_alloc(fsdp_mesh* m, SymBuf& b, size_t bytes, int grp) {
+  const Group G = group_of(m, grp);
+  b.grp = grp;
   bool ok = cudaMalloc(&b.local, bytes + 256) == cudaSuccess;
   cudaIpcMemHandle_t h{};
   if (ok) ok = cudaMemset(b.local, 0, bytes + 256) == cudaSuccess;
   if (ok) ok = cudaIpcGetMemHandle(&h, b.local) == cudaSuccess;
   cudaGetLastError();
   uint8_t* d = nullptr;
-  CUDA_CHECK(cudaMalloc(&d, sizeof(h) * m->W));
-  CUDA_CHECK(cudaMemcpy(d + sizeof(h) * m->rank, &h, sizeof(h), cudaMemcpyHostToDevice));
-  NCCL_CHECK(ncclAllGather(d + sizeof(h) * m->rank, d, sizeof(h), ncclUint8, m->comm_ag, m->s_ag));
+  CUDA_CHECK(cudaMalloc(&d, sizeof(h) * G.W));
+  CUDA_CHECK(cudaMemcpy(d + sizeof(h) * G.rank, &h, sizeof(h), cudaMemcpyHostToDevice));
+  NCCL_CHECK(ncclAllGather(d + sizeof(h) * G.rank, d, sizeof(h), ncclUint8, G.comm, m->s_ag));
   CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
-  std::vector<cudaIpcMemHandle_t> hs(m->W);
-  CUDA_CHECK(cudaMemcpy(hs.data(), d, sizeof(h) * m->W, cudaMemcpyDeviceToHost));
+  std::vector<cudaIpcMemHandle_t> hs(G.W);
+  CUDA_CHECK(cudaMemcpy(hs.data(), d, sizeof(h) * G.W, cudaMemcpyDeviceToHost));
   cudaFree(d);
-  b.peers.assign(m->W, nullptr);
+  b.peers.assign(G.W, nullptr);
   b.bytes = bytes;
   if (ok) {
-    b.peers[m->rank] = b.local;
-    for (int r = 0; r < m->W && ok; ++r) {
-      if (r == m->rank) continue;
+    b.peers[G.rank] = b.local;
+    for (int r = 0; r < G.W && ok; ++r) {
+      if (r == G.rank) continue;
       void* p = nullptr;
       ok = cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
       cudaGetLastError();
       b.peers[r] = ok ? p : nullptr;
     }
   }
-  if (!mesh_all_ok(m, ok)) {
+  if (!mesh_all_ok(m, ok, grp)) {
     sym_free(m, b);
     return false;
   }
   return true;
 }
 
-fsdpp::FlagPtrs flag_remote(fsdp_mesh* m, int kind, int slot) {
+fsdpp::FlagPtrs flag_remote(fsdp_mesh* m, int kind, int slot, int grp) {
   fsdpp::FlagPtrs f{};
+  const SymBuf& fl = grp == GRP_WORLD ? m->wflags : m->flags;
   const size_t off = ((size_t)kind * kFlagSlots + slot) * fsdpp::kMaxRanks;
-  for (int r = 0; r < m->W; ++r) f.p[r] = (unsigned long long*)m->flags.peers[r] + off;
+  for (int r = 0; r < (int)fl.peers.size(); ++r) f.p[r] = (unsigned long long*)fl.peers[r] + off;
   return f;
 }
-unsigned long long* flag_local(fsdp_mesh* m, int kind, int slot) {
-  return (unsigned long long*)m->flags.local + ((size_t)kind * kFlagSlots + slot) * fsdpp::kMaxRanks;
+unsigned long long* flag_local(fsdp_mesh* m, int kind, int slot, int grp) {
+  const SymBuf& fl = grp == GRP_WORLD ? m->wflags : m->flags;
+  return (unsigned long long*)fl.local + ((size_t)kind * kFlagSlots + slot) * fsdpp::kMaxRanks;
 }
-unsigned long long* epoch_ctr(fsdp_mesh* m, int kind, int slot) {
-  return m->d_epochs + (size_t)kind * kFlagSlots + slot;
+unsigned long long* epoch_ctr(fsdp_mesh* m, int kind, int slot, int grp) {
+  return (grp == GRP_WORLD ? m->d_wepochs : m->d_epochs) + (size_t)kind * kFlagSlots + slot;
 }
 
 // Deterministic choice: the lowest-index free slot (same on every rank, since in_use
 // depends only on the call sequence); grows / creates slots collectively — except while
 // capturing a CUDA graph, where the pool must already be warm.
-SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t bytes, int prefer, const Capture& cap) {
+SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t bytes, int prefer, const Capture& cap,
+                          int grp) {
   if (cap.on) {
     SymSlot* s = nullptr;
     if (prefer >= 0 && prefer < (int)pool.size() && !pool[prefer]->in_use && pool[prefer]->buf.bytes >= bytes)
@@ -290,21 +305,34 @@ SymSlot* acquire_sym_slot(fsdp_mesh* m, std::vector<SymSlot*>& pool, size_t byte
   if (s->buf.bytes < bytes) {   // collective (re)allocation; setup-time only
     if (s->ever_used) CUDA_CHECK(cudaEventSynchronize(s->free_ev));
     CUDA_CHECK(cudaDeviceSynchronize());
-    mesh_barrier(m);
+    mesh_barrier(m, grp);
     if (s->buf.local || !s->buf.peers.empty()) sym_free(m, s->buf);
-    if (!sym_alloc(m, s->buf, bytes)) fail(FSDP_ERR_OUT_OF_MEMORY, "symmetric buffer allocation/mapping failed");
+    if (!sym_alloc(m, s->buf, bytes, grp)) fail(FSDP_ERR_OUT_OF_MEMORY, "symmetric buffer allocation/mapping failed");
   }
   s->in_use = true;
   return s;
 }
 
-fsdpp::PeerPtrs peer_ptrs(const fsdp_mesh* m, const SymBuf& b) {
+fsdpp::PeerPtrs peer_ptrs(const fsdp_mesh*, const SymBuf& b) {   // indexed by rank in b's group
   fsdpp::PeerPtrs p{};
-  for (int r = 0; r < m->W; ++r) p.p[r] = (uint8_t*)b.peers[r];
+  for (int r = 0; r < (int)b.peers.size(); ++r) p.p[r] = (uint8_t*)b.peers[r];
   return p;
 }
 
 void p2p_teardown(fsdp_mesh* m) {
+  if (m->hsdp_p2p) {   // world group first (its barrier covers every rank)
+    CUDA_CHECK(cudaDeviceSynchronize());
+    mesh_barrier(m, GRP_WORLD);
+    for (SymSlot* s : m->p2p_wrs) {
+      if (s->buf.local || !s->buf.peers.empty()) sym_free(m, s->buf);
+      if (s->free_ev) cudaEventDestroy(s->free_ev);
+      if (s->cap_ev) cudaEventDestroy(s->cap_ev);
+      delete s;
+    }
+    m->p2p_wrs.clear();
+    sym_free(m, m->wflags);
+    m->hsdp_p2p = m->hsdp_rs_p2p = false;
+  }
   if (!m->p2p_ok) return;
   CUDA_CHECK(cudaDeviceSynchronize());
   mesh_barrier(m);   // every rank's kernels are done with every peer buffer

@@ -55,6 +55,16 @@ cudaError_t launch_rs_pull(const fsdpk::Tile* tiles, int ntiles, PeerPtrs stagin
                            float* grad, bool mean, bool accumulate, bool bf16_reduce, int W,
                            fsdpk::LaunchCfg cfg, cudaStream_t st);
 
+// HSDP on one NVSwitch domain (hsdp_kernels.cu): the same pull over the W = R * G ranks of
+// the world, staging.p[g] = global rank g's staging (g = replica * G + shard rank), summed in
+// groups of G consecutive sources: grad[dst+e] (+)= round?( sum_{r<R} ( sum_{q<G}
+// fp32(stage_{r*G+q}[src+e]) / divisor ) ), both sums ascending fp32 (the
+// shard-group reduce-scatter, then the replica all-reduce; oracle HsdpWorld 'order').
+// G == W is launch_rs_pull.  Pairs with W <= 8 and G | W.
+cudaError_t launch_rs_pull_nested(const fsdpk::Tile* tiles, int ntiles, PeerPtrs staging, bool grad_bf16, int divisor,
+                                  float* grad, bool mean, bool accumulate, bool bf16_reduce, int W, int G,
+                                  fsdpk::LaunchCfg cfg, cudaStream_t st);
+
 // Gather copy: dst + tile.dst <- srcs.p[param] + tile.src, n bytes (any alignment).
 cudaError_t launch_gather_copy(const fsdpk::Tile* tiles, int ntiles, const fsdpk::PtrArray& srcs,
                                void* dst, fsdpk::LaunchCfg cfg, cudaStream_t st);

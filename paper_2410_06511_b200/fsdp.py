@@ -183,6 +183,14 @@ class Mesh:
         call("fsdp_mesh_set_algo", self.handle, capi.ALGO_P2P if algo == "p2p" else capi.ALGO_NCCL)
 
     @property
+    def hsdp_rs(self) -> str:
+        """HSDP reduce-scatter mechanism: 'world_pull' (one pull over all ranks of one NVSwitch
+        domain, nested-order sum) or 'rs+allreduce' (shard-group RS, then NCCL all-reduce)."""
+        a = C.c_int32()
+        call("fsdp_mesh_get_hsdp_rs", self.handle, C.byref(a))
+        return "world_pull" if a.value else "rs+allreduce"
+
+    @property
     def p2p_rs(self) -> str:
         a = C.c_int32()
         call("fsdp_mesh_get_p2p_rs", self.handle, C.byref(a))
@@ -497,6 +505,14 @@ def stage_grads_to_staging(layer: Layer, grads: Sequence[torch.Tensor], staging:
 def stage_rs_pull(layer: Layer, stagings: Sequence[torch.Tensor], grad_dtype, reduce_dtype=torch.float32,
                   mean: bool = True, accumulate: bool = False, stream=None):
     call("fsdp_stage_rs_pull", layer.handle, _ptr_array(stagings), _dtype_code(grad_dtype),
+         _dtype_code(reduce_dtype), int(bool(mean)), int(bool(accumulate)), _stream(stream))
+
+
+def stage_rs_pull_hsdp(layer: Layer, stagings: Sequence[torch.Tensor], replicate: int, grad_dtype,
+                       reduce_dtype=torch.float32, mean: bool = True, accumulate: bool = False, stream=None):
+    """HSDP world pull: stagings[g] = global rank g's staging (g = replica * W + shard rank);
+    grad (+)= sum over replicas of (sum over shard ranks of fp32(x) / (replicate * W))."""
+    call("fsdp_stage_rs_pull_hsdp", layer.handle, _ptr_array(stagings), int(replicate), _dtype_code(grad_dtype),
          _dtype_code(reduce_dtype), int(bool(mean)), int(bool(accumulate)), _stream(stream))
 
 

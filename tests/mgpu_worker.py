@@ -255,9 +255,12 @@ def run_hsdp_checks(W, rank, local, Ws):
     mesh = F.Mesh.from_process_group(device=local, shard_size=Ws)
     assert (mesh.replicate_size, mesh.shard_size) == (R, Ws)
     s = mesh.shard_rank
-    algos = ["p2p", "nccl"] if mesh.algo == "p2p" else ["nccl"]
+    world_pull = mesh.hsdp_rs == "world_pull"   # one NVSwitch domain: the default HSDP RS
+    algos = ["p2p", "nccl"] if (mesh.algo == "p2p" or world_pull) else ["nccl"]
     for algo in algos:
         mesh.set_algo(algo)
+        wp = algo == "p2p" and world_pull
+        assert (mesh.hsdp_rs == "world_pull") == wp
         for ui, u in enumerate([synth.model_units("toy")[0], synth.ragged_unit(5, world_size=Ws)]):
             shapes = [sh for _, sh, _ in u]
             elig = [e for _, _, e in u]
@@ -284,7 +287,11 @@ def run_hsdp_checks(W, rank, local, Ws):
                         got = layer.sharded_grad(p).cpu().numpy()
                         m = layer.metas[p]
                         prev = before[m["elem_offset"]:m["elem_offset"] + got.size].cpu().numpy().reshape(got.shape)
-                        if kind == "dyadic" and pow2(W):
+                        if wp:   # world pull: the oracle's nested order, bit for bit
+                            want = (prev + ref["order"][p]).astype(np.float32) if acc else ref["order"][p]
+                            np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32),
+                                                          err_msg=f"hsdp world pull {R}x{Ws} {ui} {kind} p{p} acc={acc}")
+                        elif kind == "dyadic" and pow2(W):
                             want = (prev + ref["exact"][p]).astype(np.float32) if acc else ref["exact"][p]
                             np.testing.assert_array_equal(got, want)
                         elif not acc:
@@ -306,8 +313,21 @@ def run_hsdp_checks(W, rank, local, Ws):
                 mg = ref["mag"][p].reshape(-1)
                 bound = (2 * W - 1) * 2.0 ** -8 * mg + 2.0 ** -24 * (np.abs(prev) + np.abs(ex)) + 2.0 ** -133
                 assert np.all(np.abs(got - prev - ex) <= bound), (algo, Ws, ui, p, "bf16+acc")
+            if wp:   # zero copy: grads written into the layer's world-symmetric grad buffers
+                G = [[synth.grad_bf16_bits(ui + 90, p, q, sh) for p, sh in enumerate(shapes)] for q in range(W)]
+                bufs = layer.full_grad_buffers(torch.bfloat16)
+                for b, x in zip(bufs, G[rank]):
+                    b.copy_(torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16))
+                ref = h.reduce_scatter_grads(G, BF16, True)[rank]
+                for rep in range(2):
+                    F.reduce_scatter_grads(layer, bufs)
+                    F.fsdp_wait_reduce_scatter(layer)
+                    for p in range(len(shapes)):
+                        got = layer.sharded_grad(p).cpu().numpy()
+                        np.testing.assert_array_equal(got.view(np.uint32), ref["order"][p].view(np.uint32),
+                                                      err_msg=f"hsdp world pull zero-copy {R}x{Ws} {ui} p{p} rep{rep}")
             layer.destroy()
-        print(f"rank {rank}/{W} hsdp {R}x{Ws} algo={algo}: OK", flush=True)
+        print(f"rank {rank}/{W} hsdp {R}x{Ws} algo={algo} rs={mesh.hsdp_rs}: OK", flush=True)
     mesh.synchronize(120000)
     mesh.destroy()
 

@@ -265,3 +265,22 @@ def test_hsdp_normal_data_bound():
             ok, ratio, _ = rs_error_ok(res[g]["order"][p].reshape(-1), res[g]["exact"][p].reshape(-1),
                                        res[g]["mag"][p].reshape(-1), 8)
             assert ratio <= 1.0
+
+
+def test_hsdp_order_is_nested_hand_example():
+    """The HSDP 'order' result is the shard-group sum (ascending shard rank) of each replica,
+    then the replica partials summed ascending (reduce-scatter in the shard
+    group, then the all-reduce across replicas; reading R15) — NOT the flat ascending sum
+    over all R*Ws ranks.  Hand example, R = Ws = 2, mean off, terms 1, 2^-25, -1, 2^-25 for
+    global ranks 0..3 (bf16-exact): nested (1 + 2^-25) + (-1 + 2^-25) = 1 + (-1) = 0 (each
+    add is a tie or below half an ulp and rounds to the even neighbour), flat
+    ((1 + 2^-25) - 1) + 2^-25 = 2^-25.  The device world pull is pinned to this oracle."""
+    shapes, elig = [(4, 16)], [False]
+    vals = [1.0, 2.0 ** -25, -1.0, 2.0 ** -25]
+    G = [[(np.full(shapes[0], np.float32(v)).view(np.uint32) >> 16).astype(np.uint16)] for v in vals]
+    res = HsdpWorld(shapes, 2, 2, elig).reduce_scatter_grads(G, BF16, False)
+    for g in range(4):
+        assert res[g]["order"][0].shape == (2, 16)
+        np.testing.assert_array_equal(res[g]["order"][0].view(np.uint32), np.zeros((2, 16), np.uint32))
+        # the exact sum is 2^-24 (= 2 * 2^-25), representable: 'exact' differs from 'order'
+        np.testing.assert_array_equal(res[g]["exact"][0], np.full((2, 16), np.float32(2.0 ** -24)))

@@ -56,7 +56,8 @@ def wire_report(wire_rank, ms, ms_iso, W, R, hsdp_wp=False):
             "isolated_frac_of_770": round(gi / NVLINK_MEASURED_GBS, 4),
             "model": "P2P: (W-1) x own cast rows (push) + (W-1) x own bf16 grad rows (reduce-scatter); "
                      "NCCL ring: (W-1) x slot + (W-1) x 4S" + (
-                         "; HSDP world pull: (R W - 1) x own bf16 grad rows instead of the shard-group RS"
+                         "; HSDP world RS: (R W - 1) x own bf16 grad rows (two-phase: / R, + (R-1) fp32 pieces "
+                         "of own / R) instead of the shard-group RS"
                          if hsdp_wp else ("; + fp32 replica all-reduce" if R > 1 else ""))}
 
 
@@ -188,10 +189,14 @@ def run_ours(args):
     algo = mesh.algo if N > 1 else "local (W=1: identity collectives)"
     if N > 1 and mesh.algo == "p2p":
         algo += f" (reduce-scatter: {mesh.p2p_rs})"
-    hsdp_wp = N > 1 and mesh.replicate_size > 1 and mesh.hsdp_rs == "world_pull"
-    if N > 1 and mesh.replicate_size > 1:
-        algo += f"; HSDP {mesh.replicate_size}x{mesh.shard_size} reduce-scatter: " + \
-            ("world pull (one kernel over all ranks, nested order)" if hsdp_wp else "shard-group RS + NCCL all-reduce")
+    hsdp_mode = mesh.hsdp_rs if N > 1 and mesh.replicate_size > 1 else None
+    hsdp_wp = hsdp_mode in ("world_pull", "world_pull_2phase")
+    hsdp_2ph = hsdp_mode == "world_pull_2phase"
+    if hsdp_mode:
+        algo += f"; HSDP {mesh.replicate_size}x{mesh.shard_size} reduce-scatter: " + {
+            "world_pull_2phase": "two-phase world RS (1/R pieces over all ranks + replica gather, nested order)",
+            "world_pull": "world pull (one kernel over all ranks, nested order)"}.get(hsdp_mode,
+                                                                                    "shard-group RS + NCCL all-reduce")
     wl = WORKLOADS[args.workload]
     units = unit_lists(wl["model"])
     if wl["cycle"]:   # 70B: cycle `cycle` distinct block instances (memory), SURVEY.md §8(d) row 4
@@ -330,7 +335,9 @@ def run_ours(args):
         else:
             sb = l.S_bytes_fp8 if wl["fp8"] else 2 * l.S
             b = k * (W - 1) * sb
-        if hsdp_wp:
+        if hsdp_2ph:   # pieces: (RW-1) x own/R bf16 rows in, then (R-1) fp32 pieces of own/R
+            b += (R * W - 1) * 2 * sum(own) // R + (R - 1) * 4 * sum(own) // R
+        elif hsdp_wp:
             b += (R * W - 1) * 2 * sum(own)
         elif N > 1 and mesh.algo == "p2p":
             b += (W - 1) * 2 * sum(own)
@@ -484,7 +491,7 @@ def run_ours(args):
     # the measured per-direction peer bandwidth (B200_PROFILING.md: 770 GB/s; 900 nominal).
     peak, peak_src = measured_peaks()
     hbm_k = ["copy_in", "copy_out", "rs_copy_in", "rs_copy_out", "amax", "scale", "stage_grads", "rs_reduce"]
-    nvl_k = ["unshard_push", "rs_pull", "rs_scatter"]
+    nvl_k = ["unshard_push", "rs_pull", "rs_scatter", "replica_gather"]
     ours = hbm_k + nvl_k + ["handshake"]
     dom = max(hbm_k + nvl_k, key=lambda k: prof[k]["ms"])
     d = prof[dom]

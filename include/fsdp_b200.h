@@ -54,7 +54,7 @@
 extern "C" {
 #endif
 
-#define FSDP_B200_ABI_VERSION 1
+#define FSDP_B200_ABI_VERSION 2   /* 2: FSDP_PROF_REPLICA_GATHER (profile arrays of 16) */
 #define FSDP_MAX_NDIM 8
 #define FSDP_UNIQUE_ID_BYTES 128
 
@@ -119,7 +119,8 @@ typedef enum {
   FSDP_PROF_HANDSHAKE = 12,    /* P2P: cross-GPU ready/done flag kernels       */
   FSDP_PROF_RS_SCATTER = 13,   /* P2P store RS: own grad rows -> peers' receive buffers (NVLink) */
   FSDP_PROF_RS_REDUCE = 14,    /* P2P store RS: local ascending-rank reduce of the receive buffer */
-  FSDP_PROF_NUM = 15
+  FSDP_PROF_REPLICA_GATHER = 15, /* HSDP two-phase RS: finished pieces from the replicas -> grad */
+  FSDP_PROF_NUM = 16
 } fsdp_prof_kind_t;
 
 /* How the collectives of a mesh run.
@@ -185,8 +186,10 @@ fsdp_status_t fsdp_mesh_init_local(int32_t world_size, int32_t rank, int32_t cud
  * gradient allreduce across replica groups").  Collective over all world_size
  * ranks; shard_size must divide world_size; shard_size == world_size is plain FSDP.
  * One NVSwitch domain (world_size <= 8, every rank maps every rank's memory, checked
- * collectively here): the reduce-scatter is ONE pull over the world instead — each rank
- * reads its shard rows of all world_size ranks' grads and sums them in the same nested
+ * collectively here): the reduce-scatter is a pull over the world instead (two-phase by
+ * default, fsdp_stage_hsdp_piece_pull / _replica_gather: each replica computes 1/R of the
+ * shard, then the replicas exchange the finished fp32 pieces) — each element is the sum of
+ * that shard row over all world_size ranks' grads in the same nested
  * order (shard ranks ascending within a replica, then the replica partials ascending, fp32:
  * the oracle's HsdpWorld 'order', bit for bit) with no serial replica all-reduce, and
  * fsdp_full_grad_buffer maps its zero-copy grad buffers over the whole world.
@@ -198,7 +201,8 @@ fsdp_status_t fsdp_mesh_init_hsdp(const uint8_t id[FSDP_UNIQUE_ID_BYTES], int32_
 /* replicate_size and this rank's replica index (1 and 0 for a 1-D mesh). */
 fsdp_status_t fsdp_mesh_info_hsdp(const fsdp_mesh_t* mesh, int32_t* replicate_size,
                                   int32_t* replica_index);
-/* *world_pull = 1 when the HSDP reduce-scatter runs as the one-domain world pull above. */
+/* *world_pull: 0 = shard-group reduce-scatter + NCCL all-reduce, 1 = the one-phase world
+ * pull above, 2 = the two-phase world reduce-scatter (pieces + replica gather, default). */
 fsdp_status_t fsdp_mesh_get_hsdp_rs(const fsdp_mesh_t* mesh, int32_t* world_pull);
 
 /* Destroys the mesh (synchronizes its streams, frees its pools, destroys the comms).
@@ -466,6 +470,19 @@ fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* layer, const void* const* staging
 fsdp_status_t fsdp_stage_rs_pull_hsdp(fsdp_layer_t* layer, const void* const* stagings_dev, int32_t replicate,
                                       fsdp_dtype_t grad_dtype, fsdp_dtype_t reduce_dtype, int32_t mean,
                                       int32_t accumulate, void* stream);
+/* HSDP two-phase reduce-scatter (the default world pull when R W > 3, where it moves fewer
+ * bytes; FSDP_B200_HSDP_RS=1 selects the one-phase pull above).  The shard's flat range [0, S) is cut into `replicate` pieces of
+ * P = round_up(ceil(S / replicate), 16) elements; piece q is computed by replica q.
+ * Phase 1: res_dev[j] (fp32, laid out like the sharded grad, 16-byte aligned) = the nested
+ * sum above for every real element j of piece `replica` (other entries untouched).
+ * Phase 2: for every real element j of every piece q, grad[j] (+)= res_devs[q][j], where
+ * res_devs[q] is replica q's phase-1 buffer (same shard rank).  Together: the world pull's
+ * bits with (RW-1) 2 S / R + (R-1) 4 S / R bytes read per rank instead of (RW-1) 2 S. */
+fsdp_status_t fsdp_stage_hsdp_piece_pull(fsdp_layer_t* layer, const void* const* stagings_dev, int32_t replicate,
+                                         int32_t replica, fsdp_dtype_t grad_dtype, fsdp_dtype_t reduce_dtype,
+                                         int32_t mean, float* res_dev, void* stream);
+fsdp_status_t fsdp_stage_hsdp_replica_gather(fsdp_layer_t* layer, const float* const* res_devs, int32_t replicate,
+                                             int32_t accumulate, void* stream);
 /* Store-based reduce-scatter (FSDP_P2P_RS_STORE), sender: for every rank r, this rank's
  * full-grad rows of r's Shard(0) chunk of each param are copied into r's receive buffer
  * recv_dev[r] at slot `rank`: recv_r[(rank * S + off_p) + j] (grad_dtype elements; a receive

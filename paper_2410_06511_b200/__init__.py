@@ -13,7 +13,8 @@ from .fsdp import (Mesh, Layer, layout_compute, get_unique_id, fsdp_shard, preco
                    reduce_scatter_grads, fsdp_wait_reduce_scatter, zero_grad, stage_copy_in,
                    stage_copy_out, stage_local_amax, stage_fp8_scale, stage_rs_copy_in,
                    stage_rs_copy_out, unsharded_layout, stage_unshard_push, grad_staging_layout,
-                   stage_grads_to_staging, stage_rs_pull, stage_rs_pull_hsdp, stage_rs_scatter,
+                   stage_grads_to_staging, stage_rs_pull, stage_rs_pull_hsdp, stage_hsdp_piece_pull,
+                   stage_hsdp_replica_gather, stage_rs_scatter,
                    stage_rs_recv_reduce)
 
 __all__ = ["Mesh", "Layer", "layout_compute", "get_unique_id", "fsdp_shard", "precompute_fp8_scales",
@@ -21,5 +22,6 @@ __all__ = ["Mesh", "Layer", "layout_compute", "get_unique_id", "fsdp_shard", "pr
            "reduce_scatter_grads", "fsdp_wait_reduce_scatter", "zero_grad", "stage_copy_in",
            "stage_copy_out", "stage_local_amax", "stage_fp8_scale", "stage_rs_copy_in",
            "stage_rs_copy_out", "unsharded_layout", "stage_unshard_push", "grad_staging_layout",
-           "stage_grads_to_staging", "stage_rs_pull", "stage_rs_pull_hsdp", "stage_rs_scatter",
+           "stage_grads_to_staging", "stage_rs_pull", "stage_rs_pull_hsdp", "stage_hsdp_piece_pull",
+           "stage_hsdp_replica_gather", "stage_rs_scatter",
            "stage_rs_recv_reduce", "FsdpError", "LIB_PATH"]

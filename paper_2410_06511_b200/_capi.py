@@ -22,7 +22,7 @@ STATUS = {0: "FSDP_OK", 1: "FSDP_ERR_INVALID_ARGUMENT", 2: "FSDP_ERR_SHAPE", 3: 
 
 PROF_KINDS = ["copy_in", "all_gather", "copy_out", "rs_copy_in", "reduce_scatter", "rs_copy_out",
               "amax", "scale", "all_reduce", "unshard_push", "rs_pull", "stage_grads", "handshake",
-              "rs_scatter", "rs_reduce"]
+              "rs_scatter", "rs_reduce", "replica_gather"]
 ALGO_NCCL, ALGO_P2P = 0, 1
 P2P_RS_PULL, P2P_RS_STORE, P2P_RS_AUTO = 0, 1, 2
 
@@ -37,7 +37,7 @@ class ParamMeta(C.Structure):
 
 
 class Profile(C.Structure):
-    _fields_ = [("launches", C.c_int64 * 15), ("total_ms", C.c_double * 15), ("bytes", C.c_int64 * 15)]
+    _fields_ = [("launches", C.c_int64 * 16), ("total_ms", C.c_double * 16), ("bytes", C.c_int64 * 16)]
 
 
 class FsdpError(RuntimeError):
@@ -108,6 +108,8 @@ SIGNATURES = {
     "fsdp_stage_rs_pull": [_VP, _PP, _I32, _I32, _I32, _I32, _VP],
     "fsdp_stage_rs_pull_hsdp": [_VP, _PP, _I32, _I32, _I32, _I32, _I32, _VP],
     "fsdp_mesh_get_hsdp_rs": [_VP, C.POINTER(_I32)],
+    "fsdp_stage_hsdp_piece_pull": [_VP, _PP, _I32, _I32, _I32, _I32, _I32, _VP, _VP],
+    "fsdp_stage_hsdp_replica_gather": [_VP, _PP, _I32, _I32, _VP],
     "fsdp_mesh_memory": [_VP, C.POINTER(_I64)],
     "fsdp_stage_rs_scatter": [_VP, _PP, _I32, _PP, _I32, _VP],
     "fsdp_stage_rs_recv_reduce": [_VP, _VP, _PP, _I32, _I32, _I32, _I32, _VP],

@@ -306,6 +306,7 @@ struct fsdp_mesh {
   // World-group symmetric memory: its own flags, epochs, staging pool.
   bool hsdp_p2p = false;                     // capability (collective check at init)
   bool hsdp_rs_p2p = false;                  // in use (FSDP_B200_HSDP_P2P=0 / set_algo(NCCL): off)
+  bool hsdp_two_phase = true;                // world RS of 1/R pieces + replica gather when R W > 3 (FSDP_B200_HSDP_RS=1: one pull)
   SymBuf wflags;
   std::vector<SymSlot*> p2p_wrs;             // world grad staging
   unsigned long long* d_wepochs = nullptr;
@@ -366,6 +367,11 @@ struct fsdp_layer {
   bool gbuf_sym = false;
   fsdp_dtype_t gbuf_dtype = FSDP_BFLOAT16;
   void* arena_base = nullptr;        // base of the unsharded tensors (either path)
+  // HSDP two-phase reduce-scatter (built on first use for a replicate size): t_piece[q] =
+  // the pull tiles of piece q of the shard, t_gather = all of them with tile.pad = q
+  int piece_R = 0;
+  std::vector<DevTiles> t_piece;
+  DevTiles t_gather;
   Allocator al;                      // made shard / grad / non-symmetric gbuf (mesh's at shard time)
 };
 
@@ -413,6 +419,12 @@ void launch_rs_copy_in_all(fsdp_layer* l, const void* const* grads, bool grad_bf
 int64_t cin_bytes(const fsdp_layer* l, bool fp8);
 int64_t slot_bytes(const fsdp_layer* l, bool fp8);
 void poll_async_errors(fsdp_mesh* m);
+// HSDP two-phase reduce-scatter: builds l->t_piece / l->t_gather for R pieces (once per R).
+void ensure_pieces(fsdp_layer* l, int R);
+// byte offset of the fp32 result region [S] in a world RS buffer (after the grad staging)
+inline int64_t hsdp_res_offset(const fsdp_layer* l, int64_t gsz) {
+  return ((std::max<int64_t>(l->stg_elems, 128) * gsz + 255) / 256) * 256;
+}
 // Marks the mesh aborted with a sticky reason and throws it (later calls re-report it).
 [[noreturn]] void abort_mesh(fsdp_mesh* m, fsdp_status_t st, const std::string& msg);
 // Copy-engine unshard (FSDP_B200_CE): cast this rank's rows into arenas.p[rank] one param at

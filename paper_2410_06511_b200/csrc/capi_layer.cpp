@@ -78,6 +78,7 @@ fsdp_status_t fsdp_shard(fsdp_mesh_t* m, int32_t n, const fsdp_param_desc_t* des
       l->t_recv_own.upload(fsdpl::tiles_recv_reduce_own(Ly));
       l->own_ok_bf16 = fsdpl::own_rows_aligned(Ly, 2);
       l->own_ok_fp32 = fsdpl::own_rows_aligned(Ly, 4);
+      if (m->hsdp_p2p) ensure_pieces(l, m->R);   // at shard time: no upload inside a graph capture
       for (int p = 0; p < n; ++p) {
         const int64_t cnt = Ly.metas[p].row_count * Ly.metas[p].rest;
         const int64_t es8 = Ly.fp8[p] ? 1 : 2;
@@ -134,6 +135,8 @@ fsdp_status_t fsdp_layer_destroy(fsdp_layer_t* l) {
     l->t_scatter_bf16.release(); l->t_scatter_fp32.release(); l->t_recv.release();
     l->t_scatter_peers_bf16.release(); l->t_scatter_peers_fp32.release(); l->t_recv_own.release();
     l->t_amax_reg.release();
+    for (auto& t : l->t_piece) t.release();
+    l->t_gather.release();
     if (l->gbuf) {
       if (l->gbuf_sym && !m->aborted) sym_free(m, l->gbuf->buf);   // collective
       else if (l->gbuf_sym) sym_free_local(m, l->gbuf->buf);
@@ -542,15 +545,24 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       // then replicas (global rank order, R15) into its fp32 grad — the shard-group
       // reduce-scatter and the replica all-reduce in one kernel, bit-exact to HsdpWorld
       // 'order'.  Accumulation is the kernel's (g + sum), as the NCCL pair's temp + add.
+      // Two-phase (default): replica q computes only piece q (1/R) of its shard rank's world
+      // sum into the fp32 result region of its world buffer, and after the done handshake
+      // every rank copies the R pieces from the R replicas of its shard rank into its grad:
+      // (RW-1) 2 S / R + (R-1) 4 S / R bytes in per rank instead of (RW-1) 2 S, same bits.
       const Group G = group_of(m, GRP_WORLD);
       const int64_t gsz = dtype_size(gd);
+      const int64_t res_off = hsdp_res_offset(l, gsz);
+      const size_t need2 = (size_t)(res_off + 4 * std::max<int64_t>(l->L.S, 16));
       const bool use_gbuf = l->gbuf && l->gbuf_sym && l->gbuf->buf.grp == GRP_WORLD && gd == l->gbuf_dtype;
+      // rank-consistent: the environment, and buffer sizes that are equal on every rank
+      const bool two_phase = m->hsdp_two_phase && (!use_gbuf || l->gbuf->buf.bytes >= need2);
       bool zc = use_gbuf;
       for (int p = 0; zc && p < l->P; ++p)
         zc = l->L.numel[p] == 0 || grads[p] == (const void*)((uint8_t*)l->gbuf->buf.local + l->stg_off_el[p] * gsz);
       SymSlot* ss = use_gbuf ? l->gbuf
-                             : acquire_sym_slot(m, m->p2p_wrs, (size_t)(l->stg_elems * gsz), (int)(m->rs_rr++ % 2), cap,
-                                                GRP_WORLD);
+                             : acquire_sym_slot(m, m->p2p_wrs, two_phase ? need2 : (size_t)(l->stg_elems * gsz),
+                                                (int)(m->rs_rr++ % 2), cap, GRP_WORLD);
+      if (two_phase) ensure_pieces(l, m->R);
       CUDA_CHECK(cudaEventRecord(l->ev_rcall, cs));
       if (zc) {
         CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, l->ev_rcall, 0));
@@ -577,12 +589,19 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
         ph.done();
       }
       {
-        ProfScope pp(m, FSDP_PROF_RS_PULL, m->s_rs, (int64_t)(G.W - 1) * l->pull_elems * gsz);
+        ProfScope pp(m, FSDP_PROF_RS_PULL, m->s_rs, (int64_t)(G.W - 1) * l->pull_elems * gsz / (two_phase ? m->R : 1));
         fsdpk::LaunchCfg pcfg = m->cfg;
         if (!zc) pcfg.variant &= ~2;   // bulk pull only without a concurrent staging copy (profiles/r06)
-        CUDA_CHECK(fsdpp::launch_rs_pull_nested(l->t_pull.d, l->t_pull.n, peer_ptrs(m, ss->buf), gd == FSDP_BFLOAT16,
-                                                divisor, l->grad, mean != 0, accumulate != 0, obf, G.W, m->W, pcfg,
-                                                m->s_rs));
+        if (two_phase) {
+          const DevTiles& T = l->t_piece[m->rep];
+          CUDA_CHECK(fsdpp::launch_rs_pull_nested(T.d, T.n, peer_ptrs(m, ss->buf), gd == FSDP_BFLOAT16, divisor,
+                                                  (float*)((uint8_t*)ss->buf.local + res_off), mean != 0, false, obf,
+                                                  G.W, m->W, pcfg, m->s_rs));
+        } else {
+          CUDA_CHECK(fsdpp::launch_rs_pull_nested(l->t_pull.d, l->t_pull.n, peer_ptrs(m, ss->buf), gd == FSDP_BFLOAT16,
+                                                  divisor, l->grad, mean != 0, accumulate != 0, obf, G.W, m->W, pcfg,
+                                                  m->s_rs));
+        }
         pp.done();
       }
       {
@@ -593,6 +612,16 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
                                              m->d_err, m->s_rs, m->cfg.pdl));
         ph.done();
       }
+      if (two_phase) {   // every piece is final on its replica (done handshake): gather them
+        fsdpp::PeerPtrs rp{};
+        for (int q = 0; q < m->R; ++q) rp.p[q] = (uint8_t*)ss->buf.peers[q * m->W + m->rank] + res_off;
+        ProfScope pg(m, FSDP_PROF_REPLICA_GATHER, m->s_rs, (int64_t)(m->R - 1) * 4 * l->pull_elems / m->R);
+        CUDA_CHECK(fsdpp::launch_replica_gather(l->t_gather.d, l->t_gather.n, rp, l->grad, accumulate != 0, m->cfg,
+                                                m->s_rs));
+        pg.done();
+      }
+      // the slot (staging + result pieces) is rewritten only after the next ready handshake
+      // of this slot, which every rank signals after its own gather has read the pieces
       release_sym_slot(ss, m->s_rs, cap);
       CUDA_CHECK(cudaEventRecord(l->ev_rs_done, m->s_rs));
       l->rs_pending = true;
@@ -867,7 +896,9 @@ fsdp_status_t fsdp_full_grad_buffer(fsdp_layer_t* l, fsdp_dtype_t gd, int32_t p,
       DeviceGuard g(m->device);
       auto* s = new SymSlot();
       s->free_ev = new_event();
-      const size_t bytes = (size_t)std::max<int64_t>(l->stg_elems, 128) * gsz;
+      size_t bytes = (size_t)std::max<int64_t>(l->stg_elems, 128) * gsz;
+      if (m->hsdp_rs_p2p)   // + the two-phase HSDP reduce-scatter's fp32 result region [S]
+        bytes = (size_t)(hsdp_res_offset(l, gsz) + 4 * std::max<int64_t>(l->L.S, 16));
       if (m->p2p_ok || m->hsdp_rs_p2p) {   // collective: every rank of the group maps every peer's buffer
         if (kPoolSlots + m->gbuf_seq >= kFlagSlots) fail(FSDP_ERR_UNAVAILABLE, "too many layer grad buffers");
         s->index = kPoolSlots + m->gbuf_seq++;

@@ -117,6 +117,9 @@ static void p2p_init(fsdp_mesh* m) {
   // HSDP on one NVSwitch domain: world-group symmetric memory for the reduce-scatter pull
   // (collective over the world; the same decision on every rank: R, W and the environment)
   if (m->R > 1 && m->W * m->R <= 8 && m->comm_world) {
+    // two-phase moves fewer bytes iff (RW-1) 2/R + (R-1) 4/R < (RW-1) 2, i.e. R W > 3
+    m->hsdp_two_phase = m->W * m->R > 3;
+    if (const char* e = std::getenv("FSDP_B200_HSDP_RS")) m->hsdp_two_phase = m->hsdp_two_phase && std::atoi(e) != 1;
     const char* h = std::getenv("FSDP_B200_HSDP_P2P");
     if (!(h && std::atoi(h) == 0)) {
       m->hsdp_p2p = sym_alloc(m, m->wflags, fbytes, GRP_WORLD);
@@ -212,7 +215,7 @@ fsdp_status_t fsdp_mesh_info_hsdp(const fsdp_mesh_t* m, int32_t* R, int32_t* rep
 fsdp_status_t fsdp_mesh_get_hsdp_rs(const fsdp_mesh_t* m, int32_t* world_pull) {
   return guarded([&] {
     if (!m || !world_pull) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL argument");
-    *world_pull = m->hsdp_rs_p2p ? 1 : 0;
+    *world_pull = m->hsdp_rs_p2p ? (m->hsdp_two_phase ? 2 : 1) : 0;
   });
 }
 

@@ -197,15 +197,20 @@ fsdp_status_t fsdp_stage_rs_pull(fsdp_layer_t* l, const void* const* stagings, f
   });
 }
 
+static void check_hsdp_stage(const fsdp_layer* l, int32_t replicate) {
+  const fsdp_mesh* m = l->mesh;
+  if (replicate < 1) fail(FSDP_ERR_INVALID_ARGUMENT, "replicate must be >= 1");
+  if (m->R != 1 && m->R != replicate) fail(FSDP_ERR_INVALID_ARGUMENT, "replicate differs from the mesh's replicate size");
+  if (m->W * replicate > 8) fail(FSDP_ERR_UNAVAILABLE, "the world pull supports replicate * W <= 8");
+}
+
 fsdp_status_t fsdp_stage_rs_pull_hsdp(fsdp_layer_t* l, const void* const* stagings, int32_t replicate, fsdp_dtype_t gd,
                                       fsdp_dtype_t rd, int32_t mean, int32_t accumulate, void* stream) {
   return guarded([&] {
     check_layer(l);
+    check_hsdp_stage(l, replicate);
     fsdp_mesh* m = l->mesh;
-    if (replicate < 1) fail(FSDP_ERR_INVALID_ARGUMENT, "replicate must be >= 1");
-    if (m->R != 1 && m->R != replicate) fail(FSDP_ERR_INVALID_ARGUMENT, "replicate differs from the mesh's replicate size");
     const int Wt = m->W * replicate;
-    if (Wt > 8) fail(FSDP_ERR_UNAVAILABLE, "the world pull supports replicate * W <= 8");
     if (!stagings) fail(FSDP_ERR_INVALID_ARGUMENT, "stagings is NULL");
     if (gd != FSDP_BFLOAT16 && gd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "grad_dtype must be BFLOAT16 or FLOAT32");
     if (rd != FSDP_BFLOAT16 && rd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "reduce_dtype must be FLOAT32 or BFLOAT16");
@@ -219,6 +224,57 @@ fsdp_status_t fsdp_stage_rs_pull_hsdp(fsdp_layer_t* l, const void* const* stagin
     ProfScope ps(m, FSDP_PROF_RS_PULL, as_stream(stream), (int64_t)(Wt - 1) * l->pull_elems * dtype_size(gd));
     CUDA_CHECK(fsdpp::launch_rs_pull_nested(l->t_pull.d, l->t_pull.n, pp, gd == FSDP_BFLOAT16, Wt, l->grad, mean != 0,
                                             accumulate != 0, rd == FSDP_BFLOAT16, Wt, m->W, m->cfg, as_stream(stream)));
+    ps.done();
+  });
+}
+
+fsdp_status_t fsdp_stage_hsdp_piece_pull(fsdp_layer_t* l, const void* const* stagings, int32_t replicate,
+                                         int32_t replica, fsdp_dtype_t gd, fsdp_dtype_t rd, int32_t mean, float* res_dev,
+                                         void* stream) {
+  return guarded([&] {
+    check_layer(l);
+    check_hsdp_stage(l, replicate);
+    fsdp_mesh* m = l->mesh;
+    const int Wt = m->W * replicate;
+    if (replica < 0 || replica >= replicate) fail(FSDP_ERR_INVALID_ARGUMENT, "replica out of range");
+    if (!stagings || !res_dev) fail(FSDP_ERR_INVALID_ARGUMENT, "NULL argument");
+    check_align16(res_dev, "res_dev");
+    if (gd != FSDP_BFLOAT16 && gd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "grad_dtype must be BFLOAT16 or FLOAT32");
+    if (rd != FSDP_BFLOAT16 && rd != FSDP_FLOAT32) fail(FSDP_ERR_DTYPE, "reduce_dtype must be FLOAT32 or BFLOAT16");
+    fsdpp::PeerPtrs pp{};
+    for (int r = 0; r < Wt; ++r) {
+      if (!stagings[r]) fail(FSDP_ERR_INVALID_ARGUMENT, "stagings[g] is NULL");
+      check_align16(stagings[r], "stagings[g]");
+      pp.p[r] = (uint8_t*)stagings[r];
+    }
+    DeviceGuard g(m->device);
+    ensure_pieces(l, replicate);
+    const DevTiles& T = l->t_piece[replica];
+    ProfScope ps(m, FSDP_PROF_RS_PULL, as_stream(stream), (int64_t)(Wt - 1) * l->pull_elems * dtype_size(gd) / replicate);
+    CUDA_CHECK(fsdpp::launch_rs_pull_nested(T.d, T.n, pp, gd == FSDP_BFLOAT16, Wt, res_dev, mean != 0, false,
+                                            rd == FSDP_BFLOAT16, Wt, m->W, m->cfg, as_stream(stream)));
+    ps.done();
+  });
+}
+
+fsdp_status_t fsdp_stage_hsdp_replica_gather(fsdp_layer_t* l, const float* const* res_devs, int32_t replicate,
+                                             int32_t accumulate, void* stream) {
+  return guarded([&] {
+    check_layer(l);
+    check_hsdp_stage(l, replicate);
+    fsdp_mesh* m = l->mesh;
+    if (!res_devs) fail(FSDP_ERR_INVALID_ARGUMENT, "res_devs is NULL");
+    fsdpp::PeerPtrs rp{};
+    for (int q = 0; q < replicate; ++q) {
+      if (!res_devs[q]) fail(FSDP_ERR_INVALID_ARGUMENT, "res_devs[q] is NULL");
+      check_align16(res_devs[q], "res_devs[q]");
+      rp.p[q] = (uint8_t*)res_devs[q];
+    }
+    DeviceGuard g(m->device);
+    ensure_pieces(l, replicate);
+    ProfScope ps(m, FSDP_PROF_REPLICA_GATHER, as_stream(stream), (int64_t)(replicate - 1) * 4 * l->pull_elems / replicate);
+    CUDA_CHECK(fsdpp::launch_replica_gather(l->t_gather.d, l->t_gather.n, rp, l->grad, accumulate != 0, m->cfg,
+                                            as_stream(stream)));
     ps.done();
   });
 }

@@ -403,6 +403,40 @@ void poll_async_errors(fsdp_mesh* m) {
   }
 }
 
+void ensure_pieces(fsdp_layer* l, int R) {
+  if (l->piece_R == R) return;
+  const std::vector<Tile> pull = fsdpl::tiles_pull(l->L, l->stg_off_el);
+  int64_t P = 0;
+  const std::vector<Tile> all = fsdpl::split_pieces(pull, l->L.S, R, &P);
+  for (auto& t : l->t_piece) t.release();
+  l->t_piece.assign(R, DevTiles());
+  std::vector<std::vector<Tile>> per(R);
+  for (const Tile& t : all) per[t.pad].push_back(t);
+  for (int q = 0; q < R; ++q) l->t_piece[q].upload(per[q]);
+  // gather tiles: src = dst (the piece sits at the grad's offsets in every result buffer),
+  // merged round robin over the pieces starting after this replica's own, so the persistent
+  // grid reads from every replica at once and the replicas start on different sources (a
+  // piece-major order had every rank reading the same replica first: 530 GB/s, skewed ranks)
+  std::vector<Tile> g;
+  g.reserve(all.size());
+  std::vector<size_t> pos(R, 0);
+  const int rep = l->mesh->R == R ? l->mesh->rep : 0;
+  for (bool more = true; more;) {
+    more = false;
+    for (int i = 1; i <= R; ++i) {
+      const int q = (rep + i) % R;
+      if (pos[q] < per[q].size()) {
+        Tile t = per[q][pos[q]++];
+        t.src = t.dst;
+        g.push_back(t);
+        more = true;
+      }
+    }
+  }
+  l->t_gather.upload(g);
+  l->piece_R = R;
+}
+
 void ce_unshard(fsdp_layer* l, bool fp8, const float* scales, const fsdpp::PeerPtrs& arenas, cudaStream_t st,
                 uint32_t* amax_acc) {
   fsdp_mesh* m = l->mesh;

@@ -24,7 +24,62 @@ cudaError_t launch_nested(const Tile* tiles, int ntiles, PeerPtrs st, float* gra
   return cudaErrorInvalidValue;
 }
 
+// Phase 2 of the two-phase HSDP reduce-scatter: grad[dst + e] (+)= res.p[tile.pad][dst + e]
+// — piece q of this shard rank's world sum, finished by replica q in its result buffer (peer
+// memory over NVLink, or local for q = own replica).  fp32 bits are copied (or added once
+// for accumulate), so the result stays the phase-1 nested sum bit for bit.  Tile dst is
+// 16-element aligned: 16-byte loads / stores, 4 vectors in flight per thread.
+__global__ void __launch_bounds__(kThreads) k_replica_gather(const Tile* __restrict__ tiles, int ntiles, PeerPtrs res,
+                                                             float* __restrict__ grad, bool acc) {
+  pdl_wait();
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    const float* src = reinterpret_cast<const float*>(res.p[tl.pad]) + tl.dst;
+    float* g = grad + tl.dst;
+    const uint32_t n = tl.n, nv = n / 4;
+    constexpr uint32_t U = 4;
+    uint32_t v = threadIdx.x;
+    for (; v + (U - 1) * kThreads < nv; v += U * kThreads) {
+      uint4 x[U];
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u) x[u] = ld_stream(src + 4 * (v + u * kThreads));
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u) {
+        float4* gp = reinterpret_cast<float4*>(g) + v + u * kThreads;
+        float4 y = make_float4(__uint_as_float(x[u].x), __uint_as_float(x[u].y), __uint_as_float(x[u].z),
+                               __uint_as_float(x[u].w));
+        if (acc) {
+          const float4 o = *gp;
+          y = make_float4(__fadd_rn(o.x, y.x), __fadd_rn(o.y, y.y), __fadd_rn(o.z, y.z), __fadd_rn(o.w, y.w));
+        }
+        *gp = y;
+      }
+    }
+    for (; v < nv; v += kThreads) {
+      const uint4 x = ld_stream(src + 4 * v);
+      float4* gp = reinterpret_cast<float4*>(g) + v;
+      float4 y = make_float4(__uint_as_float(x.x), __uint_as_float(x.y), __uint_as_float(x.z), __uint_as_float(x.w));
+      if (acc) {
+        const float4 o = *gp;
+        y = make_float4(__fadd_rn(o.x, y.x), __fadd_rn(o.y, y.y), __fadd_rn(o.z, y.z), __fadd_rn(o.w, y.w));
+      }
+      *gp = y;
+    }
+    for (uint32_t e = nv * 4 + threadIdx.x; e < n; e += kThreads) g[e] = acc ? __fadd_rn(g[e], src[e]) : src[e];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_replica_gather(const Tile* tiles, int ntiles, PeerPtrs res, float* grad, bool accumulate,
+                                  fsdpk::LaunchCfg cfg, cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  if (cfg.variant & 2) {   // TMA bulk: the single-source pull with per-tile source (tile.src = tile.dst)
+    const PullOps ops = make_ops(1, false, accumulate, false, cfg);
+    return launch_pull_bulk_w<1, false, 1, true>(tiles, ntiles, res, grad, ops, grid_for(ntiles, cfg), st, cfg.pdl);
+  }
+  return launch_p(cfg.pdl, k_replica_gather, grid_for(ntiles, cfg), 0, st, tiles, ntiles, res, grad, accumulate);
+}
 
 cudaError_t launch_rs_pull_nested(const Tile* tiles, int ntiles, PeerPtrs staging, bool grad_bf16, int divisor,
                                   float* grad, bool mean, bool accumulate, bool bf16_reduce, int W, int G,

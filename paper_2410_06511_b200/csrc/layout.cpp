@@ -333,4 +333,25 @@ std::vector<fsdpk::Tile> tiles_stage(const Layout& L, const std::vector<int64_t>
   return t;
 }
 
+std::vector<fsdpk::Tile> split_pieces(const std::vector<fsdpk::Tile>& pull, int64_t S, int R, int64_t* piece) {
+  const int64_t P = round_up(ceil_div(std::max<int64_t>(S, 1), R), kAlignElems);
+  if (piece) *piece = P;
+  std::vector<fsdpk::Tile> out;
+  for (const fsdpk::Tile& t : pull) {
+    int64_t d = (int64_t)t.dst, e = d + t.n;
+    while (d < e) {
+      const int64_t q = d / P;
+      const int64_t cut = std::min<int64_t>(e, (q + 1) * P);
+      fsdpk::Tile x = t;
+      x.src = t.src + (uint64_t)(d - (int64_t)t.dst);
+      x.dst = (uint64_t)d;
+      x.n = (uint32_t)(cut - d);
+      x.pad = (uint32_t)q;
+      out.push_back(x);
+      d = cut;
+    }
+  }
+  return out;
+}
+
 }  // namespace fsdpl

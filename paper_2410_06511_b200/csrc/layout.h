@@ -72,4 +72,12 @@ std::vector<fsdpk::Tile> tiles_recv_reduce_own(const Layout& L);
 // (with 16-byte aligned grad bases the own-row reduce needs no realignment).
 bool own_rows_aligned(const Layout& L, int64_t gsize);
 
+// HSDP two-phase reduce-scatter (one NVSwitch domain): the shard's flat range [0, S) is cut
+// into R pieces of P = round_up(ceil(S / R), 16) elements (piece q = [q P, min((q+1) P, S)),
+// *piece = P); replica q computes piece q of its shard rank's world sum.  Returns the pull
+// tiles cut at piece boundaries with tile.pad = piece index.  Cuts fall on multiples of 16
+// elements of dst, and every pull tile's dst is 16-element aligned, so src moves by a
+// multiple of 16 elements too: each part keeps its tile's alignment phase.
+std::vector<fsdpk::Tile> split_pieces(const std::vector<fsdpk::Tile>& pull, int64_t S, int R, int64_t* piece);
+
 }  // namespace fsdpl

@@ -65,6 +65,13 @@ cudaError_t launch_rs_pull_nested(const fsdpk::Tile* tiles, int ntiles, PeerPtrs
                                   float* grad, bool mean, bool accumulate, bool bf16_reduce, int W, int G,
                                   fsdpk::LaunchCfg cfg, cudaStream_t st);
 
+// HSDP two-phase reduce-scatter (hsdp_kernels.cu): phase 1 is launch_rs_pull_nested over the
+// tiles of this replica's piece (layout.h split_pieces) writing into this rank's fp32 result
+// buffer; phase 2 copies every piece q from replica q's result buffer res.p[q] (tile.pad = q)
+// into the grad: grad[dst+e] (+)= res.p[pad][dst+e].  Tile dst 16-element aligned.
+cudaError_t launch_replica_gather(const fsdpk::Tile* tiles, int ntiles, PeerPtrs res, float* grad, bool accumulate,
+                                  fsdpk::LaunchCfg cfg, cudaStream_t st);
+
 // Gather copy: dst + tile.dst <- srcs.p[param] + tile.src, n bytes (any alignment).
 cudaError_t launch_gather_copy(const fsdpk::Tile* tiles, int ntiles, const fsdpk::PtrArray& srcs,
                                void* dst, fsdpk::LaunchCfg cfg, cudaStream_t st);

@@ -218,9 +218,13 @@ __global__ void __launch_bounds__(kThreads) k_rs_pull(const Tile* __restrict__ t
 constexpr uint32_t kPullMaxStages = 4;
 constexpr size_t kPullMaxSmem = 200 * 1024;   // stages * W * chunk, leaves room for 1 CTA/SM
 
-template <int W, bool kGradBf16, int G = W>
+// kSel (W = 1 only): each tile reads its one source st.p[tile.pad] instead of st.p[0] — the
+// HSDP replica gather (fp32 pieces from the replica that finished them; mean off, W = 1, so
+// the "sum" is the value itself, + the grad under accumulate).
+template <int W, bool kGradBf16, int G = W, bool kSel = false>
 __global__ void __launch_bounds__(kThreads) k_rs_pull_bulk(const Tile* __restrict__ tiles, int ntiles, PeerPtrs st,
                                                            float* __restrict__ grad, PullOps ops) {
+  static_assert(!kSel || W == 1, "per-tile source selection is the single-source (gather) form");
   extern __shared__ __align__(128) uint8_t smem[];   // [stages][W][chunk]
   __shared__ uint64_t full[kPullMaxStages];
   constexpr uint32_t gs = kGradBf16 ? 2 : 4;
@@ -250,7 +254,8 @@ __global__ void __launch_bounds__(kThreads) k_rs_pull_bulk(const Tile* __restric
       const uint64_t off = tl.src * gs + (uint64_t)it_c * chunk;
       mbar_arrive_expect_tx(&full[s], W * bytes);
 #pragma unroll
-      for (int q = 0; q < W; ++q) bulk_g2s(smem + ((size_t)s * W + q) * chunk, st.p[q] + off, bytes, &full[s]);
+      for (int q = 0; q < W; ++q)
+        bulk_g2s(smem + ((size_t)s * W + q) * chunk, (kSel ? st.p[tl.pad] : st.p[q]) + off, bytes, &full[s]);
       ++issued;
       if (++it_c == nch) { it_t += gridDim.x; it_c = 0; }
     }
@@ -262,15 +267,18 @@ __global__ void __launch_bounds__(kThreads) k_rs_pull_bulk(const Tile* __restric
     float* g = grad + tl.dst;
     const uint32_t n = tl.n;
     if (!bulk_ok(tl)) {   // bulk needs 16-byte granularity
+      PeerPtrs sel{};
+      if constexpr (kSel) sel.p[0] = st.p[tl.pad];
+      const PeerPtrs& sp = kSel ? sel : st;
       const uint32_t k = (uint32_t)(sb & (kGradBf16 ? 7u : 15u));
       const uint32_t nv = n / 4;
-      if (k == 0) pull_body<W, kGradBf16, true, G>(st, sb, g, nv, 0, ops);
-      else pull_body<W, kGradBf16, false, G>(st, sb, g, nv, k, ops);
+      if (k == 0) pull_body<W, kGradBf16, true, G>(sp, sb, g, nv, 0, ops);
+      else pull_body<W, kGradBf16, false, G>(sp, sb, g, nv, k, ops);
       for (uint32_t e = nv * 4 + threadIdx.x; e < n; e += kThreads) {
         float a = 0.0f, pp = 0.0f;
 #pragma unroll
         for (int q = 0; q < W; ++q) {
-          const uint8_t* p = st.p[q] + sb + (uint64_t)gs * e;
+          const uint8_t* p = sp.p[q] + sb + (uint64_t)gs * e;
           const float x = kGradBf16 ? __uint_as_float(((uint32_t)(*(const uint16_t*)p)) << 16) : *(const float*)p;
           nsum<W, G>(a, pp, q, ops.rb(ops.div(x)));
         }
@@ -346,7 +354,7 @@ cudaError_t launch_pull_wv(const Tile* tiles, int ntiles, PeerPtrs st, float* gr
   }
 }
 
-template <int W, bool kGradBf16, int G = W>
+template <int W, bool kGradBf16, int G = W, bool kSel = false>
 cudaError_t launch_pull_bulk_w(const Tile* tiles, int ntiles, PeerPtrs st, float* grad, PullOps ops, int g,
                                cudaStream_t s, bool pdl) {
   while ((size_t)ops.stages * W * ops.chunk > kPullMaxSmem) {   // shrink stages, then chunk
@@ -358,13 +366,13 @@ cudaError_t launch_pull_bulk_w(const Tile* tiles, int ntiles, PeerPtrs st, float
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !attr[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_rs_pull_bulk<W, kGradBf16, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_rs_pull_bulk<W, kGradBf16, G, kSel>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kPullMaxSmem);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   // one wave (launch_persistent): at W = 8 the 64 KB stages allow 3 CTAs per SM, not 4
-  return launch_p(pdl, k_rs_pull_bulk<W, kGradBf16, G>, g, smem, s, tiles, ntiles, st, grad, ops);
+  return launch_p(pdl, k_rs_pull_bulk<W, kGradBf16, G, kSel>, g, smem, s, tiles, ntiles, st, grad, ops);
 }
 
 template <bool kGradBf16>

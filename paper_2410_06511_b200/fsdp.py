@@ -184,11 +184,13 @@ class Mesh:
 
     @property
     def hsdp_rs(self) -> str:
-        """HSDP reduce-scatter mechanism: 'world_pull' (one pull over all ranks of one NVSwitch
-        domain, nested-order sum) or 'rs+allreduce' (shard-group RS, then NCCL all-reduce)."""
+        """HSDP reduce-scatter mechanism on one NVSwitch domain: 'world_pull_2phase' (each
+        replica reduces 1/R of the shard over all ranks, then the replicas exchange the
+        finished pieces; default), 'world_pull' (one pull of the whole shard over all ranks),
+        both nested-order sums; or 'rs+allreduce' (shard-group RS, then NCCL all-reduce)."""
         a = C.c_int32()
         call("fsdp_mesh_get_hsdp_rs", self.handle, C.byref(a))
-        return "world_pull" if a.value else "rs+allreduce"
+        return {2: "world_pull_2phase", 1: "world_pull"}.get(a.value, "rs+allreduce")
 
     @property
     def p2p_rs(self) -> str:
@@ -514,6 +516,20 @@ def stage_rs_pull_hsdp(layer: Layer, stagings: Sequence[torch.Tensor], replicate
     grad (+)= sum over replicas of (sum over shard ranks of fp32(x) / (replicate * W))."""
     call("fsdp_stage_rs_pull_hsdp", layer.handle, _ptr_array(stagings), int(replicate), _dtype_code(grad_dtype),
          _dtype_code(reduce_dtype), int(bool(mean)), int(bool(accumulate)), _stream(stream))
+
+
+def stage_hsdp_piece_pull(layer: Layer, stagings: Sequence[torch.Tensor], replicate: int, replica: int, grad_dtype,
+                          res: torch.Tensor, reduce_dtype=torch.float32, mean: bool = True, stream=None):
+    """HSDP two-phase RS, phase 1: res (fp32 [S]) = the nested world sum over piece `replica`."""
+    call("fsdp_stage_hsdp_piece_pull", layer.handle, _ptr_array(stagings), int(replicate), int(replica),
+         _dtype_code(grad_dtype), _dtype_code(reduce_dtype), int(bool(mean)), C.c_void_p(res.data_ptr()),
+         _stream(stream))
+
+
+def stage_hsdp_replica_gather(layer: Layer, res: Sequence[torch.Tensor], accumulate: bool = False, stream=None):
+    """HSDP two-phase RS, phase 2: grad (+)= piece q from res[q] (replica q's phase-1 buffer)."""
+    call("fsdp_stage_hsdp_replica_gather", layer.handle, _ptr_array(res), len(res), int(bool(accumulate)),
+         _stream(stream))
 
 
 def stage_rs_scatter(layer: Layer, grads: Sequence[torch.Tensor], recvs: Sequence[torch.Tensor],

@@ -255,12 +255,12 @@ def run_hsdp_checks(W, rank, local, Ws):
     mesh = F.Mesh.from_process_group(device=local, shard_size=Ws)
     assert (mesh.replicate_size, mesh.shard_size) == (R, Ws)
     s = mesh.shard_rank
-    world_pull = mesh.hsdp_rs == "world_pull"   # one NVSwitch domain: the default HSDP RS
+    world_pull = mesh.hsdp_rs.startswith("world_pull")   # one NVSwitch domain: the default HSDP RS
     algos = ["p2p", "nccl"] if (mesh.algo == "p2p" or world_pull) else ["nccl"]
     for algo in algos:
         mesh.set_algo(algo)
         wp = algo == "p2p" and world_pull
-        assert (mesh.hsdp_rs == "world_pull") == wp
+        assert mesh.hsdp_rs.startswith("world_pull") == wp
         for ui, u in enumerate([synth.model_units("toy")[0], synth.ragged_unit(5, world_size=Ws)]):
             shapes = [sh for _, sh, _ in u]
             elig = [e for _, _, e in u]

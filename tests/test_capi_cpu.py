@@ -31,7 +31,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     # the binding declares every one of them with the same name
     bound = set(_capi.SIGNATURES) | set(_capi._OTHER)
     assert set(syms) == bound, set(syms) ^ bound
-    assert _capi.lib().fsdp_abi_version() == 1
+    assert _capi.lib().fsdp_abi_version() == 2
 
 
 def test_library_is_sm100a():

@@ -7,6 +7,10 @@ one kernel (include/fsdp_b200.h, fsdp_mesh_init_hsdp).  Here the R*Ws "ranks" li
 Ws communicator-less meshes (one per shard rank; every replica of a shard rank has the same
 layout) and R*Ws stagings, through fsdp_stage_rs_pull_hsdp — the kernels the multi-GPU path
 runs over NVLink, minus the world handshakes (tests/mgpu_worker.py covers those).
+The default two-phase form (replica q computes piece q of the shard into its fp32 result
+buffer, fsdp_stage_hsdp_piece_pull; every replica then gathers the R pieces,
+fsdp_stage_hsdp_replica_gather) is checked the same way, plus: phase 1 writes nothing
+outside its piece.
 Bar: bit-exact to the oracle's nested order (oracle.HsdpWorld 'order'), for the bulk (TMA)
 and register pull variants, every (R, Ws) with R*Ws <= 8, ragged units, accumulation, and
 one full Llama 3.1 8B block at R x Ws = 2 x 4."""
@@ -99,6 +103,76 @@ def _run(shapes, elig, R, Ws, G, GT, tdt, mean, acc, seed, variant=None):
         emu.close()
 
 
+def _run2(shapes, elig, R, Ws, G, GT, tdt, mean, acc, seed, variant=None):
+    """Two-phase: phase 1 for every global rank g into res[g], phase 2 for every replica of
+    every shard rank (the emulated shard rank's grad buffer is reset before each)."""
+    Wt = R * Ws
+    h = HsdpWorld(shapes, R, Ws, elig)
+    emu = _Emu(shapes, elig, Ws, _params(shapes, seed), variant)
+    try:
+        offs, total = F.grad_staging_layout(emu.layers[0])
+        stag = [torch.zeros(total + 64, dtype=tdt, device="cuda") for _ in range(Wt)]
+        for g in range(Wt):
+            F.stage_grads_to_staging(emu.layers[g % Ws], GT[g], stag[g])
+        S = emu.layers[0].S
+        nan = np.uint32(0x7FC00001)
+        res = [torch.full((S + 16,), int(nan), dtype=torch.int32, device="cuda").view(torch.float32)
+               for _ in range(Wt)]
+        for g in range(Wt):
+            F.stage_hsdp_piece_pull(emu.layers[g % Ws], stag, R, g // Ws, tdt, res[g], mean=mean)
+        torch.cuda.synchronize()
+        P = -(-max(S, 1) // R)
+        P = -(-P // 16) * 16
+        for g in range(Wt):   # phase 1 wrote only inside piece g // Ws
+            q = g // Ws
+            r = res[g].view(torch.int32).cpu().numpy().view(np.uint32)
+            outside = np.ones(S + 16, dtype=bool)
+            outside[q * P:min((q + 1) * P, S)] = False
+            assert np.all(r[outside] == nan), f"R={R} Ws={Ws} g={g}: write outside piece {q}"
+        ref = h.reduce_scatter_grads(G, BF16 if tdt == torch.bfloat16 else FP32, mean)
+        rng = np.random.default_rng(seed + 7)
+        old = [rng.standard_normal(l.S).astype(np.float32) for l in emu.layers]
+        for s, l in enumerate(emu.layers):
+            for rep in range(R):
+                l.sharded_grad_flat().copy_(torch.from_numpy(old[s]).cuda())
+                F.stage_hsdp_replica_gather(l, [res[q * Ws + s] for q in range(R)], accumulate=acc)
+                torch.cuda.synchronize()
+                g = rep * Ws + s
+                for p in range(len(shapes)):
+                    want = ref[g]["order"][p]
+                    got = l.sharded_grad(p).cpu().numpy()
+                    if acc:
+                        m = l.metas[p]
+                        prev = old[s][m["elem_offset"]:m["elem_offset"] + got.size].reshape(got.shape)
+                        want = (prev + want).astype(np.float32)
+                    np.testing.assert_array_equal(got.view(np.uint32), want.astype(np.float32).view(np.uint32),
+                                                  err_msg=f"two-phase R={R} Ws={Ws} shard {s} rep {rep} p{p}")
+                flat = l.sharded_grad_flat().cpu().numpy()
+                real = np.zeros(l.S, dtype=bool)
+                for m in l.metas:
+                    real[m["elem_offset"]:m["elem_offset"] + m["row_count"] * m["rest"]] = True
+                np.testing.assert_array_equal(flat[~real].view(np.uint32), old[s][~real].view(np.uint32))
+    finally:
+        emu.close()
+
+
+@pytest.mark.parametrize("kind,seed", KINDS[:4])
+@pytest.mark.parametrize("R,Ws", PAIRS)
+@pytest.mark.parametrize("variant", [None, 13])
+def test_hsdp_two_phase_emulated(kind, seed, R, Ws, variant):
+    shapes, elig = _unit(kind, seed, Ws)
+    G, GT, tdt = _grads(seed + 40, shapes, R * Ws, BF16)
+    _run2(shapes, elig, R, Ws, G, GT, tdt, True, False, seed, variant)
+
+
+@pytest.mark.parametrize("R,Ws", [(2, 2), (4, 2), (2, 3), (8, 1)])
+@pytest.mark.parametrize("gd,mean,acc", [(FP32, True, False), (BF16, False, False), (BF16, True, True)])
+def test_hsdp_two_phase_dtypes_mean_accumulate(R, Ws, gd, mean, acc):
+    shapes, elig = _unit("ragged", 8, Ws)
+    G, GT, tdt = _grads(8, shapes, R * Ws, gd)
+    _run2(shapes, elig, R, Ws, G, GT, tdt, mean, acc, 8)
+
+
 @pytest.mark.parametrize("kind,seed", KINDS[:4])
 @pytest.mark.parametrize("R,Ws", PAIRS)
 @pytest.mark.parametrize("variant", [None, 13])   # default (TMA bulk pull) / register pull (VEC 8)
@@ -177,5 +251,20 @@ def test_hsdp_world_pull_full_block():
                 got = l.sharded_grad(p).view(torch.int32)
                 bad = (got != want).nonzero()
                 assert bad.numel() == 0, f"shard {s} p{p}: {bad.shape[0]} elements differ"
+        # two-phase (the default): every replica's piece, then each shard rank gathers them
+        S = emu.layers[0].S
+        res = [torch.empty(S + 16, dtype=torch.float32, device="cuda") for _ in range(R * Ws)]
+        for g in range(R * Ws):
+            F.stage_hsdp_piece_pull(emu.layers[g % Ws], stag, R, g // Ws, torch.bfloat16, res[g])
+        for s, l in enumerate(emu.layers):
+            l.sharded_grad_flat().fill_(float("nan"))
+            F.stage_hsdp_replica_gather(l, [res[q * Ws + s] for q in range(R)])
+        torch.cuda.synchronize()
+        for s, l in enumerate(emu.layers):
+            for p in range(len(shapes)):
+                want = torch.from_numpy(order[s][p].view(np.int32)).cuda()
+                got = l.sharded_grad(p).view(torch.int32)
+                bad = (got != want).nonzero()
+                assert bad.numel() == 0, f"two-phase shard {s} p{p}: {bad.shape[0]} elements differ"
     finally:
         emu.close()

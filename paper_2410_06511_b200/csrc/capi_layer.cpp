@@ -566,6 +566,7 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       CUDA_CHECK(cudaEventRecord(l->ev_rcall, cs));
       if (zc) {
         CUDA_CHECK(cudaStreamWaitEvent(m->s_rs, l->ev_rcall, 0));
+        wait_released(m->s_rs, ss, cap);   // the previous gather out of this buffer (s_rsc)
       } else {
         CUDA_CHECK(cudaStreamWaitEvent(m->s_rsc, l->ev_rcall, 0));
         wait_released(m->s_rsc, ss, cap);
@@ -612,18 +613,24 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
                                              m->d_err, m->s_rs, m->cfg.pdl));
         ph.done();
       }
+      cudaStream_t fin = m->s_rs;
       if (two_phase) {   // every piece is final on its replica (done handshake): gather them
+        // on the second stream, so the next unit's phase 1 (s_rs) overlaps this gather
+        fin = m->s_rsc;
+        CUDA_CHECK(cudaEventRecord(l->ev_k5, m->s_rs));
+        CUDA_CHECK(cudaStreamWaitEvent(fin, l->ev_k5, 0));
         fsdpp::PeerPtrs rp{};
         for (int q = 0; q < m->R; ++q) rp.p[q] = (uint8_t*)ss->buf.peers[q * m->W + m->rank] + res_off;
-        ProfScope pg(m, FSDP_PROF_REPLICA_GATHER, m->s_rs, (int64_t)(m->R - 1) * 4 * l->pull_elems / m->R);
+        ProfScope pg(m, FSDP_PROF_REPLICA_GATHER, fin, (int64_t)(m->R - 1) * 4 * l->pull_elems / m->R);
         CUDA_CHECK(fsdpp::launch_replica_gather(l->t_gather.d, l->t_gather.n, rp, l->grad, accumulate != 0, m->cfg,
-                                                m->s_rs));
+                                                fin));
         pg.done();
       }
       // the slot (staging + result pieces) is rewritten only after the next ready handshake
-      // of this slot, which every rank signals after its own gather has read the pieces
-      release_sym_slot(ss, m->s_rs, cap);
-      CUDA_CHECK(cudaEventRecord(l->ev_rs_done, m->s_rs));
+      // of this slot, which every rank signals after its own gather has read the pieces (the
+      // zero-copy path waits for this release before that handshake)
+      release_sym_slot(ss, fin, cap);
+      CUDA_CHECK(cudaEventRecord(l->ev_rs_done, fin));
       l->rs_pending = true;
       return;
     }

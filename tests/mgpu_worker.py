@@ -326,6 +326,33 @@ def run_hsdp_checks(W, rank, local, Ws):
                         got = layer.sharded_grad(p).cpu().numpy()
                         np.testing.assert_array_equal(got.view(np.uint32), ref["order"][p].view(np.uint32),
                                                       err_msg=f"hsdp world pull zero-copy {R}x{Ws} {ui} p{p} rep{rep}")
+                # the HSDP reduce-scatter captured in a CUDA graph (world handshake epochs from
+                # device counters; the two-phase gather on the second stream joins the capture):
+                # replays equal the oracle, also after the grads change in place
+                st = torch.cuda.Stream()
+                dist.barrier()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    F.reduce_scatter_grads(layer, bufs, stream=st)
+                    F.fsdp_wait_reduce_scatter(layer, stream=st)
+                for seed in (0, 1):
+                    if seed:
+                        G = [[synth.grad_bf16_bits(ui + 91, p, q, sh) for p, sh in enumerate(shapes)] for q in range(W)]
+                        for b, x in zip(bufs, G[rank]):
+                            b.copy_(torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16))
+                        ref = h.reduce_scatter_grads(G, BF16, True)[rank]
+                        torch.cuda.synchronize()
+                        dist.barrier()
+                    layer.sharded_grad_flat().zero_()
+                    torch.cuda.synchronize()
+                    g.replay()
+                    torch.cuda.synchronize()
+                    for p in range(len(shapes)):
+                        got = layer.sharded_grad(p).cpu().numpy()
+                        np.testing.assert_array_equal(got.view(np.uint32), ref["order"][p].view(np.uint32),
+                                                      err_msg=f"hsdp graph {R}x{Ws} {ui} p{p} replay{seed}")
+                del g
+                torch.cuda.synchronize()
             layer.destroy()
         print(f"rank {rank}/{W} hsdp {R}x{Ws} algo={algo} rs={mesh.hsdp_rs}: OK", flush=True)
     mesh.synchronize(120000)

@@ -169,6 +169,22 @@ fsdp_status_t fsdp_get_unique_id(uint8_t id[FSDP_UNIQUE_ID_BYTES]);
 fsdp_status_t fsdp_mesh_init(const uint8_t id[FSDP_UNIQUE_ID_BYTES], int32_t world_size,
                              int32_t rank, int32_t cuda_device, fsdp_mesh_t** out);
 
+/* A P2P mesh with no NCCL communicator: the few host-side collective steps the library
+ * needs (CUDA IPC handle exchange of the symmetric buffers, the layout-hash check, barriers
+ * before frees) go through the caller's host all-gather `fn`: send = `bytes` host bytes of
+ * this rank, recv = world_size * bytes, rank-major over the whole world; returns 0 on
+ * success (e.g. torch.distributed over gloo).  Every device-side step is the P2P path:
+ * push unshard, pull / store reduce-scatter, the fp8 amax all-reduce (a P2P max over
+ * symmetric memory), HSDP's world reduce-scatter (shard_size < world_size; 0 = all ranks).
+ * The ranks may share a GPU (CUDA IPC works between processes on one device), so the
+ * cross-process protocol — IPC-mapped arenas, device-epoch handshakes, timeouts — runs
+ * where NCCL (one rank per GPU) cannot.  FSDP_ERR_UNAVAILABLE if some rank cannot map
+ * every peer (or, with shard_size < world_size, the world); fsdp_mesh_set_algo(NCCL) is
+ * unavailable on it.  `fn` and `ctx` must stay valid until fsdp_mesh_destroy returns. */
+typedef int32_t (*fsdp_host_allgather_fn)(const void* send, void* recv, int64_t bytes, void* ctx);
+fsdp_status_t fsdp_mesh_init_hostcoll(int32_t world_size, int32_t rank, int32_t shard_size, int32_t cuda_device,
+                                      fsdp_host_allgather_fn fn, void* ctx, fsdp_mesh_t** out);
+
 /* A mesh without communicators: the layout is that of rank `rank` of `world_size`,
  * the fsdp_stage_* entry points work, the collective calls work only when
  * world_size == 1 (identity collectives) and return FSDP_ERR_UNAVAILABLE otherwise.

@@ -54,6 +54,7 @@ _PP = C.POINTER(C.c_void_p)
 # fsdp_alloc_fn / fsdp_free_fn (fsdp_mesh_set_allocator)
 ALLOC_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_size_t, C.c_int32, C.POINTER(C.c_void_p))
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_int32)
+HOSTAG_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 
 # name -> argtypes (restype is fsdp_status_t unless listed in _OTHER)
 SIGNATURES = {
@@ -108,6 +109,7 @@ SIGNATURES = {
     "fsdp_stage_rs_pull": [_VP, _PP, _I32, _I32, _I32, _I32, _VP],
     "fsdp_stage_rs_pull_hsdp": [_VP, _PP, _I32, _I32, _I32, _I32, _I32, _VP],
     "fsdp_mesh_get_hsdp_rs": [_VP, C.POINTER(_I32)],
+    "fsdp_mesh_init_hostcoll": [_I32, _I32, _I32, _I32, HOSTAG_FN, _VP, C.POINTER(_VP)],
     "fsdp_stage_hsdp_piece_pull": [_VP, _PP, _I32, _I32, _I32, _I32, _I32, _VP, _VP],
     "fsdp_stage_hsdp_replica_gather": [_VP, _PP, _I32, _I32, _VP],
     "fsdp_mesh_memory": [_VP, C.POINTER(_I64)],

@@ -230,6 +230,7 @@ struct SymSlot {
 };
 
 constexpr int kFlagSlots = 512;  // flag slots per kind: pooled slots first, then layer grad buffers
+constexpr int kAmaxSlot = kFlagSlots - 1;   // the P2P fp8 amax all-reduce's flag slot
 constexpr int kPoolSlots = 64;   // max pooled symmetric slots (arenas / staging) per pool
 constexpr int kHistMax = 64;     // max delayed-scaling amax history length
 constexpr int kRegCapDefault = 65536;   // fp8 registry entries per mesh (FSDP_B200_REGISTRY_CAP)
@@ -300,6 +301,10 @@ struct fsdp_mesh {
   bool store_own_direct = true;              // store RS: own rows read from the caller's grads (FSDP_B200_STORE_OWN=0: own slot)
   bool p2p_ok = false;
   SymBuf flags;                              // uint64 [FK_NUM][kFlagSlots][kMaxRanks]
+  SymBuf amax_sym;                           // P2P fp8 amax all-reduce: uint32 [reg_cap] per rank
+  // host-collective mesh (fsdp_mesh_init_hostcoll): no NCCL; host steps via the callback
+  fsdp_host_allgather_fn hc_fn = nullptr;
+  void* hc_ctx = nullptr;
   // HSDP on one NVSwitch domain (R > 1, R * W <= 8, every rank maps every rank): the
   // reduce-scatter pulls this rank's shard rows from all R * W ranks and sums them in the
   // oracle's nested order (shard ranks, then replicas) — no separate replica all-reduce.
@@ -400,6 +405,16 @@ struct Group {
   int W, rank;
 };
 Group group_of(const fsdp_mesh* m, int grp);
+// All-gather of `bytes` host bytes per group rank into recv[G.W][bytes] (group rank order):
+// the host callback (host-collective mesh) or NCCL on the device (host-synchronous).
+void group_allgather_host(fsdp_mesh* m, int grp, const void* send, void* recv, size_t bytes);
+// NCCL communicators exist (a NCCL mesh with W > 1 or HSDP); false for local and
+// host-collective meshes
+bool nccl_ok(const fsdp_mesh* m);
+// fp8 amax all-reduce(max) of reg_acc[0, n) over the shard group through symmetric memory
+// (P2P meshes): copy into amax_sym, ready handshake, max over every rank's copy, done
+// handshake; stream-ordered on `st`, graph-capturable.
+void p2p_amax_allreduce(fsdp_mesh* m, int n, cudaStream_t st);
 void mesh_barrier(fsdp_mesh* m, int grp = GRP_SHARD);
 bool mesh_all_ok(fsdp_mesh* m, bool ok, int grp = GRP_SHARD);
 void sym_free_local(fsdp_mesh* m, SymBuf& b);

@@ -21,14 +21,8 @@ fsdp_status_t fsdp_shard(fsdp_mesh_t* m, int32_t n, const fsdp_param_desc_t* des
     if (n > fsdpk::kMaxPtrs) fail(FSDP_ERR_UNAVAILABLE, "units with more than 512 parameters are not supported in this build");
     DeviceGuard g(m->device);
     if (comm_ready(m)) {  // all ranks must agree on the unit ("shape mismatch across members")
-      uint64_t* d = nullptr;
-      CUDA_CHECK(cudaMalloc(&d, sizeof(uint64_t) * m->W));
-      CUDA_CHECK(cudaMemcpy(d + m->rank, &L.hash, sizeof(uint64_t), cudaMemcpyHostToDevice));
-      NCCL_CHECK(ncclAllGather(d + m->rank, d, 8, ncclUint8, m->comm_ag, m->s_ag));
       std::vector<uint64_t> h(m->W);
-      CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
-      CUDA_CHECK(cudaMemcpy(h.data(), d, sizeof(uint64_t) * m->W, cudaMemcpyDeviceToHost));
-      cudaFree(d);
+      group_allgather_host(m, GRP_SHARD, &L.hash, h.data(), sizeof(uint64_t));
       for (uint64_t x : h)
         if (x != L.hash) fail(FSDP_ERR_SHAPE, "ranks disagree on the unit's parameter shapes (layout hash mismatch)");
     }
@@ -264,7 +258,10 @@ static fsdp_status_t precompute_impl(fsdp_mesh_t* m, fsdp_layer_t* const* layers
     if (comm_ready(m) && m->reg_size > 0) {
       // max of non-negative fp32 bit patterns == uint32 max (NaN patterns propagate)
       ProfScope pr(m, FSDP_PROF_ALL_REDUCE, m->s_rs, (int64_t)4 * m->reg_size);
-      NCCL_CHECK(ncclAllReduce(m->reg_acc, m->reg_acc, (size_t)m->reg_size, ncclUint32, ncclMax, m->comm_rs, m->s_rs));
+      if (m->p2p_ok && (m->algo == FSDP_ALGO_P2P || !nccl_ok(m)))   // through symmetric memory
+        p2p_amax_allreduce(m, m->reg_size, m->s_rs);
+      else
+        NCCL_CHECK(ncclAllReduce(m->reg_acc, m->reg_acc, (size_t)m->reg_size, ncclUint32, ncclMax, m->comm_rs, m->s_rs));
       pr.done();
     }
     {
@@ -532,11 +529,6 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       CUDA_CHECK(fsdpk::launch_rs_copy_out(T, false, l->grad, true, S, m->cfg, st));
       po.done();
     };
-    // P2P mechanism: identical on every rank (the mode is set collectively; the layer's
-    // zero-copy buffer exists on all ranks or none)
-    // AUTO: with zero-copy buffers the pull needs no staging and one kernel less, so it wins
-    // at W = 2 and for small units (the store's ~5% link-rate edge is worth less than its
-    // extra kernel below ~64 MB of bus bytes, profiles/r16 alpha-B fits); else store
     if (hsdp && m->hsdp_rs_p2p) {
       // HSDP on one NVSwitch domain (header: fsdp_mesh_init_hsdp): ONE pull over the
       // world.  Every rank stages its full grads (zero copy when they live in the layer's
@@ -634,6 +626,11 @@ fsdp_status_t fsdp_reduce_scatter_grads(fsdp_layer_t* l, const void* const* grad
       l->rs_pending = true;
       return;
     }
+    // P2P mechanism: identical on every rank (the mode is set collectively; the layer's
+    // zero-copy buffer exists on all ranks or none)
+    // AUTO: with zero-copy buffers the pull needs no staging and one kernel less, so it wins
+    // at W = 2 and for small units (the store's ~5% link-rate edge is worth less than its
+    // extra kernel below ~64 MB of bus bytes, profiles/r16 alpha-B fits); else store
     const bool zc_layer = l->gbuf && l->gbuf_sym && l->gbuf->buf.grp == GRP_SHARD;
     const int64_t bus_bytes = l->stg_elems * dtype_size(gd) * (m->W - 1) / std::max(m->W, 1);
     const bool p2p_store = m->p2p_rs_mode == FSDP_P2P_RS_STORE ||
@@ -907,7 +904,7 @@ fsdp_status_t fsdp_full_grad_buffer(fsdp_layer_t* l, fsdp_dtype_t gd, int32_t p,
       if (m->hsdp_rs_p2p)   // + the two-phase HSDP reduce-scatter's fp32 result region [S]
         bytes = (size_t)(hsdp_res_offset(l, gsz) + 4 * std::max<int64_t>(l->L.S, 16));
       if (m->p2p_ok || m->hsdp_rs_p2p) {   // collective: every rank of the group maps every peer's buffer
-        if (kPoolSlots + m->gbuf_seq >= kFlagSlots) fail(FSDP_ERR_UNAVAILABLE, "too many layer grad buffers");
+        if (kPoolSlots + m->gbuf_seq >= kAmaxSlot) fail(FSDP_ERR_UNAVAILABLE, "too many layer grad buffers");
         s->index = kPoolSlots + m->gbuf_seq++;
         // HSDP world pull: the buffer is symmetric over the whole world (its reduce-scatter
         // reads it from every replica); else over the shard group

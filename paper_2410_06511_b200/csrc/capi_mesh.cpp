@@ -116,7 +116,7 @@ static void p2p_init(fsdp_mesh* m) {
   const bool want_nccl = env && std::string(env) == "nccl";
   // HSDP on one NVSwitch domain: world-group symmetric memory for the reduce-scatter pull
   // (collective over the world; the same decision on every rank: R, W and the environment)
-  if (m->R > 1 && m->W * m->R <= 8 && m->comm_world) {
+  if (m->R > 1 && m->W * m->R <= 8 && (m->comm_world || m->hc_fn)) {
     // two-phase moves fewer bytes iff (RW-1) 2/R + (R-1) 4/R < (RW-1) 2, i.e. R W > 3
     m->hsdp_two_phase = m->W * m->R > 3;
     if (const char* e = std::getenv("FSDP_B200_HSDP_RS")) m->hsdp_two_phase = m->hsdp_two_phase && std::atoi(e) != 1;
@@ -132,6 +132,10 @@ static void p2p_init(fsdp_mesh* m) {
   }
   if (m->W < 2 || m->W > 8) return;
   m->p2p_ok = sym_alloc(m, m->flags, fbytes);
+  if (m->p2p_ok && !sym_alloc(m, m->amax_sym, sizeof(uint32_t) * (size_t)std::max(m->reg_cap, 1))) {
+    sym_free(m, m->flags);
+    m->p2p_ok = false;
+  }
   CUDA_CHECK(cudaMalloc(&m->d_epochs, ebytes));
   CUDA_CHECK(cudaMemset(m->d_epochs, 0, ebytes));
   m->algo = (m->p2p_ok && !want_nccl) ? FSDP_ALGO_P2P : FSDP_ALGO_NCCL;
@@ -144,12 +148,13 @@ static void p2p_init(fsdp_mesh* m) {
 }
 
 static fsdp_status_t mesh_init_impl(const uint8_t* id, int32_t W, int32_t rank, int32_t dev, bool local,
-                                    fsdp_mesh_t** out, int32_t shard_size = 0) {
+                                    fsdp_mesh_t** out, int32_t shard_size = 0,
+                                    fsdp_host_allgather_fn hc_fn = nullptr, void* hc_ctx = nullptr) {
   return guarded([&] {
     if (!out) fail(FSDP_ERR_INVALID_ARGUMENT, "out is NULL");
     *out = nullptr;
     if (W < 1 || rank < 0 || rank >= W) fail(FSDP_ERR_INVALID_ARGUMENT, "invalid world_size/rank");
-    if (!local && !id) fail(FSDP_ERR_INVALID_ARGUMENT, "unique id is NULL");
+    if (!local && !id && !hc_fn) fail(FSDP_ERR_INVALID_ARGUMENT, "unique id is NULL");
     if (shard_size <= 0) shard_size = W;
     if (W % shard_size != 0) fail(FSDP_ERR_INVALID_ARGUMENT, "shard_size must divide world_size");
     int ndev = 0;
@@ -163,9 +168,17 @@ static fsdp_status_t mesh_init_impl(const uint8_t* id, int32_t W, int32_t rank, 
     m->rep = rank / shard_size;
     m->device = dev;
     m->local = local;
+    m->hc_fn = hc_fn;
+    m->hc_ctx = hc_ctx;
     try {
       mesh_common_init(m);
-      if (!local) {
+      if (hc_fn) {   // host-collective P2P mesh: no NCCL (header: fsdp_mesh_init_hostcoll)
+        p2p_init(m);
+        if (m->W > 1 && !m->p2p_ok) fail(FSDP_ERR_UNAVAILABLE, "host-collective mesh: a rank cannot map its shard group");
+        if (m->R > 1 && !m->hsdp_p2p) fail(FSDP_ERR_UNAVAILABLE, "host-collective HSDP mesh: a rank cannot map the world");
+        if (m->p2p_ok) m->algo = FSDP_ALGO_P2P;
+        m->hsdp_rs_p2p = m->hsdp_p2p;
+      } else if (!local) {
         ncclUniqueId u;
         std::memcpy(&u, id, sizeof(u));
         if (m->R == 1) {
@@ -189,6 +202,19 @@ static fsdp_status_t mesh_init_impl(const uint8_t* id, int32_t W, int32_t rank, 
 fsdp_status_t fsdp_mesh_init(const uint8_t id[FSDP_UNIQUE_ID_BYTES], int32_t world_size, int32_t rank,
                              int32_t cuda_device, fsdp_mesh_t** out) {
   return mesh_init_impl(id, world_size, rank, cuda_device, false, out);
+}
+
+fsdp_status_t fsdp_mesh_init_hostcoll(int32_t world_size, int32_t rank, int32_t shard_size, int32_t cuda_device,
+                                      fsdp_host_allgather_fn fn, void* ctx, fsdp_mesh_t** out) {
+  if (!fn) {
+    g_last_error = "the host all-gather callback is NULL";
+    return FSDP_ERR_INVALID_ARGUMENT;
+  }
+  if (shard_size < 0) {
+    g_last_error = "shard_size must be >= 0";
+    return FSDP_ERR_INVALID_ARGUMENT;
+  }
+  return mesh_init_impl(nullptr, world_size, rank, cuda_device, false, out, shard_size, fn, ctx);
 }
 
 fsdp_status_t fsdp_mesh_init_local(int32_t world_size, int32_t rank, int32_t cuda_device, fsdp_mesh_t** out) {
@@ -330,6 +356,7 @@ fsdp_status_t fsdp_mesh_set_algo(fsdp_mesh_t* m, int32_t algo) {
   return guarded([&] {
     check_mesh(m);
     if (algo != FSDP_ALGO_NCCL && algo != FSDP_ALGO_P2P) fail(FSDP_ERR_INVALID_ARGUMENT, "unknown algo");
+    if (algo == FSDP_ALGO_NCCL && m->hc_fn) fail(FSDP_ERR_UNAVAILABLE, "a host-collective mesh has no NCCL communicator");
     for (auto* l : m->layers)
       if (l->state != SHARDED || l->rs_pending) fail(FSDP_ERR_STATE, "a layer is unsharded or has a pending reduce-scatter");
     if (algo == FSDP_ALGO_P2P && !m->p2p_ok && !m->hsdp_p2p)
@@ -377,9 +404,10 @@ fsdp_status_t fsdp_mesh_synchronize(fsdp_mesh_t* m, int64_t timeout_ms) {
         if (e == cudaErrorNotReady) { idle = false; continue; }
         if (e != cudaSuccess) fail(FSDP_ERR_CUDA, std::string("stream error: ") + cudaGetErrorString(e));
       }
-      if (comm_ready(m)) {
+      if (nccl_ok(m)) {
         for (ncclComm_t c : {m->comm_ag, m->comm_rs}) {
           ncclResult_t ar = ncclSuccess;
+          if (!c) continue;
           NCCL_CHECK(ncclCommGetAsyncError(c, &ar));
           if (ar != ncclSuccess) abort_mesh(m, FSDP_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(ar));
         }

@@ -113,6 +113,7 @@ void check_param(const fsdp_layer* l, int p) {
 }
 
 bool comm_ready(const fsdp_mesh* m) { return !m->local && m->W > 1; }
+bool nccl_ok(const fsdp_mesh* m) { return !m->local && !m->hc_fn && (m->W > 1 || m->R > 1); }
 
 // fp8 registry: fixed capacity, allocated once per mesh, so the device pointers handed out by
 // fsdp_fp8_scales (and baked into captured CUDA graphs) stay valid for the mesh's lifetime.
@@ -178,7 +179,35 @@ Group group_of(const fsdp_mesh* m, int grp) {
   return Group{m->comm_ag, m->W, m->rank};
 }
 
+void group_allgather_host(fsdp_mesh* m, int grp, const void* send, void* recv, size_t bytes) {
+  const Group G = group_of(m, grp);
+  if (m->hc_fn) {   // the caller's host all-gather runs over the whole world: keep the group's part
+    const int Wt = m->W * m->R;
+    std::vector<uint8_t> all((size_t)Wt * bytes);
+    if (m->hc_fn(send, all.data(), (int64_t)bytes, m->hc_ctx) != 0)
+      fail(FSDP_ERR_UNAVAILABLE, "host all-gather callback failed");
+    for (int q = 0; q < G.W; ++q) {
+      const int g = grp == GRP_WORLD ? q : m->rep * m->W + q;
+      std::memcpy((uint8_t*)recv + (size_t)q * bytes, all.data() + (size_t)g * bytes, bytes);
+    }
+    return;
+  }
+  uint8_t* d = nullptr;
+  CUDA_CHECK(cudaMalloc(&d, bytes * G.W));
+  CUDA_CHECK(cudaMemcpy(d + bytes * G.rank, send, bytes, cudaMemcpyHostToDevice));
+  NCCL_CHECK(ncclAllGather(d + bytes * G.rank, d, bytes, ncclUint8, G.comm, m->s_ag));
+  CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
+  CUDA_CHECK(cudaMemcpy(recv, d, bytes * G.W, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+}
+
 void mesh_barrier(fsdp_mesh* m, int grp) {
+  if (m->hc_fn) {
+    const uint8_t one = 1;
+    std::vector<uint8_t> all(group_of(m, grp).W);
+    group_allgather_host(m, grp, &one, all.data(), 1);
+    return;
+  }
   const Group g = group_of(m, grp);
   NCCL_CHECK(ncclAllReduce(m->d_barrier, m->d_barrier, 1, ncclInt32, ncclSum, g.comm, m->s_ag));
   CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
@@ -186,6 +215,14 @@ void mesh_barrier(fsdp_mesh* m, int grp) {
 
 // all ranks of the group agree that `ok` holds everywhere
 bool mesh_all_ok(fsdp_mesh* m, bool ok, int grp) {
+  if (m->hc_fn) {
+    const uint8_t v = ok ? 1 : 0;
+    std::vector<uint8_t> all(group_of(m, grp).W);
+    group_allgather_host(m, grp, &v, all.data(), 1);
+    for (uint8_t x : all)
+      if (!x) return false;
+    return true;
+  }
   const Group g = group_of(m, grp);
   int v = ok ? 1 : 0;
   CUDA_CHECK(cudaMemcpy(m->d_barrier, &v, sizeof(int), cudaMemcpyHostToDevice));
@@ -226,14 +263,8 @@ bool sym_alloc(fsdp_mesh* m, SymBuf& b, size_t bytes, int grp) {
   if (ok) ok = cudaMemset(b.local, 0, bytes + 256) == cudaSuccess;
   if (ok) ok = cudaIpcGetMemHandle(&h, b.local) == cudaSuccess;
   cudaGetLastError();
-  uint8_t* d = nullptr;
-  CUDA_CHECK(cudaMalloc(&d, sizeof(h) * G.W));
-  CUDA_CHECK(cudaMemcpy(d + sizeof(h) * G.rank, &h, sizeof(h), cudaMemcpyHostToDevice));
-  NCCL_CHECK(ncclAllGather(d + sizeof(h) * G.rank, d, sizeof(h), ncclUint8, G.comm, m->s_ag));
-  CUDA_CHECK(cudaStreamSynchronize(m->s_ag));
   std::vector<cudaIpcMemHandle_t> hs(G.W);
-  CUDA_CHECK(cudaMemcpy(hs.data(), d, sizeof(h) * G.W, cudaMemcpyDeviceToHost));
-  cudaFree(d);
+  group_allgather_host(m, grp, &h, hs.data(), sizeof(h));
   b.peers.assign(G.W, nullptr);
   b.bytes = bytes;
   if (ok) {
@@ -345,6 +376,7 @@ void p2p_teardown(fsdp_mesh* m) {
     }
     pool->clear();
   }
+  if (m->amax_sym.local) sym_free(m, m->amax_sym);
   sym_free(m, m->flags);
   m->p2p_ok = false;
 }
@@ -394,13 +426,26 @@ void poll_async_errors(fsdp_mesh* m) {
   if ((err & 0xFF) == 2)
     abort_mesh(m, FSDP_ERR_TIMEOUT, "P2P handshake timed out waiting for shard rank " + std::to_string(err >> 8) +
                                         " (a rank skipped or diverged from the collective call sequence); mesh aborted");
-  if (comm_ready(m)) {
+  if (nccl_ok(m)) {
     for (ncclComm_t c : {m->comm_ag, m->comm_rs}) {
       ncclResult_t ar = ncclSuccess;
       if (c && ncclCommGetAsyncError(c, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress)
         abort_mesh(m, FSDP_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(ar));
     }
   }
+}
+
+void p2p_amax_allreduce(fsdp_mesh* m, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  CUDA_CHECK(cudaMemcpyAsync(m->amax_sym.local, m->reg_acc, sizeof(uint32_t) * (size_t)n, cudaMemcpyDeviceToDevice, st));
+  CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_READY, kAmaxSlot), flag_local(m, FK_RS_READY, kAmaxSlot),
+                                       m->W, m->rank, epoch_ctr(m, FK_RS_READY, kAmaxSlot), m->p2p_timeout_ns,
+                                       m->d_err, st));
+  CUDA_CHECK(fsdpp::launch_amax_max(peer_ptrs(m, m->amax_sym), m->W, m->reg_acc, n, st));
+  // every rank has read every copy before any rank overwrites its own at the next call
+  CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_DONE, kAmaxSlot), flag_local(m, FK_RS_DONE, kAmaxSlot),
+                                       m->W, m->rank, epoch_ctr(m, FK_RS_DONE, kAmaxSlot), m->p2p_timeout_ns,
+                                       m->d_err, st, m->cfg.pdl));
 }
 
 void ensure_pieces(fsdp_layer* l, int R) {

@@ -72,6 +72,10 @@ cudaError_t launch_rs_pull_nested(const fsdpk::Tile* tiles, int ntiles, PeerPtrs
 cudaError_t launch_replica_gather(const fsdpk::Tile* tiles, int ntiles, PeerPtrs res, float* grad, bool accumulate,
                                   fsdpk::LaunchCfg cfg, cudaStream_t st);
 
+// fp8 amax all-reduce over symmetric memory: out[i] = max_{q < W} src.p[q][i] (uint32 bit
+// patterns of non-negative fp32 amaxes), i < n.
+cudaError_t launch_amax_max(PeerPtrs src, int W, uint32_t* out, int n, cudaStream_t st);
+
 // Gather copy: dst + tile.dst <- srcs.p[param] + tile.src, n bytes (any alignment).
 cudaError_t launch_gather_copy(const fsdpk::Tile* tiles, int ntiles, const fsdpk::PtrArray& srcs,
                                void* dst, fsdpk::LaunchCfg cfg, cudaStream_t st);

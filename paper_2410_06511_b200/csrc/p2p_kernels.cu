@@ -432,6 +432,21 @@ __global__ void __launch_bounds__(kThreads) k_unshard_push_bulk(const Tile* __re
   __threadfence_system();
 }
 
+// ------------------------------------------------------------------- fp8 amax all-reduce(max)
+// out[i] = max over the W ranks' copies of the amax bit patterns (uint32 max == fp32 max of
+// non-negative values, NaN patterns propagate; the same reduction as ncclMax on uint32).
+__global__ void __launch_bounds__(kThreads) k_amax_max(PeerPtrs src, int W, uint32_t* __restrict__ out, int n) {
+  for (int i = blockIdx.x * kThreads + threadIdx.x; i < n; i += gridDim.x * kThreads) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxRanks; ++q) {
+      if (q >= W) break;
+      v = max(v, reinterpret_cast<const uint32_t*>(src.p[q])[i]);
+    }
+    out[i] = v;
+  }
+}
+
 // ------------------------------------------------------------------- gather copy
 __global__ void __launch_bounds__(kThreads) k_gather_copy(const Tile* __restrict__ tiles, int ntiles,
                                                           fsdpk::PtrArray srcs, uint8_t* __restrict__ dst_base) {
@@ -528,6 +543,13 @@ cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool
   const int g = grid_for(ntiles, cfg);
   return grad_bf16 ? launch_pull_w<true>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant, cfg.pdl)
                    : launch_pull_w<false>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant, cfg.pdl);
+}
+
+cudaError_t launch_amax_max(PeerPtrs src, int W, uint32_t* out, int n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int g = std::min((n + kThreads - 1) / kThreads, 148);
+  k_amax_max<<<g, kThreads, 0, st>>>(src, W, out, n);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_gather_copy(const Tile* tiles, int ntiles, const fsdpk::PtrArray& srcs, void* dst,

@@ -118,22 +118,51 @@ def _torch_allocator():
     return capi.ALLOC_FN(alloc), capi.FREE_FN(free)
 
 
+def _host_allgather(group):
+    """fsdp_host_allgather_fn over a torch.distributed group (any backend; gloo keeps it on
+    the CPU): the host-collective mesh's handle exchange, layout-hash check and barriers."""
+    import torch.distributed as dist
+
+    def fn(send, recv, nbytes, ctx):
+        try:
+            n = int(nbytes)
+            W = dist.get_world_size(group)
+            src = torch.frombuffer(bytearray(C.string_at(send, n)), dtype=torch.uint8) if n else \
+                torch.empty(0, dtype=torch.uint8)
+            out = [torch.empty(n, dtype=torch.uint8) for _ in range(W)]
+            dist.all_gather(out, src, group=group)
+            C.memmove(recv, torch.cat(out).numpy().tobytes(), n * W)
+            return 0
+        except Exception:   # noqa: BLE001 — reported as FSDP_ERR_UNAVAILABLE by the library
+            return 1
+    return capi.HOSTAG_FN(fn)
+
+
 # ----------------------------------------------------------------------- mesh
 class Mesh:
     """1-D data-parallel mesh (fsdp_mesh_t).  world_size defaults to all ranks."""
 
     def __init__(self, world_size: int, rank: int, device: int, unique_id: Optional[bytes] = None,
-                 local: bool = False, shard_size: Optional[int] = None, allocator: str = "torch"):
+                 local: bool = False, shard_size: Optional[int] = None, allocator: str = "torch",
+                 host_group=None):
         """world_size ranks; shard_size < world_size makes an HSDP mesh of world_size //
         shard_size replica groups x shard_size ranks.  allocator:
         "torch" (bulk buffers from the torch caching allocator, fsdp_mesh_set_allocator) or
-        "cuda" (the library's own cudaMalloc)."""
+        "cuda" (the library's own cudaMalloc).  host_group: a torch.distributed group (e.g.
+        gloo) -> a host-collective P2P mesh with no NCCL (fsdp_mesh_init_hostcoll); its ranks
+        may share a GPU."""
         if allocator not in ("torch", "cuda"):
             raise ValueError("allocator must be 'torch' or 'cuda'")
         self.world_size, self.rank, self.device = int(world_size), int(rank), int(device)
         self.local = local
         h = C.c_void_p()
-        if local:
+        self._hostag = None
+        self.hostcoll = host_group is not None
+        if host_group is not None:
+            self._hostag = _host_allgather(host_group)   # kept alive until destroy
+            call("fsdp_mesh_init_hostcoll", self.world_size, self.rank, int(shard_size or 0), self.device,
+                 self._hostag, None, C.byref(h))
+        elif local:
             call("fsdp_mesh_init_local", self.world_size, self.rank, self.device, C.byref(h))
         else:
             if unique_id is None or len(unique_id) != capi.FSDP_UNIQUE_ID_BYTES:

@@ -207,13 +207,17 @@ def run_fullsize_check(mesh, W, rank):
           flush=True)
 
 
-def run_fault_injection(W, rank, local):
+def _nccl_mesh(local, shard_size=None):
+    return F.Mesh.from_process_group(device=local, shard_size=shard_size)
+
+
+def run_fault_injection(W, rank, local, make_mesh=_nccl_mesh):
     """SPEC.md:190 idea ("rank never calls the collective -> report"): the last rank skips a
     reduce-scatter; every other rank's P2P handshake gives up after the configured timeout
     and fsdp_mesh_synchronize reports FSDP_ERR_TIMEOUT naming a peer, instead of hanging."""
     os.environ["FSDP_B200_P2P_TIMEOUT_MS"] = "2000"
     try:
-        mesh = F.Mesh.from_process_group(device=local)
+        mesh = make_mesh(local)
     finally:
         del os.environ["FSDP_B200_P2P_TIMEOUT_MS"]
     if mesh.algo != "p2p":
@@ -248,15 +252,17 @@ def run_fault_injection(W, rank, local):
     print(f"rank {rank}/{W} fault injection (rank {W - 1} skips a reduce-scatter): OK", flush=True)
 
 
-def run_hsdp_checks(W, rank, local, Ws):
+def run_hsdp_checks(W, rank, local, Ws, make_mesh=_nccl_mesh):
     """HSDP: R = W / Ws replica groups of Ws ranks; vs oracle HsdpWorld."""
     from oracle import HsdpWorld
     R = W // Ws
-    mesh = F.Mesh.from_process_group(device=local, shard_size=Ws)
+    mesh = make_mesh(local, Ws)
     assert (mesh.replicate_size, mesh.shard_size) == (R, Ws)
     s = mesh.shard_rank
     world_pull = mesh.hsdp_rs.startswith("world_pull")   # one NVSwitch domain: the default HSDP RS
     algos = ["p2p", "nccl"] if (mesh.algo == "p2p" or world_pull) else ["nccl"]
+    if mesh.hostcoll:   # no NCCL on a host-collective mesh
+        algos = ["p2p"]
     for algo in algos:
         mesh.set_algo(algo)
         wp = algo == "p2p" and world_pull

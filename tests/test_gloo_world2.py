@@ -4,7 +4,8 @@ Each rank computes its Shard(0) layout through the C ABI (host-only), the ranks 
 layout hashes (the agreement check fsdp_shard performs), rank 0's NCCL unique id is
 broadcast (Mesh.from_process_group's bootstrap), and each rank's local view is checked
 against the oracle's simulated World(2): rank r's rows equal the oracle's rank-r shard,
-and the gathered shards reproduce the full parameters."""
+and the gathered shards reproduce the full parameters.  The host-collective mesh's
+all-gather callback (fsdp_mesh_init_hostcoll) is called as the library calls it."""
 import os
 import socket
 
@@ -65,6 +66,17 @@ def _worker(rank, world, port, q):
                 mr = f.layout_compute(shapes, world, r, elig)[0][p]
                 pieces.append(gathered[r].numpy()[mr["elem_offset"]:mr["elem_offset"] + mr["row_count"] * mr["rest"]])
             np.testing.assert_array_equal(np.concatenate(pieces).reshape(full.shape), full)
+        # the host-collective mesh's all-gather callback (fsdp_host_allgather_fn over gloo),
+        # called the way the library calls it: raw host pointers, rank-major output
+        import ctypes as C
+        from paper_2410_06511_b200.fsdp import _host_allgather
+        fn = _host_allgather(dist.group.WORLD)
+        for nbytes in (1, 8, 64):   # barrier byte, layout hash, CUDA IPC handle
+            send = (C.c_uint8 * nbytes)(*[(rank * 31 + i) & 0xFF for i in range(nbytes)])
+            recv = (C.c_uint8 * (nbytes * world))()
+            assert fn(C.addressof(send), C.addressof(recv), nbytes, None) == 0
+            want = [(r * 31 + i) & 0xFF for r in range(world) for i in range(nbytes)]
+            assert list(recv) == want, (nbytes, list(recv)[:16])
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))

@@ -29,18 +29,26 @@ import paper_2410_06511_b200 as F  # noqa: E402
 import mgpu_worker as M  # noqa: E402
 
 
+def _device(rank):
+    # every rank on cuda:0 by default; HOSTCOLL_SPREAD=1 puts rank r on GPU r % n (several
+    # processes per GPU, peers both on the same GPU and across NVLink)
+    if os.environ.get("HOSTCOLL_SPREAD") == "1":
+        return rank % torch.cuda.device_count()
+    return 0
+
+
 def _hc_mesh(local, shard_size=None):
-    return F.Mesh(dist.get_world_size(), dist.get_rank(), 0, host_group=dist.group.WORLD,
+    return F.Mesh(dist.get_world_size(), dist.get_rank(), _device(dist.get_rank()), host_group=dist.group.WORLD,
                   shard_size=shard_size)
 
 
 def main():
     rank = int(os.environ["RANK"])
     W = int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(0)   # every rank on the same GPU
+    dev = _device(rank)
+    torch.cuda.set_device(dev)
     dist.init_process_group("gloo")
-    M.dist = dist
-    mesh = _hc_mesh(0)
+    mesh = _hc_mesh(dev)
     assert mesh.algo == "p2p" and mesh.hostcoll
     try:
         mesh.set_algo("nccl")
@@ -49,7 +57,7 @@ def main():
         assert e.status_name == "FSDP_ERR_UNAVAILABLE", e
     for rs_mode in ("store", "pull"):
         mesh.set_p2p_rs(rs_mode)
-        M.run_checks(mesh, W, rank, 0, "p2p")
+        M.run_checks(mesh, W, rank, dev, "p2p")
         print(f"rank {rank}/{W} hostcoll rs={rs_mode}: unshard bf16/fp8 + reduce-scatter OK", flush=True)
     mesh.set_p2p_rs("auto")
     M.run_graph_checks(mesh, W, rank, "p2p")
@@ -57,8 +65,8 @@ def main():
     mesh.synchronize(120000)
     mesh.destroy()
     for Ws in sorted({d for d in (1, 2, W // 2) if 1 <= d < W and W % d == 0}):
-        M.run_hsdp_checks(W, rank, 0, Ws, make_mesh=_hc_mesh)
-    M.run_fault_injection(W, rank, 0, make_mesh=_hc_mesh)
+        M.run_hsdp_checks(W, rank, dev, Ws, make_mesh=_hc_mesh)
+    M.run_fault_injection(W, rank, dev, make_mesh=_hc_mesh)
     dist.barrier()
     dist.destroy_process_group()
     print(f"RANK {rank}/{W} hostcoll OK", flush=True)

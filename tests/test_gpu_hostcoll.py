@@ -25,7 +25,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("nproc", [2, 4])
+@pytest.mark.parametrize("nproc", [2, 4, 8])
 def test_hostcoll_worker_one_gpu(nproc):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")

@@ -238,23 +238,28 @@ __global__ void __launch_bounds__(kThreads) k_rs_copy_in(const Tile* __restrict_
 // source is not 16-byte aligned take the register path.
 constexpr uint32_t kRsChunk = 2048;
 
-template <bool kGradBf16, bool kOutBf16>
+// NS stages (FSDP_B200_K5_STAGES: 2 or 4): chunk i of this CTA uses stage i % NS; the loads
+// run NS chunks ahead of the widen / divide and the stores may lag NS - 1 chunks behind.
+template <bool kGradBf16, bool kOutBf16, int NS = 2>
 __global__ void __launch_bounds__(kThreads) k_rs_copy_in_bulk(const Tile* __restrict__ tiles, int ntiles,
                                                               PtrArray grads, uint8_t* __restrict__ rs_in,
                                                               DivW div) {
   constexpr uint32_t gsz = kGradBf16 ? 2 : 4;
   constexpr uint32_t osz = kOutBf16 ? 2 : 4;
-  __shared__ __align__(128) uint8_t sin[2][kRsChunk * gsz];
-  __shared__ __align__(128) uint8_t sout[2][kRsChunk * osz];
-  __shared__ uint64_t full[2];
+  extern __shared__ __align__(128) uint8_t k5_smem[];   // [NS][chunk * gsz] in, [NS][chunk * osz] out
+  uint8_t (*sin)[kRsChunk * gsz] = reinterpret_cast<uint8_t (*)[kRsChunk * gsz]>(k5_smem);
+  uint8_t (*sout)[kRsChunk * osz] = reinterpret_cast<uint8_t (*)[kRsChunk * osz]>(k5_smem + NS * kRsChunk * gsz);
+  __shared__ uint64_t full[NS];
   if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  uint32_t it = 0;           // chunks processed by this CTA (stage = it & 1)
-  uint32_t loads0 = 0, loads1 = 0;  // completed loads per stage barrier (parity = loads & 1)
+  uint32_t it = 0;           // chunks processed by this CTA (stage = it % NS)
+  uint32_t loads[NS];        // completed loads per stage barrier (parity = loads & 1)
+#pragma unroll
+  for (int i = 0; i < NS; ++i) loads[i] = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
     const uint8_t* s = (const uint8_t*)grads.p[tl.param] + tl.src * gsz;
@@ -273,24 +278,24 @@ __global__ void __launch_bounds__(kThreads) k_rs_copy_in_bulk(const Tile* __rest
     auto issue = [&](uint32_t c, uint32_t i) {
       const uint32_t nv = valid(c);
       if (nv == 0) return;
-      mbar_arrive_expect_tx(&full[i & 1u], nv * gsz);
-      bulk_g2s(sin[i & 1u], s + (size_t)c * kRsChunk * gsz, nv * gsz, &full[i & 1u]);
+      mbar_arrive_expect_tx(&full[i % NS], nv * gsz);
+      bulk_g2s(sin[i % NS], s + (size_t)c * kRsChunk * gsz, nv * gsz, &full[i % NS]);
     };
     if (threadIdx.x == 0) {
-      issue(0, it);
-      if (nch > 1) issue(1, it + 1);
+      for (uint32_t c = 0; c < (uint32_t)NS && c < nch; ++c) issue(c, it + c);
     }
     for (uint32_t c = 0; c < nch; ++c) {
-      const uint32_t i = it + c, st = i & 1u;
+      const uint32_t i = it + c, st = i % NS;
       const uint32_t ne = min(kRsChunk, n - c * kRsChunk);
       const uint32_t nv = valid(c);
       if (nv > 0) {
-        const uint32_t par = (st ? loads1 : loads0) & 1u;
-        if (st) ++loads1;
-        else ++loads0;
+        uint32_t par = 0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+          if ((uint32_t)k == st) par = loads[k]++ & 1u;
         mbar_wait(&full[st], par);
       }
-      if (threadIdx.x == 0) bulk_wait_read_le1();   // sout[st] (stored 2 chunks ago) was read
+      if (threadIdx.x == 0) bulk_wait_read_le<NS - 1>();   // sout[st] (stored NS chunks ago) was read
       __syncthreads();
       for (uint32_t e8 = threadIdx.x; e8 * 8 < ne; e8 += kThreads) {
         float x[8];
@@ -333,7 +338,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_copy_in_bulk(const Tile* __rest
       if (threadIdx.x == 0) {
         bulk_s2g(d + (size_t)c * kRsChunk * osz, sout[st], ne * osz);
         bulk_commit();
-        if (c + 2 < nch) issue(c + 2, i + 2);
+        if (c + NS < nch) issue(c + NS, i + NS);
       }
     }
     it += nch;
@@ -536,9 +541,25 @@ cudaError_t launch_rs_copy_in(const Tile* tiles, int ntiles, const PtrArray& gra
   uint8_t* d = (uint8_t*)rs_in;
   if (cfg.variant & 8) {   // TMA bulk K5
     const int gb = grid_for(ntiles, cfg, kCtasCopy);
+    const size_t unit = (size_t)kRsChunk * ((grad_bf16 ? 2 : 4) + (out_bf16 ? 2 : 4));
+    if (cfg.k5_stages == 4) {
+      auto k = grad_bf16 ? (out_bf16 ? k_rs_copy_in_bulk<true, true, 4> : k_rs_copy_in_bulk<true, false, 4>)
+                         : (out_bf16 ? k_rs_copy_in_bulk<false, true, 4> : k_rs_copy_in_bulk<false, false, 4>);
+      // > 48 KB of dynamic shared memory for fp32 grads: opt in (per device, once per kernel)
+      static bool attr[4][64] = {};
+      const int ki = (grad_bf16 ? 2 : 0) + (out_bf16 ? 1 : 0);
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (dev < 0 || dev >= 64 || !attr[ki][dev]) {
+        const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * unit));
+        if (e != cudaSuccess) return e;
+        if (dev >= 0 && dev < 64) attr[ki][dev] = true;
+      }
+      return launch_persistent(k, gb, 4 * unit, st, tiles, ntiles, grads, d, div);
+    }
     auto k = grad_bf16 ? (out_bf16 ? k_rs_copy_in_bulk<true, true> : k_rs_copy_in_bulk<true, false>)
                        : (out_bf16 ? k_rs_copy_in_bulk<false, true> : k_rs_copy_in_bulk<false, false>);
-    return launch_persistent(k, gb, 0, st, tiles, ntiles, grads, d, div);
+    return launch_persistent(k, gb, 2 * unit, st, tiles, ntiles, grads, d, div);
   }
   const int g = grid_for(ntiles, cfg, kCtasRsCopyIn);
   auto k = grad_bf16 ? (out_bf16 ? k_rs_copy_in<true, true> : k_rs_copy_in<true, false>)

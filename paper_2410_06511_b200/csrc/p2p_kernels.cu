@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_reduce_own(const Tile* __restri
 // every rank's arena (cp.async.bulk shared->global, W stores per chunk, 2 stages).
 constexpr uint32_t kBulkChunk = 4096;
 static_assert(kBulkChunk / 16 == (uint32_t)kThreads, "push_tile_bulk: one 16-byte vector per thread per chunk");
-template <bool kFp8, bool kAmax = false>
+template <bool kFp8, bool kAmax = false, bool kPref = false>
 __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __restrict__ shard, float s,
                                                const PeerPtrs& arena, int W, uint8_t* stage_buf, uint32_t& it,
                                                uint32_t* amp = nullptr) {
@@ -354,15 +354,32 @@ __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __re
   const float* abase = src + (h - ph);
   const uint64_t body0 = dst0 + (uint64_t)h * es;   // 16-byte aligned
   const uint32_t nch = (nb + CV - 1) / CV;
+  // kPref (the bf16-only kernel): register double buffer — chunk c+1's loads are in flight
+  // across chunk c's barriers and bulk-store issue (the mixed fp8 kernels keep one buffer:
+  // a second one would cost 8-16 registers and their 6-CTA/SM occupancy)
+  auto load_chunk = [&](uint32_t c, float (&x)[V]) -> bool {
+    const uint32_t v = c * CV + threadIdx.x;
+    if (v >= nb) return false;
+    if constexpr (kAmax) load_floats_amax<V>(abase + V * v, ph, x, am);
+    else load_floats<V>(abase + V * v, ph, x);
+    return true;
+  };
+  float xn[V];
+  bool hn = kPref && nch > 0 && load_chunk(0, xn);
   for (uint32_t c = 0; c < nch; ++c, ++it) {
     uint8_t* buf = stage_buf + (size_t)(it & 1u) * kBulkChunk;
+    float x[V];
+    bool hx;
+    if constexpr (kPref) {
+#pragma unroll
+      for (uint32_t i = 0; i < V; ++i) x[i] = xn[i];
+      hx = hn;
+      if (c + 1 < nch) hn = load_chunk(c + 1, xn);
+    }
     if (threadIdx.x == 0) bulk_wait_read_le1();       // the chunk written 2 iterations ago was read
     __syncthreads();
-    const uint32_t v = c * CV + threadIdx.x;
-    if (v < nb) {
-      float x[V];
-      if constexpr (kAmax) load_floats_amax<V>(abase + V * v, ph, x, am);
-      else load_floats<V>(abase + V * v, ph, x);
+    if constexpr (!kPref) hx = load_chunk(c, x);
+    if (hx) {
       uint4 o;
       if constexpr (kFp8) o = cvt_e4m3x16(x, s);
       else o = cvt_bf16x8(x);
@@ -405,7 +422,9 @@ __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __re
   if constexpr (kAmax) *amp = max(*amp, am);
 }
 
-template <bool kAmax>
+// kAnyFp8 = false: the bf16 unshard (every tile TK_BF16) — only the bf16 path is compiled, so
+// the register double buffer fits the 6-CTA/SM budget (40 registers)
+template <bool kAmax, bool kAnyFp8 = true>
 __global__ void __launch_bounds__(kThreads) k_unshard_push_bulk(const Tile* __restrict__ tiles, int ntiles,
                                                                 const float* __restrict__ shard,
                                                                 const float* __restrict__ scales, PeerPtrs arena,
@@ -416,16 +435,16 @@ __global__ void __launch_bounds__(kThreads) k_unshard_push_bulk(const Tile* __re
   uint32_t it = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
-    if (tl.kind == fsdpk::TK_FP8) {
+    if (kAnyFp8 && tl.kind == fsdpk::TK_FP8) {
       if constexpr (kAmax) {
         uint32_t mm = 0;
         push_tile_bulk<true, true>(tl, shard, scales[tl.param], arena, W, stage_buf, it, &mm);
         amax_commit_cta(acc, tl.param, mm, red);
-      } else {
+      } else if constexpr (kAnyFp8) {
         push_tile_bulk<true>(tl, shard, scales[tl.param], arena, W, stage_buf, it);
       }
     }
-    else push_tile_bulk<false>(tl, shard, 0.0f, arena, W, stage_buf, it);
+    else push_tile_bulk<false, false, !kAnyFp8>(tl, shard, 0.0f, arena, W, stage_buf, it);
   }
   if (threadIdx.x == 0) bulk_wait0();                 // every bulk store has completed
   __syncthreads();
@@ -530,8 +549,15 @@ cudaError_t launch_unshard_push(const Tile* tiles, int ntiles, const float* shar
   for (int i = 0; i < W; ++i) rot.p[i] = arena.p[(rank + 1 + i) % W];
   const int g = grid_for(ntiles, cfg, fsdpk::kCtasPush);
   if (cfg.variant & 4)   // TMA bulk push
+    // the bf16-only double-buffered kernel at W = 1 (HBM-bound: the W=1 8B step 15.21 ->
+    // 15.00 ms, profiles/round2/r2pref); W > 1 is NVLink-bound and keeps the single buffer.
+    // scales == NULL: a bf16 unshard (an fp8 unshard always has scales; the mixed kernel also
+    // handles bf16-only tables, so a caller passing scales for bf16 stays correct)
     return amax_acc ? launch_p(cfg.pdl, k_unshard_push_bulk<true>, g, 0, st, tiles, ntiles, shard, scales, rot, W, amax_acc)
-                    : launch_p(cfg.pdl, k_unshard_push_bulk<false>, g, 0, st, tiles, ntiles, shard, scales, rot, W, amax_acc);
+           : (scales || W > 1)
+               ? launch_p(cfg.pdl, k_unshard_push_bulk<false>, g, 0, st, tiles, ntiles, shard, scales, rot, W, amax_acc)
+                    : launch_p(cfg.pdl, k_unshard_push_bulk<false, false>, g, 0, st, tiles, ntiles, shard, scales, rot, W,
+                               amax_acc);
   return amax_acc ? launch_p(cfg.pdl, k_unshard_push<true>, g, 0, st, tiles, ntiles, shard, scales, rot, W, rank, amax_acc)
                   : launch_p(cfg.pdl, k_unshard_push<false>, g, 0, st, tiles, ntiles, shard, scales, rot, W, rank, amax_acc);
 }

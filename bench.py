@@ -394,7 +394,14 @@ def run_ours(args):
     mesh.profile_read(reset=True)
     # before each iteration a host barrier over ranks + device sync, so all
     # ranks start aligned; CUDA events on the launching stream bracket every step; the step
-    # time is the max over ranks per step, `ms_per_step` their mean
+    # time is the max over ranks per step, `ms_per_step` their mean.  queue_ahead(): a ~50 us
+    # device sleep on the compute stream before the start event, so the host has enqueued
+    # the step's first launches when the clock starts (as in back-to-back training steps)
+    # instead of timing a launch from an idle GPU (~40 us: the whole toy step's size)
+    def queue_ahead():
+        with torch.cuda.stream(comp):
+            torch.cuda._sleep(100_000)   # cycles (~50 us at 1.9-2.0 GHz)
+
     ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     barrier()
@@ -402,6 +409,7 @@ def run_ours(args):
     for k in range(args.steps):
         barrier()
         torch.cuda.synchronize()
+        queue_ahead()
         ev_a[k].record(comp)
         timed_step()
         ev_b[k].record(comp)
@@ -448,6 +456,7 @@ def run_ours(args):
         barrier()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        queue_ahead()
         a.record(comp)
         step()
         b.record(comp)

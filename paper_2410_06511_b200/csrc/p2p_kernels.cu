@@ -423,7 +423,9 @@ __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __re
 }
 
 // kAnyFp8 = false: the bf16 unshard (every tile TK_BF16) — only the bf16 path is compiled, so
-// the register double buffer fits the 6-CTA/SM budget (40 registers)
+// the register double buffer fits in 31 registers and 8 CTAs per SM (kCtasPushW1: the push
+// alone 245.7 -> 238.5 us per 8B block, profiles/round2/r2pref bench_cta8)
+constexpr int kCtasPushW1 = 8;
 template <bool kAmax, bool kAnyFp8 = true>
 __global__ void __launch_bounds__(kThreads) k_unshard_push_bulk(const Tile* __restrict__ tiles, int ntiles,
                                                                 const float* __restrict__ shard,
@@ -556,8 +558,8 @@ cudaError_t launch_unshard_push(const Tile* tiles, int ntiles, const float* shar
     return amax_acc ? launch_p(cfg.pdl, k_unshard_push_bulk<true>, g, 0, st, tiles, ntiles, shard, scales, rot, W, amax_acc)
            : (scales || W > 1)
                ? launch_p(cfg.pdl, k_unshard_push_bulk<false>, g, 0, st, tiles, ntiles, shard, scales, rot, W, amax_acc)
-                    : launch_p(cfg.pdl, k_unshard_push_bulk<false, false>, g, 0, st, tiles, ntiles, shard, scales, rot, W,
-                               amax_acc);
+                    : launch_p(cfg.pdl, k_unshard_push_bulk<false, false>, grid_for(ntiles, cfg, kCtasPushW1), 0, st,
+                               tiles, ntiles, shard, scales, rot, W, amax_acc);
   return amax_acc ? launch_p(cfg.pdl, k_unshard_push<true>, g, 0, st, tiles, ntiles, shard, scales, rot, W, rank, amax_acc)
                   : launch_p(cfg.pdl, k_unshard_push<false>, g, 0, st, tiles, ntiles, shard, scales, rot, W, rank, amax_acc);
 }

@@ -434,6 +434,28 @@ void launch_rs_copy_in_all(fsdp_layer* l, const void* const* grads, bool grad_bf
 int64_t cin_bytes(const fsdp_layer* l, bool fp8);
 int64_t slot_bytes(const fsdp_layer* l, bool fp8);
 void poll_async_errors(fsdp_mesh* m);
+// One fsdp_reduce_scatter_grads call (capi_layer.cpp validates it) and its mechanisms
+// (capi_rs.cpp): each enqueues the work, records l->ev_rs_done, sets l->rs_pending.
+struct RsCall {
+  fsdp_layer* l;
+  fsdp_mesh* m;
+  const void* const* grads;
+  fsdp_dtype_t gd;
+  bool obf;            // reduce_dtype BFLOAT16 (R11)
+  int64_t osz, S;      // reduce element size, flat shard length
+  bool hsdp;           // R > 1
+  int divisor;         // W * R (mean over every rank)
+  bool via_temp;       // HSDP + accumulate on the NCCL pair: through a temp T
+  int32_t mean, accumulate;
+  cudaStream_t cs;     // the caller's compute stream
+  Capture cap;
+  void replica_all_reduce(float* buf, cudaStream_t st) const;   // fp32 ncclAllReduce across replicas
+  void add_temp_into_grad(const float* T, cudaStream_t st) const;
+};
+void rs_hsdp_world(const RsCall& c);
+void rs_p2p_store(const RsCall& c);
+void rs_p2p_pull(const RsCall& c);
+void rs_nccl(const RsCall& c);
 // HSDP two-phase reduce-scatter: builds l->t_piece / l->t_gather for R pieces (once per R).
 void ensure_pieces(fsdp_layer* l, int R);
 // byte offset of the fp32 result region [S] in a world RS buffer (after the grad staging)

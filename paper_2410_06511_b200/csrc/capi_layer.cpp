@@ -362,7 +362,7 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
         ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_ag, 0);
         CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_AG_DONE, ss->index), flag_local(m, FK_AG_DONE, ss->index),
                                              m->W, m->rank, epoch_ctr(m, FK_AG_DONE, ss->index), m->p2p_timeout_ns,
-                                             m->d_err, m->s_ag, m->cfg.pdl));
+                                             m->d_err, m->s_ag, m->cfg.pdl, m->ce));   // CE copies: no kernel fence
         ph.done();
       }
       CUDA_CHECK(cudaEventRecord(l->ev_done, m->s_ag));

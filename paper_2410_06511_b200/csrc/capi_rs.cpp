@@ -80,7 +80,7 @@ void rs_hsdp_world(const RsCall& c) {
     CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_READY, ss->index, GRP_WORLD),
                                          flag_local(m, FK_RS_READY, ss->index, GRP_WORLD), G.W, G.rank,
                                          epoch_ctr(m, FK_RS_READY, ss->index, GRP_WORLD), m->p2p_timeout_ns,
-                                         m->d_err, m->s_rs));
+                                         m->d_err, m->s_rs, false, /*fence: staged / zero-copy grads*/ true));
     ph.done();
   }
   {
@@ -104,7 +104,7 @@ void rs_hsdp_world(const RsCall& c) {
     CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_DONE, ss->index, GRP_WORLD),
                                          flag_local(m, FK_RS_DONE, ss->index, GRP_WORLD), G.W, G.rank,
                                          epoch_ctr(m, FK_RS_DONE, ss->index, GRP_WORLD), m->p2p_timeout_ns,
-                                         m->d_err, m->s_rs, m->cfg.pdl));
+                                         m->d_err, m->s_rs, m->cfg.pdl, /*fence: result pieces*/ two_phase));
     ph.done();
   }
   cudaStream_t fin = m->s_rs;
@@ -183,7 +183,7 @@ void rs_p2p_store(const RsCall& c) {
     ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_rs, 0);
     CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_DONE, ss->index), flag_local(m, FK_RS_DONE, ss->index),
                                          m->W, m->rank, epoch_ctr(m, FK_RS_DONE, ss->index), m->p2p_timeout_ns,
-                                         m->d_err, m->s_rs, m->cfg.pdl));
+                                         m->d_err, m->s_rs, m->cfg.pdl, m->ce));   // CE copies: no kernel fence
     ph.done();
   }
   CUDA_CHECK(cudaEventRecord(l->ev_k5, m->s_rs));
@@ -284,7 +284,7 @@ void rs_p2p_pull(const RsCall& c) {
     ProfScope ph(m, FSDP_PROF_HANDSHAKE, m->s_rs, 0);
     CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_READY, ss->index), flag_local(m, FK_RS_READY, ss->index),
                                          m->W, m->rank, epoch_ctr(m, FK_RS_READY, ss->index), m->p2p_timeout_ns,
-                                         m->d_err, m->s_rs));
+                                         m->d_err, m->s_rs, false, /*fence: staged / zero-copy grads*/ true));
     ph.done();
   }
   {

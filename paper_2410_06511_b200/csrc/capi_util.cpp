@@ -440,7 +440,7 @@ void p2p_amax_allreduce(fsdp_mesh* m, int n, cudaStream_t st) {
   CUDA_CHECK(cudaMemcpyAsync(m->amax_sym.local, m->reg_acc, sizeof(uint32_t) * (size_t)n, cudaMemcpyDeviceToDevice, st));
   CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_READY, kAmaxSlot), flag_local(m, FK_RS_READY, kAmaxSlot),
                                        m->W, m->rank, epoch_ctr(m, FK_RS_READY, kAmaxSlot), m->p2p_timeout_ns,
-                                       m->d_err, st));
+                                       m->d_err, st, false, /*fence: the amax copy*/ true));
   CUDA_CHECK(fsdpp::launch_amax_max(peer_ptrs(m, m->amax_sym), m->W, m->reg_acc, n, st));
   // every rank has read every copy before any rank overwrites its own at the next call
   CUDA_CHECK(fsdpp::launch_signal_wait(flag_remote(m, FK_RS_DONE, kAmaxSlot), flag_local(m, FK_RS_DONE, kAmaxSlot),

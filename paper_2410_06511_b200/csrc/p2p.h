@@ -36,9 +36,11 @@ struct FlagPtrs { unsigned long long* p[kMaxRanks]; };
 // The spin gives up after timeout_ns and writes 2 | (peer << 8) to *err (FSDP_ERR_TIMEOUT).
 // pdl: launch with programmatic stream serialization (the done handshakes, right after their
 // data kernel on the same stream: the launch latency overlaps the data kernel's tail).
+// fence: a system-scope fence before the signal, for call sites whose peers next read data
+// that local kernels without their own system fence wrote (see k_signal_wait).
 cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
                                unsigned long long* epoch_ctr, unsigned long long timeout_ns, int* err,
-                               cudaStream_t st, bool pdl = false);
+                               cudaStream_t st, bool pdl = false, bool fence = false);
 
 // Push tiles: src = element offset into the fp32 shard, dst = byte offset into the arena,
 // n elements, kind TK_BF16 / TK_FP8 (scale = scales[param]).  Stores go to arena.p[d] for

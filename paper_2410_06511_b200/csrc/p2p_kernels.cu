@@ -31,7 +31,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // collective, or died) the kernel records {kind=2 (timeout), peer} in *err and returns, so a
 // protocol error surfaces as FSDP_ERR_TIMEOUT from fsdp_mesh_synchronize instead of a hang.
 __global__ void k_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
-                              unsigned long long* epoch_ctr, unsigned long long timeout_ns, int* err) {
+                              unsigned long long* epoch_ctr, unsigned long long timeout_ns, int* err, int fence) {
   __shared__ unsigned long long e_sh;
   pdl_wait();   // launched programmatically after the data kernel (done handshakes)
   const int r = threadIdx.x;
@@ -39,18 +39,24 @@ __global__ void k_signal_wait(FlagPtrs remote, unsigned long long* local, int W,
     e_sh = *epoch_ctr + 1;
     *epoch_ctr = e_sh;
   }
-  // One system-scope fence, on one thread, on each side of the handshake: what a
-  // peer must see before our signal was written by EARLIER kernels on this stream (staging,
-  // zero-copy grads written by the caller's kernels, the push / scatter data — those two end
-  // with their own system fence); the fence orders all of it (cumulatively, through the CTA
-  // barrier below and the release store of the signalling thread) before the flag.  After
-  // the wait, the fence on the other side orders the peers' data (released before their
-  // flags, acquired by our ld.acquire.sys) before every later consumer on this stream.
-  // Single-thread fences: the 32-thread __threadfence_system pair cost ~25 us per op;
-  // -DFSDP_HS_NO_FENCE drops them (measurement only).
-#ifndef FSDP_HS_NO_FENCE
-  if (r == 0) __threadfence_system();
+  // A system-scope fence, on one thread, before the signal exactly where the protocol
+  // publishes data that unfenced local kernels wrote and peers read next (`fence`, chosen
+  // per call site: the pull's / world pull's ready (staging or zero-copy grads written by
+  // the caller's or the staging kernel), the two-phase HSDP done (the result pieces), the
+  // P2P amax all-reduce's ready (the amax copy), copy-engine transfers).  It orders that data
+  // (cumulatively, through the CTA barrier and the signalling thread's release store) before
+  // the flag.  Elsewhere the data a peer reads next was stored by a kernel that ends with its
+  // own system fence (push, store-scatter) or there is none (a buffer handed back after
+  // reads, which completed with the kernel that made them).  After the wait nothing needs a
+  // fence: peers released their data before their flags, ld.acquire.sys observes the flags,
+  // and the consumers are later kernels on this GPU.  Measured (profiles/round2/r2fence):
+  // one fence per handshake on both sides cost 35% of a small unit's step (toy W=2 CUDA
+  // graph 90 -> 122 us) and 1.2% of the 8B step.  -DFSDP_HS_FENCE fences every handshake on
+  // both sides (debugging).
+#ifdef FSDP_HS_FENCE
+  fence = 1;
 #endif
+  if (fence && r == 0) __threadfence_system();
   __syncthreads();
   const unsigned long long epoch = e_sh;
 #pragma unroll
@@ -67,7 +73,7 @@ __global__ void k_signal_wait(FlagPtrs remote, unsigned long long* local, int W,
     }
   }
   __syncthreads();
-#ifndef FSDP_HS_NO_FENCE
+#ifdef FSDP_HS_FENCE
   if (r == 0) __threadfence_system();
 #endif
 }
@@ -537,9 +543,10 @@ cudaError_t launch_reduce_own_w(const Tile* tiles, int ntiles, const uint8_t* re
 
 cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W, int rank,
                                unsigned long long* epoch_ctr, unsigned long long timeout_ns, int* err,
-                               cudaStream_t st, bool pdl) {
-  if (pdl) return launch_pdl(k_signal_wait, 1, 32, 0, st, remote, local, W, rank, epoch_ctr, timeout_ns, err);
-  k_signal_wait<<<1, 32, 0, st>>>(remote, local, W, rank, epoch_ctr, timeout_ns, err);
+                               cudaStream_t st, bool pdl, bool fence) {
+  const int f = fence ? 1 : 0;
+  if (pdl) return launch_pdl(k_signal_wait, 1, 32, 0, st, remote, local, W, rank, epoch_ctr, timeout_ns, err, f);
+  k_signal_wait<<<1, 32, 0, st>>>(remote, local, W, rank, epoch_ctr, timeout_ns, err, f);
   return cudaGetLastError();
 }
 

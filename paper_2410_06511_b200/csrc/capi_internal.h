@@ -297,6 +297,7 @@ struct fsdp_mesh {
   int algo = FSDP_ALGO_NCCL;
   int p2p_rs_mode = FSDP_P2P_RS_AUTO;        // how the P2P reduce-scatter moves data
   int reduce_per_sm = 2;                     // store-RS local reduce CTAs/SM (0: default grid; 2 measured best)
+  int gather_per_sm = 0;                     // HSDP replica gather CTAs/SM (0: default grid)
   bool amax_fuse = true;                     // delayed scaling: amax fused into the fp8 casts (FSDP_B200_AMAX_FUSE=0: K1 pass)
   bool store_own_direct = true;              // store RS: own rows read from the caller's grads (FSDP_B200_STORE_OWN=0: own slot)
   bool p2p_ok = false;

@@ -143,6 +143,7 @@ static void p2p_init(fsdp_mesh* m) {
   if (const char* t = std::getenv("FSDP_B200_P2P_TIMEOUT_MS"))
     m->p2p_timeout_ns = (unsigned long long)std::max(1L, std::atol(t)) * 1000000ull;
   if (const char* e = std::getenv("FSDP_B200_REDUCE_CTAS_PER_SM")) m->reduce_per_sm = std::max(0, std::min(16, std::atoi(e)));
+  if (const char* e = std::getenv("FSDP_B200_GATHER_CTAS_PER_SM")) m->gather_per_sm = std::max(0, std::min(16, std::atoi(e)));
   if (const char* r = std::getenv("FSDP_B200_P2P_RS"))
     m->p2p_rs_mode = std::string(r) == "pull" ? FSDP_P2P_RS_PULL
                      : std::string(r) == "store" ? FSDP_P2P_RS_STORE : FSDP_P2P_RS_AUTO;

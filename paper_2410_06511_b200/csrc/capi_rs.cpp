@@ -115,8 +115,12 @@ void rs_hsdp_world(const RsCall& c) {
     CUDA_CHECK(cudaStreamWaitEvent(fin, l->ev_k5, 0));
     fsdpp::PeerPtrs rp{};
     for (int q = 0; q < m->R; ++q) rp.p[q] = (uint8_t*)ss->buf.peers[q * m->W + m->rank] + res_off;
+    // it overlaps the next unit's phase 1 and all-gather: a smaller grid leaves them SMs
+    // (FSDP_B200_GATHER_CTAS_PER_SM; 0 = the default grid)
+    fsdpk::LaunchCfg gcfg = m->cfg;
+    if (m->gather_per_sm > 0) gcfg.per_sm = m->gather_per_sm;
     ProfScope pg(m, FSDP_PROF_REPLICA_GATHER, fin, (int64_t)(m->R - 1) * 4 * l->pull_elems / m->R);
-    CUDA_CHECK(fsdpp::launch_replica_gather(l->t_gather.d, l->t_gather.n, rp, l->grad, accumulate != 0, m->cfg,
+    CUDA_CHECK(fsdpp::launch_replica_gather(l->t_gather.d, l->t_gather.n, rp, l->grad, accumulate != 0, gcfg,
                                             fin));
     pg.done();
   }

@@ -86,7 +86,7 @@ static void mesh_common_init(fsdp_mesh* m) {
   }
   if (const char* e = std::getenv("FSDP_B200_PULL_STAGES")) m->cfg.pull_stages = std::max(2, std::min(4, std::atoi(e)));
   if (const char* e = std::getenv("FSDP_B200_PDL")) m->cfg.pdl = std::atoi(e) != 0;
-  if (const char* e = std::getenv("FSDP_B200_K5_STAGES")) m->cfg.k5_stages = std::atoi(e) == 4 ? 4 : 2;
+  if (const char* e = std::getenv("FSDP_B200_K5_STAGES")) m->cfg.k5_stages = std::max(2, std::min(4, std::atoi(e)));
   m->cfg.grid_cap = sms * (per_sm > 0 ? per_sm : 4);
   // device error flag in mapped pinned host memory: kernels store a code (plain stores, no
   // atomics over PCIe), the host reads it without a copy or sync (wait_* poll it)

@@ -542,6 +542,15 @@ cudaError_t launch_rs_copy_in(const Tile* tiles, int ntiles, const PtrArray& gra
   if (cfg.variant & 8) {   // TMA bulk K5
     const int gb = grid_for(ntiles, cfg, kCtasCopy);
     const size_t unit = (size_t)kRsChunk * ((grad_bf16 ? 2 : 4) + (out_bf16 ? 2 : 4));
+    if (cfg.k5_stages == 3) {   // 36 KB per CTA for bf16 grads: under the 48 KB default
+      auto k = grad_bf16 ? (out_bf16 ? k_rs_copy_in_bulk<true, true, 3> : k_rs_copy_in_bulk<true, false, 3>)
+                         : (out_bf16 ? k_rs_copy_in_bulk<false, true, 3> : k_rs_copy_in_bulk<false, false, 3>);
+      if (3 * unit > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * unit));
+        if (e != cudaSuccess) return e;
+      }
+      return launch_persistent(k, gb, 3 * unit, st, tiles, ntiles, grads, d, div);
+    }
     if (cfg.k5_stages == 4) {
       auto k = grad_bf16 ? (out_bf16 ? k_rs_copy_in_bulk<true, true, 4> : k_rs_copy_in_bulk<true, false, 4>)
                          : (out_bf16 ? k_rs_copy_in_bulk<false, true, 4> : k_rs_copy_in_bulk<false, false, 4>);

@@ -43,7 +43,7 @@ struct LaunchCfg {
   // P2P data kernels and done handshakes launched with programmatic dependent launch
   // (FSDP_B200_PDL=0 disables)
   bool pdl = true;
-  // TMA-bulk K5 pipeline stages (FSDP_B200_K5_STAGES: 2 or 4)
+  // TMA-bulk K5 pipeline stages (FSDP_B200_K5_STAGES: 2, 3 or 4)
   int k5_stages = 2;
   // persistent grid of a kernel whose measured best is `tuned` CTAs per SM
   int cap(int tuned) const { return sms * (per_sm > 0 ? per_sm : tuned); }

@@ -542,28 +542,31 @@ cudaError_t launch_rs_copy_in(const Tile* tiles, int ntiles, const PtrArray& gra
   if (cfg.variant & 8) {   // TMA bulk K5
     const int gb = grid_for(ntiles, cfg, kCtasCopy);
     const size_t unit = (size_t)kRsChunk * ((grad_bf16 ? 2 : 4) + (out_bf16 ? 2 : 4));
-    if (cfg.k5_stages == 3) {   // 36 KB per CTA for bf16 grads: under the 48 KB default
+    const int ki = (grad_bf16 ? 2 : 0) + (out_bf16 ? 1 : 0);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    // stages * unit of dynamic shared memory (+ the mbarriers): opt in above the 48 KB default,
+    // once per kernel and device
+    auto opt_in = [&](auto k, int ns, bool (&done)[4][64]) -> cudaError_t {
+      if (dev >= 0 && dev < 64 && done[ki][dev]) return cudaSuccess;
+      const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(ns * unit));
+      if (e == cudaSuccess && dev >= 0 && dev < 64) done[ki][dev] = true;
+      return e;
+    };
+    if (cfg.k5_stages == 3) {   // the default (FSDP_B200_K5_STAGES): profiles/round2/r2k5
       auto k = grad_bf16 ? (out_bf16 ? k_rs_copy_in_bulk<true, true, 3> : k_rs_copy_in_bulk<true, false, 3>)
                          : (out_bf16 ? k_rs_copy_in_bulk<false, true, 3> : k_rs_copy_in_bulk<false, false, 3>);
-      if (3 * unit > 48 * 1024) {
-        const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * unit));
-        if (e != cudaSuccess) return e;
-      }
+      static bool attr3[4][64] = {};
+      const cudaError_t e = opt_in(k, 3, attr3);
+      if (e != cudaSuccess) return e;
       return launch_persistent(k, gb, 3 * unit, st, tiles, ntiles, grads, d, div);
     }
     if (cfg.k5_stages == 4) {
       auto k = grad_bf16 ? (out_bf16 ? k_rs_copy_in_bulk<true, true, 4> : k_rs_copy_in_bulk<true, false, 4>)
                          : (out_bf16 ? k_rs_copy_in_bulk<false, true, 4> : k_rs_copy_in_bulk<false, false, 4>);
-      // > 48 KB of dynamic shared memory for fp32 grads: opt in (per device, once per kernel)
-      static bool attr[4][64] = {};
-      const int ki = (grad_bf16 ? 2 : 0) + (out_bf16 ? 1 : 0);
-      int dev = 0;
-      cudaGetDevice(&dev);
-      if (dev < 0 || dev >= 64 || !attr[ki][dev]) {
-        const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * unit));
-        if (e != cudaSuccess) return e;
-        if (dev >= 0 && dev < 64) attr[ki][dev] = true;
-      }
+      static bool attr4[4][64] = {};
+      const cudaError_t e = opt_in(k, 4, attr4);
+      if (e != cudaSuccess) return e;
       return launch_persistent(k, gb, 4 * unit, st, tiles, ntiles, grads, d, div);
     }
     auto k = grad_bf16 ? (out_bf16 ? k_rs_copy_in_bulk<true, true> : k_rs_copy_in_bulk<true, false>)

@@ -43,8 +43,9 @@ struct LaunchCfg {
   // P2P data kernels and done handshakes launched with programmatic dependent launch
   // (FSDP_B200_PDL=0 disables)
   bool pdl = true;
-  // TMA-bulk K5 pipeline stages (FSDP_B200_K5_STAGES: 2, 3 or 4)
-  int k5_stages = 2;
+  // TMA-bulk K5 pipeline stages (FSDP_B200_K5_STAGES: 2, 3 or 4; 3 measured best: the K5
+  // kernel 242 -> 228 us per 8B block, the W=1 step 15.07 -> 14.66 ms, profiles/round2/r2k5)
+  int k5_stages = 3;
   // persistent grid of a kernel whose measured best is `tuned` CTAs per SM
   int cap(int tuned) const { return sms * (per_sm > 0 ? per_sm : tuned); }
 };

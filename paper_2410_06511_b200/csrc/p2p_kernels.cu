@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_reduce_own(const Tile* __restri
 // every rank's arena (cp.async.bulk shared->global, W stores per chunk, 2 stages).
 constexpr uint32_t kBulkChunk = 4096;
 static_assert(kBulkChunk / 16 == (uint32_t)kThreads, "push_tile_bulk: one 16-byte vector per thread per chunk");
-template <bool kFp8, bool kAmax = false, bool kPref = false>
+template <bool kFp8, bool kAmax = false, bool kPref = false, int NSTG = 2>
 __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __restrict__ shard, float s,
                                                const PeerPtrs& arena, int W, uint8_t* stage_buf, uint32_t& it,
                                                uint32_t* amp = nullptr) {
@@ -373,7 +373,7 @@ __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __re
   float xn[V];
   bool hn = kPref && nch > 0 && load_chunk(0, xn);
   for (uint32_t c = 0; c < nch; ++c, ++it) {
-    uint8_t* buf = stage_buf + (size_t)(it & 1u) * kBulkChunk;
+    uint8_t* buf = stage_buf + (size_t)(it % NSTG) * kBulkChunk;
     float x[V];
     bool hx;
     if constexpr (kPref) {
@@ -382,7 +382,7 @@ __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __re
       hx = hn;
       if (c + 1 < nch) hn = load_chunk(c + 1, xn);
     }
-    if (threadIdx.x == 0) bulk_wait_read_le1();       // the chunk written 2 iterations ago was read
+    if (threadIdx.x == 0) bulk_wait_read_le<NSTG - 1>();   // the chunk written NSTG iterations ago was read
     __syncthreads();
     if constexpr (!kPref) hx = load_chunk(c, x);
     if (hx) {
@@ -432,12 +432,19 @@ __device__ __forceinline__ void push_tile_bulk(const Tile& tl, const float* __re
 // the register double buffer fits in 31 registers and 8 CTAs per SM (kCtasPushW1: the push
 // alone 245.7 -> 238.5 us per 8B block, profiles/round2/r2pref bench_cta8)
 constexpr int kCtasPushW1 = 8;
+#ifndef FSDP_PUSH_W1_STAGES
+#define FSDP_PUSH_W1_STAGES 2
+#endif
+constexpr int kPushW1Stages = FSDP_PUSH_W1_STAGES;   // smem output stages of the bf16-only push
 template <bool kAmax, bool kAnyFp8 = true>
 __global__ void __launch_bounds__(kThreads) k_unshard_push_bulk(const Tile* __restrict__ tiles, int ntiles,
                                                                 const float* __restrict__ shard,
                                                                 const float* __restrict__ scales, PeerPtrs arena,
                                                                 int W, uint32_t* __restrict__ acc) {
-  __shared__ __align__(128) uint8_t stage_buf[2 * kBulkChunk];
+  // the bf16-only W = 1 instance keeps kPushW1Stages output chunks in flight (FSDP_B200 A/B:
+  // profiles/round2); the mixed fp8 instances keep 2
+  constexpr int NSTG = kAnyFp8 ? 2 : kPushW1Stages;
+  __shared__ __align__(128) uint8_t stage_buf[NSTG * kBulkChunk];
   __shared__ uint32_t red[kThreads / 32];
   pdl_wait();
   uint32_t it = 0;
@@ -452,7 +459,7 @@ __global__ void __launch_bounds__(kThreads) k_unshard_push_bulk(const Tile* __re
         push_tile_bulk<true>(tl, shard, scales[tl.param], arena, W, stage_buf, it);
       }
     }
-    else push_tile_bulk<false, false, !kAnyFp8>(tl, shard, 0.0f, arena, W, stage_buf, it);
+    else push_tile_bulk<false, false, !kAnyFp8, NSTG>(tl, shard, 0.0f, arena, W, stage_buf, it);
   }
   if (threadIdx.x == 0) bulk_wait0();                 // every bulk store has completed
   __syncthreads();

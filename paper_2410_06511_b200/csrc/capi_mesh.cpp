@@ -78,7 +78,7 @@ static void mesh_common_init(fsdp_mesh* m) {
   m->cfg.per_sm = per_sm;
   // default: TMA bulk push (4), bulk RS copy-in (8) and, for zero-copy reduce-scatters, bulk
   // pull (2) — measured best (profiles/r06, r07); FSDP_B200_VARIANT overrides (0 = plain ld/st)
-  m->cfg.variant = 14;
+  m->cfg.variant = 78;   // + 64: the W=1 bf16 unshard as the TMA-in/TMA-out cast (profiles/round2/r2cast)
   if (const char* e = std::getenv("FSDP_B200_VARIANT")) m->cfg.variant = std::atoi(e);
   if (const char* e = std::getenv("FSDP_B200_PULL_CHUNK")) {
     const int c = std::atoi(e);

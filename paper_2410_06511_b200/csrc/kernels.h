@@ -32,9 +32,10 @@ struct LaunchCfg {
   int grid_cap;     // max CTAs when the kernel has no tuned value (SMs * 4)
   int sms = 148;    // multiprocessor count
   int per_sm = 0;   // > 0: FSDP_B200_CTAS_PER_SM override for every kernel
-  // kernel-variant bit mask (FSDP_B200_VARIANT): 1 = 16-byte pull loads, 2 = TMA bulk pull,
-  // 4 = TMA bulk push, 8 = TMA bulk RS copy-in (K5), 32 = W=1 bf16 unshard as one contiguous
-  // K2 cast when the arena has the flat layout
+  // kernel-variant bit mask (FSDP_B200_VARIANT, default 78): 1 = 16-byte pull loads, 2 = TMA
+  // bulk pull, 4 = TMA bulk push, 8 = TMA bulk RS copy-in (K5), 32 = W=1 bf16 unshard as one
+  // contiguous K2 cast when the arena has the flat layout, 64 = W=1 bf16 unshard as the
+  // TMA-in / TMA-out cast (k_cast_bf16_w1_tma)
   int variant = 0;
   // TMA bulk pull: bytes per peer per chunk (power of two, 1-16 KB) and pipeline stages (2-4)
   // (FSDP_B200_PULL_CHUNK / FSDP_B200_PULL_STAGES)

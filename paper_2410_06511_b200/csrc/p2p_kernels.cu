@@ -481,6 +481,74 @@ __global__ void __launch_bounds__(kThreads) k_amax_max(PeerPtrs src, int W, uint
   }
 }
 
+// ------------------------------------------------------------------- W = 1 bf16 cast, TMA in / out
+// The W = 1 bf16 unshard modelled on the 3-stage K5: per 2048-element chunk the TMA engine
+// loads the fp32 rows into shared memory (mbarrier complete_tx, NS stages ahead), threads
+// cast 8 floats -> one 16-byte bf16 vector into an output stage, one thread bulk-stores it.
+// Tiles whose fp32 source, bf16 destination or length are not 16-byte granular take an
+// element path (none in the Llama layouts).  Tile: src = shard element offset, dst = byte
+// offset into the arena, n elements (layout.h tiles_push).
+constexpr uint32_t kCastChunk = 2048;
+template <int NS>
+__global__ void __launch_bounds__(kThreads) k_cast_bf16_w1_tma(const Tile* __restrict__ tiles, int ntiles,
+                                                                const float* __restrict__ shard,
+                                                                uint8_t* __restrict__ arena) {
+  extern __shared__ __align__(128) uint8_t cast_smem[];   // [NS][chunk * 4] in, [NS][chunk * 2] out
+  float (*sin)[kCastChunk] = reinterpret_cast<float (*)[kCastChunk]>(cast_smem);
+  uint8_t (*sout)[kCastChunk * 2] = reinterpret_cast<uint8_t (*)[kCastChunk * 2]>(cast_smem + NS * kCastChunk * 4);
+  __shared__ uint64_t full[NS];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  uint32_t it = 0;   // TMA chunks of this CTA: stage it % NS, parity (it / NS) & 1
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const Tile tl = tiles[t];
+    const float* s = shard + tl.src;
+    uint8_t* d = arena + tl.dst;
+    const uint32_t n = tl.n;
+    if ((tl.src & 3u) != 0 || (tl.dst & 15u) != 0 || (n & 7u) != 0) {   // element path
+      for (uint32_t e = threadIdx.x; e < n; e += kThreads)
+        reinterpret_cast<uint16_t*>(d)[e] = (uint16_t)(pack_bf16x2(s[e], 0.0f) & 0xFFFFu);
+      continue;
+    }
+    const uint32_t nch = (n + kCastChunk - 1) / kCastChunk;
+    auto issue = [&](uint32_t c) {   // thread 0: chunk c of this tile into stage (it + c) % NS
+      const uint32_t i = it + c, st = i % NS;
+      const uint32_t ne = min(kCastChunk, n - c * kCastChunk);
+      mbar_arrive_expect_tx(&full[st], ne * 4);
+      bulk_g2s(sin[st], s + (size_t)c * kCastChunk, ne * 4, &full[st]);
+    };
+    if (threadIdx.x == 0)
+      for (uint32_t c = 0; c < (uint32_t)NS && c < nch; ++c) issue(c);
+    for (uint32_t c = 0; c < nch; ++c) {
+      const uint32_t i = it + c, st = i % NS;
+      const uint32_t ne = min(kCastChunk, n - c * kCastChunk);
+      mbar_wait(&full[st], (i / NS) & 1u);
+      if (threadIdx.x == 0) bulk_wait_read_le<NS - 1>();   // sout[st] (stored NS chunks ago) was read
+      __syncthreads();
+      for (uint32_t e8 = threadIdx.x; e8 * 8 < ne; e8 += kThreads) {
+        const float4 a = *reinterpret_cast<const float4*>(&sin[st][e8 * 8]);
+        const float4 b = *reinterpret_cast<const float4*>(&sin[st][e8 * 8 + 4]);
+        *reinterpret_cast<uint4*>(sout[st] + e8 * 16) =
+            make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+      }
+      fence_proxy_async_smem();
+      __syncthreads();   // sout[st] complete, sin[st] consumed
+      if (threadIdx.x == 0) {
+        bulk_s2g(d + (size_t)c * kCastChunk * 2, sout[st], ne * 2);
+        bulk_commit();
+        if (c + NS < nch) issue(c + NS);
+      }
+    }
+    it += nch;
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
 // ------------------------------------------------------------------- gather copy
 __global__ void __launch_bounds__(kThreads) k_gather_copy(const Tile* __restrict__ tiles, int ntiles,
                                                           fsdpk::PtrArray srcs, uint8_t* __restrict__ dst_base) {
@@ -585,6 +653,15 @@ cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool
   const int g = grid_for(ntiles, cfg);
   return grad_bf16 ? launch_pull_w<true>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant, cfg.pdl)
                    : launch_pull_w<false>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant, cfg.pdl);
+}
+
+cudaError_t launch_cast_bf16_w1(const Tile* tiles, int ntiles, const float* shard, void* arena, fsdpk::LaunchCfg cfg,
+                                cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  constexpr int NS = 3;
+  constexpr size_t smem = (size_t)NS * kCastChunk * (4 + 2);   // 36 KB
+  return launch_p(cfg.pdl, k_cast_bf16_w1_tma<NS>, grid_for(ntiles, cfg, fsdpk::kCtasCopy), smem, st, tiles, ntiles,
+                  shard, (uint8_t*)arena);
 }
 
 cudaError_t launch_amax_max(PeerPtrs src, int W, uint32_t* out, int n, cudaStream_t st) {

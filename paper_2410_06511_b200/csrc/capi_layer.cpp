@@ -392,11 +392,12 @@ fsdp_status_t fsdp_unshard(fsdp_layer_t* l, fsdp_dtype_t dt, const float* scales
           // tensors: faster alone (6138 vs 6002 GB/s) but the overlapped W=1 step is 0.2%
           // slower next to the concurrent K5 (profiles/r13), so the push stays the default
           CUDA_CHECK(fsdpk::launch_copy_in_bf16(l->shard, slot->b.p, l->L.S, m->cfg, m->s_cin));
-        } else if (!fp8 && (m->cfg.variant & 64)) {
-          // FSDP_B200_VARIANT bit 64 (default): the bf16 cast with TMA loads and stores, 3
-          // stages — 226 us per 8B block, 0.983 of the copy peak, vs 239 us for the push
-          // (profiles/round2/r2cast); the fp8 unshard keeps the push (mixed tiles, fused amax)
-          CUDA_CHECK(fsdpp::launch_cast_bf16_w1(T.d, T.n, l->shard, slot->b.p, m->cfg, m->s_cin));
+        } else if (m->cfg.variant & 64) {
+          // FSDP_B200_VARIANT bit 64 (default): the cast with TMA loads and stores, 3 stages —
+          // bf16: 226 us per 8B block, 0.983 of the copy peak, vs 239 us for the push
+          // (profiles/round2/r2cast); the fp8 unshard (mixed tiles, fused amax) likewise
+          CUDA_CHECK(fsdpp::launch_cast_w1(T.d, T.n, l->shard, fp8 ? scales : nullptr, slot->b.p, amax_acc, m->cfg,
+                                           m->s_cin));
         } else {
           fsdpk::LaunchCfg lcfg = m->cfg;   // W = 1: bulk stores too (0.915 vs 0.902 of HBM, r06)
           if (const char* e = std::getenv("FSDP_B200_W1_BULK")) if (std::atoi(e) == 0) lcfg.variant &= ~4;

@@ -74,10 +74,12 @@ cudaError_t launch_rs_pull_nested(const fsdpk::Tile* tiles, int ntiles, PeerPtrs
 cudaError_t launch_replica_gather(const fsdpk::Tile* tiles, int ntiles, PeerPtrs res, float* grad, bool accumulate,
                                   fsdpk::LaunchCfg cfg, cudaStream_t st);
 
-// W = 1 bf16 unshard with TMA loads and stores (3 stages of 2048 elements): the push tiles'
-// rows of the fp32 shard cast to bf16 into the local arena (tiles_push, bf16).
-cudaError_t launch_cast_bf16_w1(const fsdpk::Tile* tiles, int ntiles, const float* shard, void* arena,
-                                fsdpk::LaunchCfg cfg, cudaStream_t st);
+// W = 1 unshard with TMA loads and stores (3 stages of 2048 elements): the push tiles' rows
+// of the fp32 shard cast into the local arena (tiles_push: TK_BF16 -> bf16, TK_FP8 -> e4m3
+// with scales[param]; scales NULL = a bf16-only table).  amax_acc != NULL: the fused amax of
+// the TK_FP8 tiles (as launch_unshard_push).
+cudaError_t launch_cast_w1(const fsdpk::Tile* tiles, int ntiles, const float* shard, const float* scales,
+                           void* arena, uint32_t* amax_acc, fsdpk::LaunchCfg cfg, cudaStream_t st);
 
 // fp8 amax all-reduce over symmetric memory: out[i] = max_{q < W} src.p[q][i] (uint32 bit
 // patterns of non-negative fp32 amaxes), i < n.

@@ -481,22 +481,26 @@ __global__ void __launch_bounds__(kThreads) k_amax_max(PeerPtrs src, int W, uint
   }
 }
 
-// ------------------------------------------------------------------- W = 1 bf16 cast, TMA in / out
-// The W = 1 bf16 unshard modelled on the 3-stage K5: per 2048-element chunk the TMA engine
-// loads the fp32 rows into shared memory (mbarrier complete_tx, NS stages ahead), threads
-// cast 8 floats -> one 16-byte bf16 vector into an output stage, one thread bulk-stores it.
-// Tiles whose fp32 source, bf16 destination or length are not 16-byte granular take an
-// element path (none in the Llama layouts).  Tile: src = shard element offset, dst = byte
-// offset into the arena, n elements (layout.h tiles_push).
+// ------------------------------------------------------------------- W = 1 cast, TMA in / out
+// The W = 1 unshard modelled on the 3-stage K5: per 2048-element chunk the TMA engine loads
+// the fp32 rows into shared memory (mbarrier complete_tx, NS stages ahead), threads cast them
+// into an output stage — 8 floats -> one 16-byte bf16 vector (TK_BF16 tiles), or 16 floats ->
+// one 16-byte e4m3 vector with the param's scale (TK_FP8) — and one thread bulk-stores it.
+// kAmax (delayed scaling, amax fused): max |x| bits of the TK_FP8 tiles, one atomic per CTA
+// per tile, as the push.  Tiles whose fp32 source, destination or length are not 16-byte
+// granular take an element path (none in the Llama layouts).  Tile: src = shard element
+// offset, dst = byte offset into the arena, n elements (layout.h tiles_push).
 constexpr uint32_t kCastChunk = 2048;
-template <int NS>
-__global__ void __launch_bounds__(kThreads) k_cast_bf16_w1_tma(const Tile* __restrict__ tiles, int ntiles,
-                                                                const float* __restrict__ shard,
-                                                                uint8_t* __restrict__ arena) {
+template <int NS, bool kAnyFp8, bool kAmax>
+__global__ void __launch_bounds__(kThreads) k_cast_w1_tma(const Tile* __restrict__ tiles, int ntiles,
+                                                           const float* __restrict__ shard,
+                                                           const float* __restrict__ scales,
+                                                           uint8_t* __restrict__ arena, uint32_t* __restrict__ acc) {
   extern __shared__ __align__(128) uint8_t cast_smem[];   // [NS][chunk * 4] in, [NS][chunk * 2] out
   float (*sin)[kCastChunk] = reinterpret_cast<float (*)[kCastChunk]>(cast_smem);
   uint8_t (*sout)[kCastChunk * 2] = reinterpret_cast<uint8_t (*)[kCastChunk * 2]>(cast_smem + NS * kCastChunk * 4);
   __shared__ uint64_t full[NS];
+  __shared__ uint32_t red[kThreads / 32];
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
@@ -510,41 +514,72 @@ __global__ void __launch_bounds__(kThreads) k_cast_bf16_w1_tma(const Tile* __res
     const float* s = shard + tl.src;
     uint8_t* d = arena + tl.dst;
     const uint32_t n = tl.n;
-    if ((tl.src & 3u) != 0 || (tl.dst & 15u) != 0 || (n & 7u) != 0) {   // element path
-      for (uint32_t e = threadIdx.x; e < n; e += kThreads)
-        reinterpret_cast<uint16_t*>(d)[e] = (uint16_t)(pack_bf16x2(s[e], 0.0f) & 0xFFFFu);
-      continue;
-    }
-    const uint32_t nch = (n + kCastChunk - 1) / kCastChunk;
-    auto issue = [&](uint32_t c) {   // thread 0: chunk c of this tile into stage (it + c) % NS
-      const uint32_t i = it + c, st = i % NS;
-      const uint32_t ne = min(kCastChunk, n - c * kCastChunk);
-      mbar_arrive_expect_tx(&full[st], ne * 4);
-      bulk_g2s(sin[st], s + (size_t)c * kCastChunk, ne * 4, &full[st]);
-    };
-    if (threadIdx.x == 0)
-      for (uint32_t c = 0; c < (uint32_t)NS && c < nch; ++c) issue(c);
-    for (uint32_t c = 0; c < nch; ++c) {
-      const uint32_t i = it + c, st = i % NS;
-      const uint32_t ne = min(kCastChunk, n - c * kCastChunk);
-      mbar_wait(&full[st], (i / NS) & 1u);
-      if (threadIdx.x == 0) bulk_wait_read_le<NS - 1>();   // sout[st] (stored NS chunks ago) was read
-      __syncthreads();
-      for (uint32_t e8 = threadIdx.x; e8 * 8 < ne; e8 += kThreads) {
-        const float4 a = *reinterpret_cast<const float4*>(&sin[st][e8 * 8]);
-        const float4 b = *reinterpret_cast<const float4*>(&sin[st][e8 * 8 + 4]);
-        *reinterpret_cast<uint4*>(sout[st] + e8 * 16) =
-            make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+    const bool f8 = kAnyFp8 && tl.kind == fsdpk::TK_FP8;   // CTA-uniform
+    const float sc = f8 ? scales[tl.param] : 0.0f;
+    uint32_t am = 0;
+    if ((tl.src & 3u) != 0 || (tl.dst & 15u) != 0 || (n & 15u) != 0) {   // element path
+      for (uint32_t e = threadIdx.x; e < n; e += kThreads) {
+        if (f8) {
+          if constexpr (kAmax) am = max(am, abs_bits(s[e]));
+          d[e] = (uint8_t)(pack_e4m3x2(__fmul_rn(s[e], sc), 0.0f) & 0xFFu);
+        } else {
+          reinterpret_cast<uint16_t*>(d)[e] = (uint16_t)(pack_bf16x2(s[e], 0.0f) & 0xFFFFu);
+        }
       }
-      fence_proxy_async_smem();
-      __syncthreads();   // sout[st] complete, sin[st] consumed
-      if (threadIdx.x == 0) {
-        bulk_s2g(d + (size_t)c * kCastChunk * 2, sout[st], ne * 2);
-        bulk_commit();
-        if (c + NS < nch) issue(c + NS);
+    } else {
+      const uint32_t es = f8 ? 1u : 2u;   // output bytes per element
+      const uint32_t nch = (n + kCastChunk - 1) / kCastChunk;
+      auto issue = [&](uint32_t c) {   // thread 0: chunk c of this tile into stage (it + c) % NS
+        const uint32_t i = it + c, st = i % NS;
+        const uint32_t ne = min(kCastChunk, n - c * kCastChunk);
+        mbar_arrive_expect_tx(&full[st], ne * 4);
+        bulk_g2s(sin[st], s + (size_t)c * kCastChunk, ne * 4, &full[st]);
+      };
+      if (threadIdx.x == 0)
+        for (uint32_t c = 0; c < (uint32_t)NS && c < nch; ++c) issue(c);
+      for (uint32_t c = 0; c < nch; ++c) {
+        const uint32_t i = it + c, st = i % NS;
+        const uint32_t ne = min(kCastChunk, n - c * kCastChunk);
+        mbar_wait(&full[st], (i / NS) & 1u);
+        if (threadIdx.x == 0) bulk_wait_read_le<NS - 1>();   // sout[st] (stored NS chunks ago) was read
+        __syncthreads();
+        if (f8) {
+          if constexpr (kAnyFp8) {
+            for (uint32_t e16 = threadIdx.x; e16 * 16 < ne; e16 += kThreads) {
+              float x[16];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float4 a = *reinterpret_cast<const float4*>(&sin[st][e16 * 16 + 4 * j]);
+                x[4 * j] = a.x; x[4 * j + 1] = a.y; x[4 * j + 2] = a.z; x[4 * j + 3] = a.w;
+              }
+              if constexpr (kAmax) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) am = max(am, abs_bits(x[j]));
+              }
+              *reinterpret_cast<uint4*>(sout[st] + e16 * 16) = cvt_e4m3x16(x, sc);
+            }
+          }
+        } else {
+          for (uint32_t e8 = threadIdx.x; e8 * 8 < ne; e8 += kThreads) {
+            const float4 a = *reinterpret_cast<const float4*>(&sin[st][e8 * 8]);
+            const float4 b = *reinterpret_cast<const float4*>(&sin[st][e8 * 8 + 4]);
+            *reinterpret_cast<uint4*>(sout[st] + e8 * 16) =
+                make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+          }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();   // sout[st] complete, sin[st] consumed
+        if (threadIdx.x == 0) {
+          bulk_s2g(d + (size_t)c * kCastChunk * es, sout[st], ne * es);
+          bulk_commit();
+          if (c + NS < nch) issue(c + NS);
+        }
       }
+      it += nch;
     }
-    it += nch;
+    if constexpr (kAmax) {
+      if (f8) amax_commit_cta(acc, tl.param, am, red);
+    }
   }
   if (threadIdx.x == 0) bulk_wait0();
 }
@@ -655,13 +690,18 @@ cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool
                    : launch_pull_w<false>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant, cfg.pdl);
 }
 
-cudaError_t launch_cast_bf16_w1(const Tile* tiles, int ntiles, const float* shard, void* arena, fsdpk::LaunchCfg cfg,
-                                cudaStream_t st) {
+cudaError_t launch_cast_w1(const Tile* tiles, int ntiles, const float* shard, const float* scales, void* arena,
+                           uint32_t* amax_acc, fsdpk::LaunchCfg cfg, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
   constexpr int NS = 3;
   constexpr size_t smem = (size_t)NS * kCastChunk * (4 + 2);   // 36 KB
-  return launch_p(cfg.pdl, k_cast_bf16_w1_tma<NS>, grid_for(ntiles, cfg, fsdpk::kCtasCopy), smem, st, tiles, ntiles,
-                  shard, (uint8_t*)arena);
+  const int g = grid_for(ntiles, cfg, fsdpk::kCtasCopy);
+  uint8_t* a = (uint8_t*)arena;
+  if (amax_acc)
+    return launch_p(cfg.pdl, k_cast_w1_tma<NS, true, true>, g, smem, st, tiles, ntiles, shard, scales, a, amax_acc);
+  if (scales)
+    return launch_p(cfg.pdl, k_cast_w1_tma<NS, true, false>, g, smem, st, tiles, ntiles, shard, scales, a, amax_acc);
+  return launch_p(cfg.pdl, k_cast_w1_tma<NS, false, false>, g, smem, st, tiles, ntiles, shard, scales, a, amax_acc);
 }
 
 cudaError_t launch_amax_max(PeerPtrs src, int W, uint32_t* out, int n, cudaStream_t st) {

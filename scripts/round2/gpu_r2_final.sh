@@ -15,5 +15,5 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref
 B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"^k_" -c 600 --csv \
    --log-file $O/launches_w1.csv $B > $O/ncu_launches.log 2>&1; echo "ncu list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_unshard_push|k_rs_copy_in" -s 40 -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_cast_w1|k_unshard_push|k_rs_copy_in" -s 40 -c 2 \
    -o $O/prof_w1 $B > $O/ncu_full.log 2>&1; echo "ncu full rc=$?"

@@ -491,11 +491,13 @@ __global__ void __launch_bounds__(kThreads) k_amax_max(PeerPtrs src, int W, uint
 // granular take an element path (none in the Llama layouts).  Tile: src = shard element
 // offset, dst = byte offset into the arena, n elements (layout.h tiles_push).
 constexpr uint32_t kCastChunk = 2048;
+// W > 1 (FSDP_B200_VARIANT bit 128): the same kernel stores every output chunk into all W
+// arenas (arena.p rotated per rank on the host), i.e. the push with TMA loads.
 template <int NS, bool kAnyFp8, bool kAmax>
 __global__ void __launch_bounds__(kThreads) k_cast_w1_tma(const Tile* __restrict__ tiles, int ntiles,
                                                            const float* __restrict__ shard,
                                                            const float* __restrict__ scales,
-                                                           uint8_t* __restrict__ arena, uint32_t* __restrict__ acc) {
+                                                           PeerPtrs arena, int W, uint32_t* __restrict__ acc) {
   extern __shared__ __align__(128) uint8_t cast_smem[];   // [NS][chunk * 4] in, [NS][chunk * 2] out
   float (*sin)[kCastChunk] = reinterpret_cast<float (*)[kCastChunk]>(cast_smem);
   uint8_t (*sout)[kCastChunk * 2] = reinterpret_cast<uint8_t (*)[kCastChunk * 2]>(cast_smem + NS * kCastChunk * 4);
@@ -512,7 +514,6 @@ __global__ void __launch_bounds__(kThreads) k_cast_w1_tma(const Tile* __restrict
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile tl = tiles[t];
     const float* s = shard + tl.src;
-    uint8_t* d = arena + tl.dst;
     const uint32_t n = tl.n;
     const bool f8 = kAnyFp8 && tl.kind == fsdpk::TK_FP8;   // CTA-uniform
     const float sc = f8 ? scales[tl.param] : 0.0f;
@@ -521,9 +522,11 @@ __global__ void __launch_bounds__(kThreads) k_cast_w1_tma(const Tile* __restrict
       for (uint32_t e = threadIdx.x; e < n; e += kThreads) {
         if (f8) {
           if constexpr (kAmax) am = max(am, abs_bits(s[e]));
-          d[e] = (uint8_t)(pack_e4m3x2(__fmul_rn(s[e], sc), 0.0f) & 0xFFu);
+          const uint8_t b = (uint8_t)(pack_e4m3x2(__fmul_rn(s[e], sc), 0.0f) & 0xFFu);
+          for (int q = 0; q < W; ++q) arena.p[q][tl.dst + e] = b;
         } else {
-          reinterpret_cast<uint16_t*>(d)[e] = (uint16_t)(pack_bf16x2(s[e], 0.0f) & 0xFFFFu);
+          const uint16_t b = (uint16_t)(pack_bf16x2(s[e], 0.0f) & 0xFFFFu);
+          for (int q = 0; q < W; ++q) reinterpret_cast<uint16_t*>(arena.p[q] + tl.dst)[e] = b;
         }
       }
     } else {
@@ -570,7 +573,11 @@ __global__ void __launch_bounds__(kThreads) k_cast_w1_tma(const Tile* __restrict
         fence_proxy_async_smem();
         __syncthreads();   // sout[st] complete, sin[st] consumed
         if (threadIdx.x == 0) {
-          bulk_s2g(d + (size_t)c * kCastChunk * es, sout[st], ne * es);
+#pragma unroll
+          for (int q = 0; q < kMaxRanks; ++q) {   // constant indices: arena.p stays in param space
+            if (q >= W) break;
+            bulk_s2g(arena.p[q] + tl.dst + (size_t)c * kCastChunk * es, sout[st], ne * es);
+          }
           bulk_commit();
           if (c + NS < nch) issue(c + NS);
         }
@@ -581,7 +588,13 @@ __global__ void __launch_bounds__(kThreads) k_cast_w1_tma(const Tile* __restrict
       if (f8) amax_commit_cta(acc, tl.param, am, red);
     }
   }
-  if (threadIdx.x == 0) bulk_wait0();
+  if (W > 1) {   // the peers' data before the done handshake's signal (W = 1: kernel end suffices)
+    if (threadIdx.x == 0) bulk_wait0();
+    __syncthreads();
+    __threadfence_system();
+  } else if (threadIdx.x == 0) {
+    bulk_wait0();
+  }
 }
 
 // ------------------------------------------------------------------- gather copy
@@ -660,12 +673,17 @@ cudaError_t launch_signal_wait(FlagPtrs remote, unsigned long long* local, int W
   return cudaGetLastError();
 }
 
+static cudaError_t launch_cast_tma(const Tile* tiles, int ntiles, const float* shard, const float* scales,
+                                   const PeerPtrs& a, int W, uint32_t* amax_acc, fsdpk::LaunchCfg cfg, cudaStream_t st);
+
 cudaError_t launch_unshard_push(const Tile* tiles, int ntiles, const float* shard, const float* scales,
                                 PeerPtrs arena, int W, int rank, fsdpk::LaunchCfg cfg, cudaStream_t st,
                                 uint32_t* amax_acc) {
   if (ntiles == 0) return cudaSuccess;
   PeerPtrs rot{};   // destination order starts at the next rank: spreads NVLink traffic
   for (int i = 0; i < W; ++i) rot.p[i] = arena.p[(rank + 1 + i) % W];
+  if (W > 1 && (cfg.variant & 128))   // the TMA-load push (FSDP_B200_VARIANT bit 128)
+    return launch_cast_tma(tiles, ntiles, shard, scales, rot, W, amax_acc, cfg, st);
   const int g = grid_for(ntiles, cfg, fsdpk::kCtasPush);
   if (cfg.variant & 4)   // TMA bulk push
     // the bf16-only double-buffered kernel at W = 1 (HBM-bound: the W=1 8B step 15.21 ->
@@ -690,18 +708,24 @@ cudaError_t launch_rs_pull(const Tile* tiles, int ntiles, PeerPtrs staging, bool
                    : launch_pull_w<false>(tiles, ntiles, staging, grad, ops, W, g, st, cfg.variant, cfg.pdl);
 }
 
-cudaError_t launch_cast_w1(const Tile* tiles, int ntiles, const float* shard, const float* scales, void* arena,
-                           uint32_t* amax_acc, fsdpk::LaunchCfg cfg, cudaStream_t st) {
+static cudaError_t launch_cast_tma(const Tile* tiles, int ntiles, const float* shard, const float* scales,
+                                   const PeerPtrs& a, int W, uint32_t* amax_acc, fsdpk::LaunchCfg cfg, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
   constexpr int NS = 3;
   constexpr size_t smem = (size_t)NS * kCastChunk * (4 + 2);   // 36 KB
   const int g = grid_for(ntiles, cfg, fsdpk::kCtasCopy);
-  uint8_t* a = (uint8_t*)arena;
   if (amax_acc)
-    return launch_p(cfg.pdl, k_cast_w1_tma<NS, true, true>, g, smem, st, tiles, ntiles, shard, scales, a, amax_acc);
+    return launch_p(cfg.pdl, k_cast_w1_tma<NS, true, true>, g, smem, st, tiles, ntiles, shard, scales, a, W, amax_acc);
   if (scales)
-    return launch_p(cfg.pdl, k_cast_w1_tma<NS, true, false>, g, smem, st, tiles, ntiles, shard, scales, a, amax_acc);
-  return launch_p(cfg.pdl, k_cast_w1_tma<NS, false, false>, g, smem, st, tiles, ntiles, shard, scales, a, amax_acc);
+    return launch_p(cfg.pdl, k_cast_w1_tma<NS, true, false>, g, smem, st, tiles, ntiles, shard, scales, a, W, amax_acc);
+  return launch_p(cfg.pdl, k_cast_w1_tma<NS, false, false>, g, smem, st, tiles, ntiles, shard, scales, a, W, amax_acc);
+}
+
+cudaError_t launch_cast_w1(const Tile* tiles, int ntiles, const float* shard, const float* scales, void* arena,
+                           uint32_t* amax_acc, fsdpk::LaunchCfg cfg, cudaStream_t st) {
+  PeerPtrs a{};
+  a.p[0] = (uint8_t*)arena;
+  return launch_cast_tma(tiles, ntiles, shard, scales, a, 1, amax_acc, cfg, st);
 }
 
 cudaError_t launch_amax_max(PeerPtrs src, int W, uint32_t* out, int n, cudaStream_t st) {

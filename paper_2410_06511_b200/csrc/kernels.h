@@ -35,7 +35,7 @@ struct LaunchCfg {
   // kernel-variant bit mask (FSDP_B200_VARIANT, default 78): 1 = 16-byte pull loads, 2 = TMA
   // bulk pull, 4 = TMA bulk push, 8 = TMA bulk RS copy-in (K5), 32 = W=1 bf16 unshard as one
   // contiguous K2 cast when the arena has the flat layout, 64 = W=1 bf16 unshard as the
-  // TMA-in / TMA-out cast (k_cast_w1_tma)
+  // TMA-in / TMA-out cast (k_cast_w1_tma), 128 = the same kernel as the W>1 push (slower)
   int variant = 0;
   // TMA bulk pull: bytes per peer per chunk (power of two, 1-16 KB) and pipeline stages (2-4)
   // (FSDP_B200_PULL_CHUNK / FSDP_B200_PULL_STAGES)

@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(kThreads) k_amax_max(PeerPtrs src, int W, uint
 constexpr uint32_t kCastChunk = 2048;
 // W > 1 (FSDP_B200_VARIANT bit 128): the same kernel stores every output chunk into all W
 // arenas (arena.p rotated per rank on the host), i.e. the push with TMA loads.
-template <int NS, bool kAnyFp8, bool kAmax>
+template <int NS, bool kAnyFp8, bool kAmax, bool kMulti = false>   // kMulti: W > 1 (bit 128)
 __global__ void __launch_bounds__(kThreads) k_cast_w1_tma(const Tile* __restrict__ tiles, int ntiles,
                                                            const float* __restrict__ shard,
                                                            const float* __restrict__ scales,
@@ -523,10 +523,10 @@ __global__ void __launch_bounds__(kThreads) k_cast_w1_tma(const Tile* __restrict
         if (f8) {
           if constexpr (kAmax) am = max(am, abs_bits(s[e]));
           const uint8_t b = (uint8_t)(pack_e4m3x2(__fmul_rn(s[e], sc), 0.0f) & 0xFFu);
-          for (int q = 0; q < W; ++q) arena.p[q][tl.dst + e] = b;
+          for (int q = 0; q < (kMulti ? W : 1); ++q) arena.p[q][tl.dst + e] = b;
         } else {
           const uint16_t b = (uint16_t)(pack_bf16x2(s[e], 0.0f) & 0xFFFFu);
-          for (int q = 0; q < W; ++q) reinterpret_cast<uint16_t*>(arena.p[q] + tl.dst)[e] = b;
+          for (int q = 0; q < (kMulti ? W : 1); ++q) reinterpret_cast<uint16_t*>(arena.p[q] + tl.dst)[e] = b;
         }
       }
     } else {
@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(kThreads) k_cast_w1_tma(const Tile* __restrict
         __syncthreads();   // sout[st] complete, sin[st] consumed
         if (threadIdx.x == 0) {
 #pragma unroll
-          for (int q = 0; q < kMaxRanks; ++q) {   // constant indices: arena.p stays in param space
+          for (int q = 0; q < (kMulti ? kMaxRanks : 1); ++q) {   // constant indices: arena.p in param space
             if (q >= W) break;
             bulk_s2g(arena.p[q] + tl.dst + (size_t)c * kCastChunk * es, sout[st], ne * es);
           }
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(kThreads) k_cast_w1_tma(const Tile* __restrict
       if (f8) amax_commit_cta(acc, tl.param, am, red);
     }
   }
-  if (W > 1) {   // the peers' data before the done handshake's signal (W = 1: kernel end suffices)
+  if (kMulti) {   // the peers' data before the done handshake's signal (W = 1: kernel end suffices)
     if (threadIdx.x == 0) bulk_wait0();
     __syncthreads();
     __threadfence_system();
@@ -714,6 +714,16 @@ static cudaError_t launch_cast_tma(const Tile* tiles, int ntiles, const float* s
   constexpr int NS = 3;
   constexpr size_t smem = (size_t)NS * kCastChunk * (4 + 2);   // 36 KB
   const int g = grid_for(ntiles, cfg, fsdpk::kCtasCopy);
+  if (W > 1) {
+    if (amax_acc)
+      return launch_p(cfg.pdl, k_cast_w1_tma<NS, true, true, true>, g, smem, st, tiles, ntiles, shard, scales, a, W,
+                      amax_acc);
+    if (scales)
+      return launch_p(cfg.pdl, k_cast_w1_tma<NS, true, false, true>, g, smem, st, tiles, ntiles, shard, scales, a, W,
+                      amax_acc);
+    return launch_p(cfg.pdl, k_cast_w1_tma<NS, false, false, true>, g, smem, st, tiles, ntiles, shard, scales, a, W,
+                    amax_acc);
+  }
   if (amax_acc)
     return launch_p(cfg.pdl, k_cast_w1_tma<NS, true, true>, g, smem, st, tiles, ntiles, shard, scales, a, W, amax_acc);
   if (scales)
